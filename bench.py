@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark of the MFA-DVR hot path on B200 (BASELINE.json metric:
+"MFA ray-samples/s (value+gradient) and frames/s at 1/2/4/8 B200; % roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step is one pass of the whole hot path over one batch: mfa_render of every
+view of the workload (Algorithm 1 for every pixel: span, basis + derivatives,
+(p+1)^3 contraction, TF, Phong, compositing, ERT).  Default workload is C5
+(BASELINE.json configs[4], the largest: 64 views of 3840x2160, degree 3,
+1024x256x256 non-uniform model), the configuration north_star's multi-GPU bar
+is stated on; it fits one GPU.  With N GPUs the model is replicated and the
+(view, tile) units are sharded, then gathered with NCCL (strong scaling: the
+batch is fixed).  value = composited ray-samples (all ranks) / max-over-ranks
+time.  --impl reference times the fp64 CPU oracle (the reference arm of this
+tier) on host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MFA ray-samples/s (value+gradient) and frames/s at 1/2/4/8 B200; % roofline"
+UNIT = "ray-samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--views", type=int, default=None, help="override the number of views (tests only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
+    ap.add_argument("--out-fp16", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(rows), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_oracle_sample(w, seconds: float, cfg_idx: int, nthreads=None):
+    """Oracle (as it stands) on a bounded seeded tile sample of view 0; returns
+    (samples/s, cores, description).  Calibrated on a small sample first."""
+    import oracle as O
+    from paper_2204_11762_b200 import workloads as WL
+    om = O.Model.from_workload(w)
+    cam = w.cameras[0]
+    cores = nthreads or O.ncores()
+    frac = 0.002
+    t0 = time.perf_counter()
+    pix = WL.tile_subset(cfg_idx, cam.width, cam.height, frac)[0]
+    r = O.render(om, cam, w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
+    dt = max(time.perf_counter() - t0, 1e-3)
+    frac = min(1.0, frac * max(1.0, seconds / dt))
+    pix = WL.tile_subset(cfg_idx, cam.width, cam.height, frac)[0]
+    t0 = time.perf_counter()
+    r = O.render(om, cam, w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
+    dt = time.perf_counter() - t0
+    ns = int(r["count"].sum())
+    desc = (f"{len(pix)} pixels ({frac * 100:.2f}% of the 16x16 tiles, seeded) of view 0 of {w.name}; "
+            f"{ns} composited samples in {dt:.2f} s")
+    return ns / dt, cores, desc, dt
+
+
+def run_reference(args):
+    """Reference arm: the fp64 oracle on host cores, each step a bounded sample."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+    from paper_2204_11762_b200 import workloads as WL
+    c = int(args.workload[1:])
+    kw = {"n_views": args.views} if args.views else {}
+    w = WL.make_config(c, **kw)
+    om = O.Model.from_workload(w)
+    cores = O.ncores()
+    cam = w.cameras[0]
+    # size each step to ~ (120 s / (steps + warmup)) of CPU work, at least 1 tile
+    budget = min(20.0, 120.0 / max(1, args.steps + args.warmup))
+    frac = 0.001
+    t0 = time.perf_counter()
+    pix = WL.tile_subset(c, cam.width, cam.height, frac)[0]
+    O.render(om, cam, w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
+    dt = max(time.perf_counter() - t0, 1e-3)
+    frac = min(1.0, frac * max(1.0, budget / dt))
+    tot_s = 0
+    tot_t = 0.0
+    for i in range(args.warmup + args.steps):
+        v = i % len(w.cameras)
+        pix = WL.tile_subset(c, cam.width, cam.height, frac, views=(v,))[v]
+        t0 = time.perf_counter()
+        r = O.render(om, w.cameras[v], w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            tot_s += int(r["count"].sum())
+            tot_t += dt
+    val = tot_s / tot_t
+    desc = f"per step a seeded {frac * 100:.3f}% tile sample of one view of {w.name}"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator)", "config": {"workload": w.name},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_11762_b200 import Model, dist as D, roofline as RL, unpack_tiles, workloads as WL
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or world == 1, "launch N>1 with torch.distributed.run"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = int(args.workload[1:])
+    kw = {"n_views": args.views} if args.views else {}
+    w = WL.make_config(c, **kw)
+    V = len(w.cameras)
+    W, H = w.cameras[0].width, w.cameras[0].height
+    stream = torch.cuda.current_stream()
+    m = Model.from_workload(w)
+    info = m.info()
+    tf = torch.from_numpy(w.tf).cuda()
+    out_dt = torch.float16 if args.out_fp16 else torch.float32
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    launches_per_step = 0
+
+    if world == 1:
+        img = torch.empty((V, H, W, 4), dtype=out_dt, device="cuda")
+        launches_per_step = (V + 63) // 64
+
+        def step():
+            m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, out=img, samples=cnt, out_fp16=args.out_fp16)
+    else:
+        lists = D.assign_units(V, W, H, world)
+        mine = torch.from_numpy(lists[rank]).cuda()
+        tiles_all = torch.from_numpy(np.concatenate(lists)).cuda()
+        packed = torch.empty((len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
+        gathered = torch.empty((world * len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
+        img = torch.empty((V, H, W, 4), dtype=torch.float32, device="cuda") if rank == 0 else None
+        launches_per_step = 1 + (1 if rank == 0 else 0)
+
+        def step():
+            m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=mine, out=packed, samples=cnt,
+                     out_fp16=args.out_fp16)
+            dist.all_gather_into_tensor(gathered, packed)
+            if rank == 0:
+                unpack_tiles(gathered, tiles_all, V, W, H, out=img)
+
+    # ---- warm-up, then exactly K timed steps ------------------------------
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    cnt.zero_()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev0.record(stream)
+    for i in range(args.steps):
+        kev[i][0].record(stream)
+        step()
+        kev[i][1].record(stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    kernel_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    samples = int(cnt.item())
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    s = torch.tensor([samples], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+    ms_max = float(t.item())
+    samples_all = int(s.item())
+    value = samples_all / (ms_max / 1e3)
+    ms_per_step = ms_max / args.steps
+
+    # ---- roofline of the dominant kernel (render) --------------------------
+    p = w.degree
+    F = RL.flops_per_sample(p, bool(w.params.shading))
+    per_launch_samples = samples / args.steps / max(1, (V + 63) // 64 if world == 1 else 1)
+    launch_ms = kernel_ms / max(1, (V + 63) // 64 if world == 1 else 1)
+    achieved_tf = F * per_launch_samples / (launch_ms / 1e3) / 1e12
+    peak_tf, peak_src = RL.fp32_peak_tflops()
+    Bs = RL.bytes_per_sample(p)
+    roof = {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": achieved_tf / peak_tf, "traffic": None,
+            "kernel": "render_kernel", "flops_per_sample": F, "samples_per_launch": per_launch_samples,
+            "launch_ms": launch_ms, "peak_source": peak_src,
+            "counted_bytes_per_sample": Bs,
+            "l2_counted_GBps": Bs * per_launch_samples / (launch_ms / 1e3) / 1e9}
+    if clocks.get("sm_mhz"):
+        pk_clk, _ = RL.fp32_peak_tflops(clocks["sm_mhz"])
+        roof["frac_at_observed_clock"] = achieved_tf / pk_clk
+
+    # ---- end to end through the C ABI with host buffers --------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, w, m, world, rank, local, out_dt)
+
+    # ---- CPU baseline (oracle on host cores), rank 0, N = 1 only -----------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, desc, _ = cpu_oracle_sample(w, args.cpu_seconds, c)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generator of the BASELINE.json config recipe; no dataset)",
+            "config": {"workload": w.name, "views": V, "width": W, "height": H, "degree": p,
+                       "nctrl": list(w.nctrl), "uniform_knots": bool(w.uniform), "step_spans": w.step_spans,
+                       "shading": int(w.params.shading), "o_max": w.params.o_max,
+                       "out": "fp16" if args.out_fp16 else "fp32",
+                       "parallelism": f"screen-tile sharding x{world}, model replicated, NCCL all-gather"
+                       if world > 1 else "single GPU",
+                       "l2": f"inputs larger than L2: row-quad grid {info['device_bytes'] / 2**20:.0f} MiB, "
+                             f"image {V * H * W * (8 if args.out_fp16 else 16) / 2**20:.0f} MiB per step"},
+            "frames_per_s": V * args.steps / (ms_max / 1e3),
+            "samples_per_step": samples_all / args.steps,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(res))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, w, m, world, rank, local, out_dt):
+    """Same metric through the public API with HOST buffers: per step the TF
+    table and cameras go host->device and the finished image device->host."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_11762_b200 import dist as D, unpack_tiles
+    V = len(w.cameras)
+    W, H = w.cameras[0].width, w.cameras[0].height
+    K = max(1, min(args.steps, 3))
+    el = 2 if out_dt == torch.float16 else 4
+    cam_bytes = 96 * V
+    tf_bytes = w.tf.nbytes
+    if world == 1:
+        try:
+            host = torch.empty((V, H, W, 4), dtype=out_dt).pin_memory()
+        except RuntimeError:
+            return None
+        m.render_host(w.cameras, w.tf, w.v_lo, w.v_hi, w.params, host, out_fp16=(out_dt == torch.float16))
+        tot = 0
+        t0 = time.perf_counter()
+        for _ in range(K):
+            tot += m.render_host(w.cameras, w.tf, w.v_lo, w.v_hi, w.params, host,
+                                 out_fp16=(out_dt == torch.float16))
+        dt = time.perf_counter() - t0
+        return {"value": tot / dt, "unit": UNIT, "h2d_bytes_per_step": tf_bytes + cam_bytes,
+                "d2h_bytes_per_step": V * H * W * 4 * el + 8, "api": "mfa_render_host (C ABI, host buffers)",
+                "steps": K, "timer": "wall clock around the blocking call"}
+    lists = D.assign_units(V, W, H, world)
+    mine = torch.from_numpy(lists[rank]).cuda()
+    tiles_all = torch.from_numpy(np.concatenate(lists)).cuda()
+    tf_host = torch.from_numpy(w.tf).pin_memory()
+    tf_dev = torch.empty_like(tf_host, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    host = torch.empty((V, H, W, 4), dtype=torch.float32).pin_memory() if rank == 0 else None
+    img = torch.empty((V, H, W, 4), dtype=torch.float32, device="cuda") if rank == 0 else None
+    packed = torch.empty((len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
+    gathered = torch.empty((world * len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
+
+    def step():
+        tf_dev.copy_(tf_host, non_blocking=True)
+        m.render(w.cameras, tf_dev, w.v_lo, w.v_hi, w.params, tiles=mine, out=packed, samples=cnt,
+                 out_fp16=(out_dt == torch.float16))
+        dist.all_gather_into_tensor(gathered, packed)
+        if rank == 0:
+            unpack_tiles(gathered, tiles_all, V, W, H, out=img)
+            host.copy_(img, non_blocking=True)
+    step()
+    torch.cuda.synchronize()
+    cnt.zero_()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(K):
+        step()
+    torch.cuda.synchronize()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    s = cnt.clone()
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    dist.all_reduce(s, op=dist.ReduceOp.SUM)
+    return {"value": int(s.item()) / float(dt.item()), "unit": UNIT, "h2d_bytes_per_step": tf_bytes + cam_bytes,
+            "d2h_bytes_per_step": V * H * W * 16, "api": "Model.render (tiles) + NCCL + unpack, host copies",
+            "steps": K, "timer": "wall clock, max over ranks"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

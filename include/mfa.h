@@ -1,0 +1,206 @@
+/*
+ * mfa.h -- C ABI of the B200-native MFA-DVR hot path (libmfa.so).
+ *
+ * Method: Sun, Lenz, Yu, Peterka, "MFA-DVR: direct volume rendering of MFA
+ * models" (arXiv 2204.11762).  "P:n" = line n of the paper text
+ * (reference PAPER.md), "S:n" = line n of SPEC.md, "R-n" = a reading of the
+ * paper recorded in DESIGN.md §2.  SURVEY.md §8(b) lists these entry points.
+ *
+ * Conventions shared by every call
+ *  - Plain C types only; no C++ or CUDA types cross the boundary.  A stream
+ *    argument is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Every call validates its arguments synchronously, before anything is
+ *    enqueued, and returns a status.  On a non-OK status nothing was enqueued
+ *    and mfa_last_error() returns a message naming the offending argument.
+ *  - Work is asynchronous on the given stream; outputs are valid once the
+ *    stream reaches the enqueued work.  Asynchronous CUDA faults surface as
+ *    MFA_ERR_CUDA on a later call (or at the caller's synchronisation).
+ *  - A model is bound to the CUDA device that was current at create time;
+ *    calls made while another device is current return MFA_ERR_DEVICE.
+ *  - A model is immutable after create: any number of threads and
+ *    streams may call eval / render on it concurrently.  The caller
+ *    guarantees no work is in flight when it calls mfa_model_destroy.
+ *  - The library allocates nothing on the eval / render paths: outputs go to
+ *    caller-owned device buffers.
+ */
+#ifndef MFA_H
+#define MFA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mfa_model_t* mfa_model;
+typedef void* mfa_stream;
+
+typedef enum {
+    MFA_OK = 0,
+    MFA_ERR_INVALID_ARG = 1,  /* NULL pointer, bad size, inconsistent shapes */
+    MFA_ERR_KNOTS = 2,        /* knot vector violates S:24-27 (length, order, clamping, multiplicity) */
+    MFA_ERR_UNSUPPORTED = 3,  /* degree outside {1..5} or unequal per axis; > MFA_MAX_VIEWS handled by splitting */
+    MFA_ERR_DOMAIN = 4,       /* non-finite control value */
+    MFA_ERR_CUDA = 5,         /* a CUDA runtime error (message has the CUDA error string) */
+    MFA_ERR_OOM = 6,          /* device allocation failed */
+    MFA_ERR_DEVICE = 7        /* called with a different current device than the model's */
+} mfa_status;
+
+#define MFA_MAX_DEGREE 5
+
+/* ------------------------------------------------------------------------
+ * mfa_model_create -- ingest an MFA model.
+ *
+ * The model is the tensor-product B-spline of P:74 ("a tensor product of
+ * nonuniform rational B-spline functions ... represented by a set of control
+ * points and knots"), with all weights 1 (R-1) and size proportional to the
+ * number of control points.
+ *
+ * degree[3]   polynomial degree per axis (u, v, w).  This build compiles
+ *             degrees 1..5 and requires degree[0]==degree[1]==degree[2];
+ *             otherwise MFA_ERR_UNSUPPORTED.
+ * nctrl[3]    control-point counts n_u, n_v, n_w; each >= degree+1.
+ * knots[3]    host pointers to fp64 knot vectors, length nctrl[d]+degree+1:
+ *             nondecreasing, clamped (first and last degree+1 entries are 0
+ *             and 1), interior multiplicity <= degree; copied.
+ *             Else MFA_ERR_KNOTS with axis and index in the message.
+ * ctrl        fp32 control values, u fastest: ctrl[(k*n_v + j)*n_u + i]
+ *             (S:115 order); host pointer if ctrl_on_device == 0, else a
+ *             device pointer on the current device; copied (the caller may
+ *             free it when the call returns).  Non-finite -> MFA_ERR_DOMAIN.
+ * stream      stream for the device-side ingest; the call synchronises it
+ *             before returning.
+ * out         receives the model handle (NULL on failure).
+ *
+ * Device memory: 4*(4 n_u n_v n_w) bytes for the row-quad layout (DESIGN.md
+ * §5) plus per-axis span tables (< 1 MB).
+ * ---------------------------------------------------------------------- */
+mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3],
+                            const double* const knots[3], const float* ctrl,
+                            int32_t ctrl_on_device, mfa_stream stream, mfa_model* out);
+
+typedef struct {
+    int32_t degree[3];
+    int64_t nctrl[3];
+    int32_t uniform[3];     /* 1 if the interior knots are exactly k/S */
+    float v_min, v_max;     /* min / max control value (a TF domain default) */
+    int64_t device_bytes;   /* device memory owned by the model */
+    int32_t device;         /* CUDA ordinal the model lives on */
+} mfa_model_desc;
+
+mfa_status mfa_model_info(mfa_model m, mfa_model_desc* out);
+
+/* Frees the model's device memory.  NULL is accepted (no-op). */
+mfa_status mfa_model_destroy(mfa_model m);
+
+/* ------------------------------------------------------------------------
+ * mfa_eval_batch -- queryValueMFA / queryGradientMFA for n points
+ * (Algorithm 1 lines 6 and 9; "computing all derivatives along
+ * the three dimensions at once").
+ *
+ * u, v, w     device fp32 arrays (SoA) of n parameter-space points in [0,1]^3.
+ * value       device fp32 output, n entries (required).
+ * du, dv, dw  device fp32 outputs: the PARAMETER-space partials dF/du, dF/dv,
+ *             dF/dw (R-4).  All three NULL -> value only (no
+ *             derivative work); otherwise all three must be non-NULL.
+ * n_domain_errors  optional device counter (unsigned long long); incremented
+ *             by the number of points outside [0,1]^3 or NaN.  Those points
+ *             get NaN outputs (batched form of S:74's domain error, R-18).
+ * n == 0 is valid and enqueues nothing.
+ * ---------------------------------------------------------------------- */
+mfa_status mfa_eval_batch(mfa_model m, int64_t n, const float* u, const float* v, const float* w,
+                          float* value, float* du, float* dv, float* dw,
+                          unsigned long long* n_domain_errors, mfa_stream stream);
+
+/* ------------------------------------------------------------------------
+ * mfa_render -- Algorithm 1 for every pixel of n_views views.
+ *
+ * Per pixel: a ray through the pixel centre (R-14 camera), clipped to
+ * the box (l.2-3), samples at t_in + (k+1/2)*step (constant
+ * distance; R-7), normalised to [0,1]^3 (l.5), value and
+ * gradient queried (l.6, l.9), transfer function (l.7), Phong shading with a
+ * headlight (l.10-11; R-11), front-to-back compositing (l.13) and early ray
+ * termination when A > o_max (l.14-15; R-13).  Output is premultiplied RGBA
+ * (C_r, C_g, C_b, A), background (0,0,0,0) (l.18; R-12).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    double eye[3], look_at[3], up[3];
+    double fov_y_deg;          /* > 0 perspective vertical field of view; 0 -> orthographic */
+    double ortho_half_height;  /* half height of the orthographic viewport (world units) */
+    int32_t width, height;     /* pixels; all views of one call share width and height */
+} mfa_camera;
+
+typedef struct {
+    const float* rgba;         /* device, n_entries x {r,g,b,a}, non-premultiplied */
+    int32_t n_entries;         /* 2 .. 1024 */
+    float v_lo, v_hi;          /* value domain mapped onto the table (v_hi > v_lo) */
+} mfa_tf;
+
+typedef struct {
+    double box_min[3], box_max[3];   /* world placement of the parameter cube */
+    double step;                     /* sample distance, world units (> 0) */
+    double o_max;                    /* ERT threshold O_Max (l.14); >= 1 disables ERT */
+    int32_t shading;                 /* ShadingOn (l.8) */
+    double ka, kd, ks, shininess;    /* Phong constants */
+    double grad_eps;                 /* |physical gradient| <= grad_eps -> ambient only (R-11) */
+    int32_t out_fp16;                /* 0: fp32 RGBA (16 B/px); 1: fp16 RGBA (8 B/px) */
+} mfa_render_params;
+
+#define MFA_TILE 16
+
+typedef struct {
+    int64_t n_tiles;
+    const int32_t* tiles;      /* device, n_tiles x {view, tile_x, tile_y}, 16x16-pixel tiles */
+} mfa_tiles;
+
+/*
+ * cams        HOST array of n_views cameras (copied into the launch).
+ * tf, prm     host structs (tf->rgba is a device pointer).
+ * tiles       NULL: render every pixel; rgba_out is [n_views][H][W][4].
+ *             non-NULL: render only the listed 16x16 tiles; rgba_out is the
+ *             packed buffer [n_tiles][16][16][4] (pixels outside the image are
+ *             left untouched).  Used for screen-tile sharding across GPUs.
+ * rgba_out    device buffer, fp32 or fp16 per prm->out_fp16.
+ * samples_out optional device counter: += the number of composited samples
+ *             (each sample up to and including the ERT sample).
+ * Deterministic: a pixel's value does not depend on tiling, view batching or
+ * launch configuration.
+ */
+mfa_status mfa_render(mfa_model m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
+                      const mfa_render_params* prm, const mfa_tiles* tiles, void* rgba_out,
+                      unsigned long long* samples_out, mfa_stream stream);
+
+/*
+ * mfa_render_host -- the same frame(s) as mfa_render (tiles == NULL), with
+ * HOST buffers: tf_rgba_host (n_entries x 4 fp32) is copied in, and the image
+ * [n_views][H][W][4] (fp32 or fp16 per prm->out_fp16) is written to
+ * rgba_host, view by view, with the device->host copy of view v overlapping
+ * the rendering of view v+1 (two device staging buffers, two streams).
+ * rgba_host should be page-locked for the copies to overlap.  samples_host
+ * (optional) receives the composited-sample count.  Returns after the image
+ * is on the host.
+ */
+mfa_status mfa_render_host(mfa_model m, int32_t n_views, const mfa_camera* cams,
+                           const float* tf_rgba_host, int32_t tf_n_entries, float v_lo, float v_hi,
+                           const mfa_render_params* prm, void* rgba_host,
+                           unsigned long long* samples_host, mfa_stream stream);
+
+/*
+ * mfa_unpack_tiles -- scatter a packed tile buffer [n_tiles][16][16][4] (as
+ * written by mfa_render with tiles) into images [n_views][H][W][4] (fp32).
+ * in_fp16 selects the packed element type.  Device pointers.
+ */
+mfa_status mfa_unpack_tiles(const void* packed, int32_t in_fp16, const int32_t* tiles, int64_t n_tiles,
+                            int32_t n_views, int32_t width, int32_t height, float* image_out,
+                            mfa_stream stream);
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char* mfa_last_error(void);
+
+/* Library version string, e.g. "mfa-b200 0.1 sm_100a". */
+const char* mfa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFA_H */

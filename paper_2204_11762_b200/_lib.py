@@ -1,0 +1,259 @@
+"""Thin Python binding of libmfa.so (include/mfa.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; PyTorch is
+used for device memory and streams.  There is no fallback: if libmfa.so is
+missing or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmfa.so")
+
+MFA_OK = 0
+STATUS = {0: "MFA_OK", 1: "MFA_ERR_INVALID_ARG", 2: "MFA_ERR_KNOTS", 3: "MFA_ERR_UNSUPPORTED",
+          4: "MFA_ERR_DOMAIN", 5: "MFA_ERR_CUDA", 6: "MFA_ERR_OOM", 7: "MFA_ERR_DEVICE"}
+TILE = 16
+
+# C-ABI symbols declared in include/mfa.h (checked by tests/test_abi.py)
+EXPORTS = ("mfa_model_create", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
+           "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version")
+
+
+class MfaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Camera_t(C.Structure):
+    _fields_ = [("eye", C.c_double * 3), ("look_at", C.c_double * 3), ("up", C.c_double * 3),
+                ("fov_y_deg", C.c_double), ("ortho_half_height", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class TF_t(C.Structure):
+    _fields_ = [("rgba", C.c_void_p), ("n_entries", C.c_int32), ("v_lo", C.c_float), ("v_hi", C.c_float)]
+
+
+class RenderParams_t(C.Structure):
+    _fields_ = [("box_min", C.c_double * 3), ("box_max", C.c_double * 3), ("step", C.c_double),
+                ("o_max", C.c_double), ("shading", C.c_int32), ("ka", C.c_double), ("kd", C.c_double),
+                ("ks", C.c_double), ("shininess", C.c_double), ("grad_eps", C.c_double),
+                ("out_fp16", C.c_int32)]
+
+
+class Tiles_t(C.Structure):
+    _fields_ = [("n_tiles", C.c_int64), ("tiles", C.c_void_p)]
+
+
+class ModelDesc_t(C.Structure):
+    _fields_ = [("degree", C.c_int32 * 3), ("nctrl", C.c_int64 * 3), ("uniform", C.c_int32 * 3),
+                ("v_min", C.c_float), ("v_max", C.c_float), ("device_bytes", C.c_int64),
+                ("device", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libmfa.so (raises if it is missing -- no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2204_11762_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.mfa_model_create.restype = C.c_int
+        L.mfa_model_create.argtypes = [C.POINTER(i32), C.POINTER(i64), C.POINTER(C.POINTER(C.c_double)), vp, i32,
+                                       vp, C.POINTER(vp)]
+        L.mfa_model_info.restype = C.c_int
+        L.mfa_model_info.argtypes = [vp, C.POINTER(ModelDesc_t)]
+        L.mfa_model_destroy.restype = C.c_int
+        L.mfa_model_destroy.argtypes = [vp]
+        L.mfa_eval_batch.restype = C.c_int
+        L.mfa_eval_batch.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.mfa_render.restype = C.c_int
+        L.mfa_render.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
+                                 C.POINTER(Tiles_t), vp, vp, vp]
+        L.mfa_render_host.restype = C.c_int
+        L.mfa_render_host.argtypes = [vp, i32, C.POINTER(Camera_t), vp, i32, C.c_float, C.c_float,
+                                      C.POINTER(RenderParams_t), vp, vp, vp]
+        L.mfa_unpack_tiles.restype = C.c_int
+        L.mfa_unpack_tiles.argtypes = [vp, i32, vp, i64, i32, i32, i32, vp, vp]
+        L.mfa_last_error.restype = C.c_char_p
+        L.mfa_last_error.argtypes = []
+        L.mfa_version.restype = C.c_char_p
+        L.mfa_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != MFA_OK:
+        raise MfaError(st, lib().mfa_last_error().decode())
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def cameras_t(cams):
+    arr = (Camera_t * len(cams))()
+    for i, c in enumerate(cams):
+        for k in range(3):
+            arr[i].eye[k] = c.eye[k]
+            arr[i].look_at[k] = c.look_at[k]
+            arr[i].up[k] = c.up[k]
+        arr[i].fov_y_deg = c.fov_y_deg
+        arr[i].ortho_half_height = c.ortho_half_height
+        arr[i].width = c.width
+        arr[i].height = c.height
+    return arr
+
+
+def params_t(p, out_fp16=False):
+    r = RenderParams_t()
+    for k in range(3):
+        r.box_min[k] = p.box_min[k]
+        r.box_max[k] = p.box_max[k]
+    r.step = p.step
+    r.o_max = p.o_max
+    r.shading = int(p.shading)
+    r.ka, r.kd, r.ks, r.shininess = p.ka, p.kd, p.ks, p.shininess
+    r.grad_eps = p.grad_eps
+    r.out_fp16 = int(bool(out_fp16))
+    return r
+
+
+class Model:
+    """An MFA model resident on the current CUDA device (mfa_model_create)."""
+
+    def __init__(self, degree, knots, ctrl, stream=None):
+        import torch
+        if np.isscalar(degree):
+            degree = (int(degree),) * 3
+        self._h = C.c_void_p(0)
+        L = lib()
+        deg = (C.c_int32 * 3)(*[int(x) for x in degree])
+        if isinstance(ctrl, torch.Tensor):
+            assert ctrl.dim() == 3
+            nw, nv, nu = ctrl.shape
+            on_dev = int(ctrl.is_cuda)
+            ctrl_c = ctrl.contiguous().float()
+            cptr = C.c_void_p(ctrl_c.data_ptr())
+        else:
+            ctrl_c = np.ascontiguousarray(ctrl, dtype=np.float32)
+            nw, nv, nu = ctrl_c.shape
+            on_dev = 0
+            cptr = C.c_void_p(ctrl_c.ctypes.data)
+        n = (C.c_int64 * 3)(nu, nv, nw)
+        self._knots = [np.ascontiguousarray(k, dtype=np.float64) for k in knots]
+        kp = (C.POINTER(C.c_double) * 3)(*[k.ctypes.data_as(C.POINTER(C.c_double)) for k in self._knots])
+        h = C.c_void_p(0)
+        _check(L.mfa_model_create(deg, n, kp, cptr, on_dev, _stream_ptr(stream), C.byref(h)))
+        self._h = h
+        self.degree = tuple(int(x) for x in degree)
+        self.nctrl = (nu, nv, nw)
+
+    @classmethod
+    def from_workload(cls, w, stream=None):
+        return cls(w.degree, w.knots, w.ctrl, stream=stream)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> dict:
+        d = ModelDesc_t()
+        _check(lib().mfa_model_info(self._h, C.byref(d)))
+        return dict(degree=tuple(d.degree), nctrl=tuple(d.nctrl), uniform=tuple(d.uniform),
+                    v_min=d.v_min, v_max=d.v_max, device_bytes=d.device_bytes, device=d.device)
+
+    def close(self):
+        if self._h and self._h.value:
+            lib().mfa_model_destroy(self._h)
+            self._h = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- queryValueMFA / queryGradientMFA (mfa_eval_batch) --------------------
+    def eval(self, u, v, w, grad=True, out=None, n_domain_errors=None, stream=None):
+        """u, v, w: CUDA fp32 tensors (n,).  Returns (value, du, dv, dw)
+        (parameter-space partials), or (value,) if grad is False."""
+        import torch
+        n = u.numel()
+        dev = u.device
+        if out is None:
+            out = tuple(torch.empty(n, device=dev, dtype=torch.float32) for _ in range(4 if grad else 1))
+        val = out[0]
+        du, dv, dw = (out[1], out[2], out[3]) if grad else (None, None, None)
+        _check(lib().mfa_eval_batch(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(du), _ptr(dv),
+                                    _ptr(dw), _ptr(n_domain_errors), _stream_ptr(stream)))
+        return out
+
+    # -- Algorithm 1 (mfa_render) ---------------------------------------------
+    def render(self, cams, tf, v_lo, v_hi, params, tiles=None, out=None, samples=None, out_fp16=False,
+               stream=None):
+        """cams: list of Camera; tf: CUDA fp32 tensor (n,4); params: RenderParams.
+        Returns the image [V,H,W,4] (or packed tiles [T,16,16,4] if tiles given)."""
+        import torch
+        tf = tf.contiguous()
+        tft = TF_t(C.c_void_p(tf.data_ptr()), tf.shape[0], float(v_lo), float(v_hi))
+        ca = cameras_t(cams)
+        pr = params_t(params, out_fp16)
+        dt = torch.float16 if out_fp16 else torch.float32
+        W, H = cams[0].width, cams[0].height
+        tl = None
+        if tiles is not None:
+            tl = Tiles_t(tiles.shape[0], C.c_void_p(tiles.data_ptr()))
+            shape = (tiles.shape[0], TILE, TILE, 4)
+        else:
+            shape = (len(cams), H, W, 4)
+        if out is None:
+            out = torch.empty(shape, device=tf.device, dtype=dt)
+        _check(lib().mfa_render(self._h, len(cams), ca, C.byref(tft), C.byref(pr),
+                                C.byref(tl) if tl is not None else None, _ptr(out), _ptr(samples),
+                                _stream_ptr(stream)))
+        return out
+
+    def render_host(self, cams, tf_host: np.ndarray, v_lo, v_hi, params, out_host, out_fp16=False,
+                    stream=None) -> int:
+        """Host-buffer render (mfa_render_host): tf from host memory, image
+        written to out_host (pinned CPU tensor [V,H,W,4]).  Returns the
+        composited-sample count."""
+        tfh = np.ascontiguousarray(tf_host, dtype=np.float32)
+        cnt = C.c_ulonglong(0)
+        _check(lib().mfa_render_host(self._h, len(cams), cameras_t(cams), C.c_void_p(tfh.ctypes.data),
+                                     tfh.shape[0], float(v_lo), float(v_hi), C.byref(params_t(params, out_fp16)),
+                                     C.c_void_p(out_host.data_ptr()), C.byref(cnt), _stream_ptr(stream)))
+        return int(cnt.value)
+
+
+def unpack_tiles(packed, tiles, n_views, width, height, out=None, stream=None):
+    """Scatter packed [T,16,16,4] tiles into [V,H,W,4] fp32 images (mfa_unpack_tiles)."""
+    import torch
+    if out is None:
+        out = torch.zeros((n_views, height, width, 4), device=packed.device, dtype=torch.float32)
+    _check(lib().mfa_unpack_tiles(_ptr(packed), int(packed.dtype == torch.float16), _ptr(tiles), tiles.shape[0],
+                                  n_views, width, height, _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def version() -> str:
+    return lib().mfa_version().decode()

@@ -1,0 +1,126 @@
+// mfa_eval_batch kernel: per point a4 span -> a5 basis +
+// derivatives -> a6 gather -> a7 contraction; value and parameter-space
+// gradient (Algorithm 1 lines 6 and 9; "all derivatives
+// along the three dimensions at once").  One point per thread, grid-stride,
+// grid = a multiple of the SM count.
+#include "kernels.cuh"
+
+namespace mfa {
+
+struct EvalArgs {
+    const float4* Q;
+    int nu, nv, nw;
+    AxisArgs ax[3];
+    const float* u;
+    const float* v;
+    const float* w;
+    float* value;
+    float* du;
+    float* dv;
+    float* dw;
+    unsigned long long* n_err;
+    int64_t n;
+};
+
+template <int P, bool UNI, bool GRAD>
+__global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalArgs args) {
+    const int row_v = args.nu, row_w = args.nu * args.nv;
+    unsigned errs = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < args.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float q[3] = {__ldg(args.u + i), __ldg(args.v + i), __ldg(args.w + i)};
+        if (!(q[0] >= 0.f && q[0] <= 1.f && q[1] >= 0.f && q[1] <= 1.f && q[2] >= 0.f && q[2] <= 1.f)) {
+            ++errs;
+            args.value[i] = __int_as_float(0x7fc00000);
+            if (GRAD) {
+                args.du[i] = __int_as_float(0x7fc00000);
+                args.dv[i] = __int_as_float(0x7fc00000);
+                args.dw[i] = __int_as_float(0x7fc00000);
+            }
+            continue;
+        }
+        int s[3];
+        float t[3], sc[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            if (UNI) {
+                uni_span_f32(q[d], args.ax[d].S, args.ax[d].nsp, s[d], t[d]);
+                sc[d] = args.ax[d].S;
+            } else {
+                nonuni_span_f32(args.ax[d], q[d], s[d], t[d], sc[d]);
+            }
+        }
+        const float4* base = args.Q + ((int64_t)s[2] * args.nv + s[1]) * args.nu + s[0];
+        if (GRAD) {
+            float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+            axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], sc[0], Bu);
+            axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], sc[1], Bv);
+            axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], sc[2], Bw);
+            float val, gu, gv, gw;
+            contract_vg<P>(base, row_v, row_w, Bu, Bv, Bw, val, gu, gv, gw);
+            args.value[i] = val;
+            args.du[i] = gu;
+            args.dv[i] = gv;
+            args.dw[i] = gw;
+        } else {
+            float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+            axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+            axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+            axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+            args.value[i] = contract_v<P>(base, row_v, row_w, Nu, Nv, Nw);
+        }
+    }
+    if (args.n_err) {
+        for (int o = 16; o > 0; o >>= 1) errs += __shfl_xor_sync(0xffffffffu, errs, o);
+        if ((threadIdx.x & 31) == 0 && errs) atomicAdd(args.n_err, (unsigned long long)errs);
+    }
+}
+
+template <int P, bool UNI, bool GRAD>
+static cudaError_t launch_eval_t(const EvalArgs& a, cudaStream_t st) {
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (a.n + 255) / 256;
+    const int64_t grid = std::min<int64_t>(want, (int64_t)sms * 16);
+    eval_kernel<P, UNI, GRAD><<<(unsigned)grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int P>
+static cudaError_t dispatch_eval(const EvalArgs& a, bool uni, bool grad, cudaStream_t st) {
+    if (uni) return grad ? launch_eval_t<P, true, true>(a, st) : launch_eval_t<P, true, false>(a, st);
+    return grad ? launch_eval_t<P, false, true>(a, st) : launch_eval_t<P, false, false>(a, st);
+}
+
+mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v, const float* w, float* value,
+                       float* du, float* dv, float* dw, unsigned long long* n_err, cudaStream_t st) {
+    EvalArgs a;
+    a.Q = m->Q;
+    a.nu = (int)m->n[0];
+    a.nv = (int)m->n[1];
+    a.nw = (int)m->n[2];
+    for (int d = 0; d < 3; ++d) a.ax[d] = make_axis_args(m->ax[d]);
+    a.u = u;
+    a.v = v;
+    a.w = w;
+    a.value = value;
+    a.du = du;
+    a.dv = dv;
+    a.dw = dw;
+    a.n_err = n_err;
+    a.n = n;
+    const bool uni = m->uniform[0] && m->uniform[1] && m->uniform[2];
+    const bool grad = du != nullptr;
+    cudaError_t e;
+    switch (m->p) {
+        case 1: e = dispatch_eval<1>(a, uni, grad, st); break;
+        case 2: e = dispatch_eval<2>(a, uni, grad, st); break;
+        case 3: e = dispatch_eval<3>(a, uni, grad, st); break;
+        case 4: e = dispatch_eval<4>(a, uni, grad, st); break;
+        default: e = dispatch_eval<5>(a, uni, grad, st); break;
+    }
+    return e == cudaSuccess ? MFA_OK : cuda_fail(e, "eval launch");
+}
+
+}  // namespace mfa

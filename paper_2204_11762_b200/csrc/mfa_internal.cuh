@@ -1,0 +1,78 @@
+// Internal declarations of libmfa (not part of the C ABI).
+//
+// Device layout of a model:
+//   Q        float4[n_w][n_v][n_u]: Q[k][j][i] = (P[k][j][i], P[k][j][i+1],
+//            P[k][j][i+2], P[k][j][i+3]) with zeros past n_u-1.  One aligned
+//            16-byte load fetches the p+1 <= 4 consecutive u-values of a row of
+//            the (p+1)^3 neighbourhood at any starting index ("row quads").
+//   per axis span tables (span s = knot interval [U[p+s], U[p+s+1]]):
+//     coef   float[nsp][REC]: power-basis coefficients of the p+1 non-zero
+//            basis functions on span s in the local coordinate
+//            t = (u - U[p+s]) / h_s in [0,1]:  N_{s+a}(t) = sum_m coef[a][m] t^m
+//     invh   float[nsp]  1/h_s (0 for zero-length spans)
+//     kh,kl  float[nsp+1] knots U[p..n] as an fp32 pair (kh + kl == U exactly
+//            up to 2^-48 relative)
+//     kfx    int64[nsp+1] knots U[p..n] in fixed point, 2^62 per unit
+//     bucket int32[M]   bucket b covers [b/M, (b+1)/M): the last span whose
+//            left knot is <= b/M (start of a short linear search)
+//   interior (uniform axes): coefficients of the first interior span, passed
+//            as kernel parameters so the FMAs read them from the constant bank.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/mfa.h"
+
+namespace mfa {
+
+constexpr int kMaxP = MFA_MAX_DEGREE;
+constexpr int kMaxViewsPerLaunch = 64;
+constexpr int kUniFracBits = 40;   // uniform axes: span-unit fixed point, 24.40
+constexpr int kNonUniFracBits = 62; // non-uniform axes: parameter fixed point, 2.62
+
+__host__ __device__ constexpr int rec_floats(int p) { return (((p + 1) * (p + 1)) + 3) / 4 * 4; }
+
+struct AxisTables {
+    const float* coef = nullptr;      // [nsp][rec_floats(p)]
+    const float* invh = nullptr;      // [nsp]
+    const float* kh = nullptr;        // [nsp+1]
+    const float* kl = nullptr;        // [nsp+1]
+    const long long* kfx = nullptr;   // [nsp+1]
+    const int* bucket = nullptr;      // [M]
+    int nsp = 0;                      // n - p (number of knot spans incl. zero-length)
+    int M = 0;                        // bucket count
+    int ic_lo = 0, ic_hi = -1;        // uniform: spans [ic_lo, ic_hi] use the interior constants
+    int uniform = 0;
+    float S = 0.f;                    // uniform: number of spans as float
+    float interior[(kMaxP + 1) * (kMaxP + 1)] = {};  // uniform interior span coefficients
+};
+
+struct Model {
+    int device = 0;
+    int p = 0;
+    int64_t n[3] = {0, 0, 0};
+    int uniform[3] = {0, 0, 0};
+    float vmin = 0.f, vmax = 0.f;
+    float4* Q = nullptr;
+    AxisTables ax[3];
+    void* table_mem = nullptr;   // one allocation for all axis tables
+    int64_t device_bytes = 0;
+};
+
+// error plumbing
+void set_error(const std::string& msg);
+mfa_status fail(mfa_status st, const std::string& msg);
+mfa_status cuda_fail(cudaError_t e, const char* what);
+mfa_status check_device(const Model* m);
+
+// kernel launchers (defined in eval.cu / render.cu)
+mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v, const float* w,
+                       float* value, float* du, float* dv, float* dw,
+                       unsigned long long* n_err, cudaStream_t st);
+mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
+                         const mfa_render_params* prm, const mfa_tiles* tiles, void* out,
+                         unsigned long long* samples, cudaStream_t st);
+
+}  // namespace mfa

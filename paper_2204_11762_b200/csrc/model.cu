@@ -1,0 +1,557 @@
+// libmfa: model ingest, error plumbing, tile unpack (K4)
+// and the host-buffer render driver.
+//
+// mfa_model_create validates the knot vectors, copies the fp32
+// control grid, and builds on the device
+//   * the row-quad layout Q (K1 relayout kernel),
+//   * per-axis span tables: the power-basis coefficients of the p+1 non-zero
+//     basis functions on every knot span, derived from the Cox-de Boor
+//     recursion in fp64 and stored in fp32, plus knot tables
+//     for span search (fp32 pairs, 2^62 fixed point, buckets),
+//   * the value range [min P, max P] and a finiteness check.
+#include <cuda_fp16.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "mfa_internal.cuh"
+
+namespace mfa {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+mfa_status fail(mfa_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+mfa_status cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return e == cudaErrorMemoryAllocation ? MFA_ERR_OOM : MFA_ERR_CUDA;
+}
+
+mfa_status check_device(const Model* m) {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev != m->device)
+        return fail(MFA_ERR_DEVICE, "model lives on device " + std::to_string(m->device) +
+                                        " but device " + std::to_string(dev) + " is current");
+    return MFA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K1: row-quad relayout.  Q[k][j][i] = (P[i], P[i+1], P[i+2], P[i+3]) of row (k,j).
+// ---------------------------------------------------------------------------
+__global__ void relayout_quads_kernel(const float* __restrict__ P, float4* __restrict__ Q, int64_t nu,
+                                      int64_t rows) {
+    const int64_t total = nu * rows;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx % nu;
+        const float* r = P + (idx - i);
+        float4 q;
+        q.x = r[i];
+        q.y = (i + 1 < nu) ? r[i + 1] : 0.f;
+        q.z = (i + 2 < nu) ? r[i + 2] : 0.f;
+        q.w = (i + 3 < nu) ? r[i + 3] : 0.f;
+        Q[idx] = q;
+    }
+}
+
+// Order-preserving float <-> uint mapping for atomic min/max.
+__device__ __forceinline__ unsigned int f2ord(float f) {
+    unsigned int u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+static inline float ord2f(unsigned int u) {
+    unsigned int b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+    float f;
+    memcpy(&f, &b, 4);
+    return f;
+}
+
+__global__ void minmax_kernel(const float* __restrict__ P, int64_t n, unsigned int* out /*min,max,nonfinite*/) {
+    unsigned int lo = 0xffffffffu, hi = 0u, bad = 0u;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float x = P[i];
+        if (!isfinite(x)) { bad++; continue; }
+        unsigned int o = f2ord(x);
+        lo = min(lo, o);
+        hi = max(hi, o);
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, s));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, s));
+        bad += __shfl_xor_sync(0xffffffffu, bad, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out + 0, lo);
+        atomicMax(out + 1, hi);
+        if (bad) atomicAdd(out + 2, bad);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K0: span tables.  One thread per knot span s (knot index i = p + s).
+// The p+1 non-zero basis functions on [U_i, U_{i+1}) are polynomials in the
+// local coordinate t = (u - U_i)/h.  They follow from the Cox-de Boor
+// recursion  N_{j,k} = (u-U_j)/(U_{j+k}-U_j) N_{j,k-1}
+//                    + (U_{j+k+1}-u)/(U_{j+k+1}-U_{j+1}) N_{j+1,k-1}
+// applied to polynomials in t (u = U_i + h t), in fp64.
+// ---------------------------------------------------------------------------
+__global__ void span_tables_kernel(const double* __restrict__ U, int p, int nsp, int rec,
+                                   float* __restrict__ coef, float* __restrict__ invh) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nsp) return;
+    const int i = p + s;
+    const double Ui = U[i], h = U[i + 1] - U[i];
+    float* out = coef + (int64_t)s * rec;
+    for (int q = 0; q < rec; ++q) out[q] = 0.f;
+    if (!(h > 0.0)) {
+        invh[s] = 0.f;
+        return;
+    }
+    invh[s] = (float)(1.0 / h);
+    double P[kMaxP + 1][kMaxP + 1];  // P[r][m]: function r of the current level, coefficient of t^m
+    double Nx[kMaxP + 1][kMaxP + 1];
+    for (int r = 0; r <= kMaxP; ++r)
+        for (int m = 0; m <= kMaxP; ++m) P[r][m] = 0.0;
+    P[0][0] = 1.0;  // level 0: N_{i,0} = 1 on the span
+    for (int k = 1; k <= p; ++k) {
+        for (int r = 0; r <= k; ++r) {
+            for (int m = 0; m <= kMaxP; ++m) Nx[r][m] = 0.0;
+            const int j = i - k + r;
+            if (r >= 1) {  // (u - U_j)/(U_{j+k} - U_j) * N_{j,k-1}; N_{j,k-1} is old function r-1
+                const double den = U[j + k] - U[j];
+                const double c0 = (Ui - U[j]) / den, c1 = h / den;
+                for (int m = 0; m < k; ++m) {
+                    Nx[r][m] += c0 * P[r - 1][m];
+                    Nx[r][m + 1] += c1 * P[r - 1][m];
+                }
+            }
+            if (r <= k - 1) {  // (U_{j+k+1} - u)/(U_{j+k+1} - U_{j+1}) * N_{j+1,k-1}; old function r
+                const double den = U[j + k + 1] - U[j + 1];
+                const double c0 = (U[j + k + 1] - Ui) / den, c1 = -h / den;
+                for (int m = 0; m < k; ++m) {
+                    Nx[r][m] += c0 * P[r][m];
+                    Nx[r][m + 1] += c1 * P[r][m];
+                }
+            }
+        }
+        for (int r = 0; r <= k; ++r)
+            for (int m = 0; m <= kMaxP; ++m) P[r][m] = Nx[r][m];
+    }
+    for (int a = 0; a <= p; ++a)
+        for (int m = 0; m <= p; ++m) out[a * (p + 1) + m] = (float)P[a][m];
+}
+
+__global__ void knot_tables_kernel(const double* __restrict__ U, int p, int nsp, float* __restrict__ kh,
+                                   float* __restrict__ kl, long long* __restrict__ kfx, int M,
+                                   int* __restrict__ bucket) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t <= nsp) {
+        const double u = U[p + t];
+        const float hi = (float)u;
+        kh[t] = hi;
+        kl[t] = (float)(u - (double)hi);
+        kfx[t] = llrint(ldexp(u, kNonUniFracBits));
+    }
+    if (t < M) {
+        // last span s in [0, nsp-1] with U[p+s] <= t/M
+        const double x = (double)t / (double)M;
+        int lo = 0, hi = nsp - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (U[p + mid] <= x) lo = mid; else hi = mid - 1;
+        }
+        bucket[t] = lo;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: scatter packed 16x16 tiles into images.
+// ---------------------------------------------------------------------------
+__global__ void unpack_tiles_kernel(const void* __restrict__ packed, int in_fp16, const int* __restrict__ tiles,
+                                    int64_t n_tiles, int W, int H, float4* __restrict__ img) {
+    const int64_t t = blockIdx.x;
+    if (t >= n_tiles) return;
+    const int view = tiles[3 * t], tx = tiles[3 * t + 1], ty = tiles[3 * t + 2];
+    if (view < 0) return;  // padding unit
+    const int px = threadIdx.x & 15, py = threadIdx.x >> 4;
+    const int x = tx * MFA_TILE + px, y = ty * MFA_TILE + py;
+    if (x >= W || y >= H) return;
+    const int64_t src = t * (MFA_TILE * MFA_TILE) + threadIdx.x;
+    float4 v;
+    if (in_fp16) {
+        const __half2* p = reinterpret_cast<const __half2*>(packed) + 2 * src;
+        float2 a = __half22float2(p[0]), b = __half22float2(p[1]);
+        v = make_float4(a.x, a.y, b.x, b.y);
+    } else {
+        v = reinterpret_cast<const float4*>(packed)[src];
+    }
+    img[((int64_t)view * H + y) * W + x] = v;
+}
+
+}  // namespace mfa
+
+using namespace mfa;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" const char* mfa_last_error(void) { return g_err.c_str(); }
+
+extern "C" const char* mfa_version(void) { return "mfa-b200 0.1 sm_100a"; }
+
+static mfa_status validate_knots(int d, int p, int64_t n, const double* U, int* uniform) {
+    const char* ax = d == 0 ? "u" : (d == 1 ? "v" : "w");
+    const int64_t len = n + p + 1;
+    for (int64_t i = 0; i < len; ++i)
+        if (!isfinite(U[i]))
+            return fail(MFA_ERR_KNOTS, std::string("knots[") + ax + "][" + std::to_string(i) + "] is not finite");
+    for (int64_t i = 0; i + 1 < len; ++i)
+        if (U[i + 1] < U[i])
+            return fail(MFA_ERR_KNOTS, std::string("knots[") + ax + "] decreases at index " + std::to_string(i + 1));
+    for (int i = 0; i <= p; ++i) {
+        if (U[i] != 0.0)
+            return fail(MFA_ERR_KNOTS, std::string("knots[") + ax + "][" + std::to_string(i) +
+                                           "] must be 0 (clamped, first p+1 knots)");
+        if (U[len - 1 - i] != 1.0)
+            return fail(MFA_ERR_KNOTS, std::string("knots[") + ax + "][" + std::to_string(len - 1 - i) +
+                                           "] must be 1 (clamped, last p+1 knots)");
+    }
+    int64_t run = 1;
+    for (int64_t i = p + 2; i < n; ++i) {  // interior knots U[p+1..n-1]
+        run = (U[i] == U[i - 1]) ? run + 1 : 1;
+        if (run > p)
+            return fail(MFA_ERR_KNOTS, std::string("knots[") + ax + "] interior multiplicity > degree at index " +
+                                           std::to_string(i));
+    }
+    if (n > p + 1 && (U[p + 1] == 0.0 || U[n - 1] == 1.0))
+        return fail(MFA_ERR_KNOTS, std::string("knots[") + ax + "] interior knot equals an end knot");
+    const int64_t S = n - p;
+    int uni = 1;
+    for (int64_t k = 1; k < S && uni; ++k)
+        if (U[p + k] != (double)k / (double)S) uni = 0;
+    *uniform = uni;
+    return MFA_OK;
+}
+
+extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3], const double* const knots[3],
+                                       const float* ctrl, int32_t ctrl_on_device, mfa_stream stream,
+                                       mfa_model* out) {
+    if (!out) return fail(MFA_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!degree || !nctrl || !knots || !ctrl) return fail(MFA_ERR_INVALID_ARG, "NULL argument");
+    const int p = degree[0];
+    if (degree[1] != p || degree[2] != p)
+        return fail(MFA_ERR_UNSUPPORTED, "this build requires equal degrees on all axes");
+    if (p < 1 || p > MFA_MAX_DEGREE)
+        return fail(MFA_ERR_UNSUPPORTED, "degree " + std::to_string(p) + " outside the compiled set 1..5");
+    for (int d = 0; d < 3; ++d) {
+        if (!knots[d]) return fail(MFA_ERR_INVALID_ARG, "knots[" + std::to_string(d) + "] is NULL");
+        if (nctrl[d] < p + 1)
+            return fail(MFA_ERR_INVALID_ARG, "nctrl[" + std::to_string(d) + "] < degree+1");
+        if (nctrl[d] > (1 << 22))
+            return fail(MFA_ERR_UNSUPPORTED, "nctrl[" + std::to_string(d) + "] > 2^22");
+    }
+    int uniform[3];
+    for (int d = 0; d < 3; ++d) {
+        mfa_status st = validate_knots(d, p, nctrl[d], knots[d], &uniform[d]);
+        if (st != MFA_OK) return st;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    Model* m = new Model();
+    m->p = p;
+    for (int d = 0; d < 3; ++d) {
+        m->n[d] = nctrl[d];
+        m->uniform[d] = uniform[d];
+    }
+    cudaError_t e = cudaGetDevice(&m->device);
+    if (e != cudaSuccess) { delete m; return cuda_fail(e, "cudaGetDevice"); }
+
+    const int64_t nu = nctrl[0], nv = nctrl[1], nw = nctrl[2];
+    const int64_t npts = nu * nv * nw;
+    float* Pdev = nullptr;
+    float* Pown = nullptr;
+    double* Udev = nullptr;
+    unsigned int* mm = nullptr;
+    auto cleanup = [&](mfa_status s) {
+        if (Pown) cudaFree(Pown);
+        if (Udev) cudaFree(Udev);
+        if (mm) cudaFree(mm);
+        if (s != MFA_OK) {
+            if (m->Q) cudaFree(m->Q);
+            if (m->table_mem) cudaFree(m->table_mem);
+            delete m;
+        }
+        return s;
+    };
+    if (ctrl_on_device) {
+        Pdev = const_cast<float*>(ctrl);
+    } else {
+        if ((e = cudaMalloc(&Pown, npts * sizeof(float))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc ctrl"));
+        if ((e = cudaMemcpyAsync(Pown, ctrl, npts * sizeof(float), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+            return cleanup(cuda_fail(e, "copy ctrl"));
+        Pdev = Pown;
+    }
+    // finiteness + value range
+    if ((e = cudaMalloc(&mm, 3 * sizeof(unsigned int))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc"));
+    unsigned int init[3] = {0xffffffffu, 0u, 0u};
+    cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    minmax_kernel<<<1184, 256, 0, st>>>(Pdev, npts, mm);
+    // row quads
+    if ((e = cudaMalloc(&m->Q, npts * sizeof(float4))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc Q"));
+    relayout_quads_kernel<<<4736, 256, 0, st>>>(Pdev, m->Q, nu, nv * nw);
+    m->device_bytes = npts * (int64_t)sizeof(float4);
+
+    // axis tables: one allocation
+    const int rec = rec_floats(p);
+    size_t off[3][6];
+    size_t total = 0;
+    int Mb[3];
+    auto bump = [&](size_t bytes) {
+        size_t o = total;
+        total += (bytes + 255) & ~(size_t)255;
+        return o;
+    };
+    for (int d = 0; d < 3; ++d) {
+        const int nsp = (int)(nctrl[d] - p);
+        int M = 1;
+        while (M < 4 * nsp) M <<= 1;
+        Mb[d] = M;
+        off[d][0] = bump(sizeof(float) * rec * nsp);        // coef
+        off[d][1] = bump(sizeof(float) * nsp);              // invh
+        off[d][2] = bump(sizeof(float) * (nsp + 1));        // kh
+        off[d][3] = bump(sizeof(float) * (nsp + 1));        // kl
+        off[d][4] = bump(sizeof(long long) * (nsp + 1));    // kfx
+        off[d][5] = bump(sizeof(int) * M);                  // bucket
+    }
+    size_t uoff[3];
+    size_t utotal = 0;
+    for (int d = 0; d < 3; ++d) {
+        uoff[d] = utotal;
+        utotal += sizeof(double) * (nctrl[d] + p + 1);
+    }
+    if ((e = cudaMalloc(&m->table_mem, total)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc tables"));
+    if ((e = cudaMalloc(&Udev, utotal)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc knots"));
+    m->device_bytes += total;
+    char* base = (char*)m->table_mem;
+    for (int d = 0; d < 3; ++d) {
+        const int nsp = (int)(nctrl[d] - p);
+        double* Ud = (double*)((char*)Udev + uoff[d]);
+        cudaMemcpyAsync(Ud, knots[d], sizeof(double) * (nctrl[d] + p + 1), cudaMemcpyHostToDevice, st);
+        AxisTables& A = m->ax[d];
+        A.coef = (float*)(base + off[d][0]);
+        A.invh = (float*)(base + off[d][1]);
+        A.kh = (float*)(base + off[d][2]);
+        A.kl = (float*)(base + off[d][3]);
+        A.kfx = (long long*)(base + off[d][4]);
+        A.bucket = (int*)(base + off[d][5]);
+        A.nsp = nsp;
+        A.M = Mb[d];
+        A.uniform = uniform[d];
+        A.S = (float)nsp;
+        span_tables_kernel<<<(nsp + 127) / 128, 128, 0, st>>>(Ud, p, nsp, rec, (float*)A.coef, (float*)A.invh);
+        const int nt = std::max(nsp + 1, Mb[d]);
+        knot_tables_kernel<<<(nt + 255) / 256, 256, 0, st>>>(Ud, p, nsp, (float*)A.kh, (float*)A.kl,
+                                                             (long long*)A.kfx, Mb[d], (int*)A.bucket);
+        // uniform interior spans [p-1, S-p] share one polynomial set
+        A.ic_lo = p - 1;
+        A.ic_hi = nsp - p;
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(cuda_fail(e, "model ingest kernels"));
+    unsigned int hmm[3];
+    if ((e = cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "copy range"));
+    for (int d = 0; d < 3; ++d) {
+        AxisTables& A = m->ax[d];
+        if (A.uniform && A.ic_hi >= A.ic_lo) {
+            if ((e = cudaMemcpyAsync(A.interior, A.coef + (int64_t)A.ic_lo * rec, sizeof(float) * (p + 1) * (p + 1),
+                                     cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+                return cleanup(cuda_fail(e, "copy interior"));
+        } else {
+            A.ic_lo = 0;
+            A.ic_hi = -1;
+        }
+    }
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cleanup(cuda_fail(e, "model ingest"));
+    if (hmm[2] != 0)
+        return cleanup(fail(MFA_ERR_DOMAIN, std::to_string(hmm[2]) + " non-finite control values"));
+    m->vmin = ord2f(hmm[0]);
+    m->vmax = ord2f(hmm[1]);
+    cleanup(MFA_OK);
+    *out = reinterpret_cast<mfa_model>(m);
+    return MFA_OK;
+}
+
+extern "C" mfa_status mfa_model_info(mfa_model h, mfa_model_desc* out) {
+    if (!h || !out) return fail(MFA_ERR_INVALID_ARG, "NULL argument");
+    const Model* m = reinterpret_cast<const Model*>(h);
+    for (int d = 0; d < 3; ++d) {
+        out->degree[d] = m->p;
+        out->nctrl[d] = m->n[d];
+        out->uniform[d] = m->uniform[d];
+    }
+    out->v_min = m->vmin;
+    out->v_max = m->vmax;
+    out->device_bytes = m->device_bytes;
+    out->device = m->device;
+    return MFA_OK;
+}
+
+extern "C" mfa_status mfa_model_destroy(mfa_model h) {
+    if (!h) return MFA_OK;
+    Model* m = reinterpret_cast<Model*>(h);
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != m->device) cudaSetDevice(m->device);
+    if (m->Q) cudaFree(m->Q);
+    if (m->table_mem) cudaFree(m->table_mem);
+    if (cur != m->device && cur >= 0) cudaSetDevice(cur);
+    delete m;
+    return MFA_OK;
+}
+
+extern "C" mfa_status mfa_eval_batch(mfa_model h, int64_t n, const float* u, const float* v, const float* w,
+                                     float* value, float* du, float* dv, float* dw,
+                                     unsigned long long* n_domain_errors, mfa_stream stream) {
+    if (!h) return fail(MFA_ERR_INVALID_ARG, "model is NULL");
+    if (n < 0) return fail(MFA_ERR_INVALID_ARG, "n < 0");
+    if (n == 0) return MFA_OK;
+    if (!u || !v || !w || !value) return fail(MFA_ERR_INVALID_ARG, "u, v, w and value are required");
+    const int ng = (du != nullptr) + (dv != nullptr) + (dw != nullptr);
+    if (ng != 0 && ng != 3) return fail(MFA_ERR_INVALID_ARG, "du, dv, dw must be all NULL or all non-NULL");
+    const Model* m = reinterpret_cast<const Model*>(h);
+    mfa_status s = check_device(m);
+    if (s != MFA_OK) return s;
+    return launch_eval(m, n, u, v, w, value, du, dv, dw, n_domain_errors, (cudaStream_t)stream);
+}
+
+static mfa_status validate_render(const Model* m, int32_t n_views, const mfa_camera* cams,
+                                  const mfa_render_params* prm) {
+    if (n_views < 1) return fail(MFA_ERR_INVALID_ARG, "n_views < 1");
+    if (!cams || !prm) return fail(MFA_ERR_INVALID_ARG, "cams and prm are required");
+    for (int v = 0; v < n_views; ++v) {
+        const mfa_camera& c = cams[v];
+        if (c.width < 1 || c.height < 1) return fail(MFA_ERR_INVALID_ARG, "camera " + std::to_string(v) + ": size < 1");
+        if (c.width != cams[0].width || c.height != cams[0].height)
+            return fail(MFA_ERR_INVALID_ARG, "all views of one call must share width and height");
+        if (!(c.fov_y_deg >= 0.0 && c.fov_y_deg < 180.0))
+            return fail(MFA_ERR_INVALID_ARG, "camera " + std::to_string(v) + ": fov_y_deg outside [0,180)");
+        if (c.fov_y_deg == 0.0 && !(c.ortho_half_height > 0.0))
+            return fail(MFA_ERR_INVALID_ARG, "camera " + std::to_string(v) + ": ortho_half_height <= 0");
+        double f[3] = {c.look_at[0] - c.eye[0], c.look_at[1] - c.eye[1], c.look_at[2] - c.eye[2]};
+        double x[3] = {f[1] * c.up[2] - f[2] * c.up[1], f[2] * c.up[0] - f[0] * c.up[2], f[0] * c.up[1] - f[1] * c.up[0]};
+        double lf = sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+        double lx = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+        if (!(lf > 0.0) || !(lx > 1e-12 * lf))
+            return fail(MFA_ERR_INVALID_ARG, "camera " + std::to_string(v) + ": degenerate eye/look_at/up");
+    }
+    for (int d = 0; d < 3; ++d)
+        if (!(prm->box_max[d] > prm->box_min[d])) return fail(MFA_ERR_INVALID_ARG, "box_max <= box_min");
+    if (!(prm->step > 0.0)) return fail(MFA_ERR_INVALID_ARG, "step <= 0");
+    (void)m;
+    return MFA_OK;
+}
+
+extern "C" mfa_status mfa_render(mfa_model h, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
+                                 const mfa_render_params* prm, const mfa_tiles* tiles, void* rgba_out,
+                                 unsigned long long* samples_out, mfa_stream stream) {
+    if (!h) return fail(MFA_ERR_INVALID_ARG, "model is NULL");
+    const Model* m = reinterpret_cast<const Model*>(h);
+    mfa_status s = validate_render(m, n_views, cams, prm);
+    if (s != MFA_OK) return s;
+    if (!tf || !tf->rgba || tf->n_entries < 2 || tf->n_entries > 1024 || !(tf->v_hi > tf->v_lo))
+        return fail(MFA_ERR_INVALID_ARG, "tf: need rgba, 2 <= n_entries <= 1024, v_hi > v_lo");
+    if (!rgba_out) return fail(MFA_ERR_INVALID_ARG, "rgba_out is NULL");
+    if (tiles && (tiles->n_tiles < 0 || (tiles->n_tiles > 0 && !tiles->tiles)))
+        return fail(MFA_ERR_INVALID_ARG, "tiles: bad n_tiles / tiles pointer");
+    if ((s = check_device(m)) != MFA_OK) return s;
+    return launch_render(m, n_views, cams, tf, prm, tiles, rgba_out, samples_out, (cudaStream_t)stream);
+}
+
+extern "C" mfa_status mfa_unpack_tiles(const void* packed, int32_t in_fp16, const int32_t* tiles, int64_t n_tiles,
+                                       int32_t n_views, int32_t width, int32_t height, float* image_out,
+                                       mfa_stream stream) {
+    if (n_tiles < 0 || n_views < 1 || width < 1 || height < 1) return fail(MFA_ERR_INVALID_ARG, "bad sizes");
+    if (n_tiles == 0) return MFA_OK;
+    if (!packed || !tiles || !image_out) return fail(MFA_ERR_INVALID_ARG, "NULL pointer");
+    unpack_tiles_kernel<<<(unsigned)n_tiles, MFA_TILE * MFA_TILE, 0, (cudaStream_t)stream>>>(
+        packed, in_fp16, tiles, n_tiles, width, height, reinterpret_cast<float4*>(image_out));
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? MFA_OK : cuda_fail(e, "unpack_tiles launch");
+}
+
+extern "C" mfa_status mfa_render_host(mfa_model h, int32_t n_views, const mfa_camera* cams, const float* tf_rgba_host,
+                                      int32_t tf_n_entries, float v_lo, float v_hi, const mfa_render_params* prm,
+                                      void* rgba_host, unsigned long long* samples_host, mfa_stream stream) {
+    if (!h) return fail(MFA_ERR_INVALID_ARG, "model is NULL");
+    const Model* m = reinterpret_cast<const Model*>(h);
+    mfa_status s = validate_render(m, n_views, cams, prm);
+    if (s != MFA_OK) return s;
+    if (!tf_rgba_host || tf_n_entries < 2 || tf_n_entries > 1024 || !(v_hi > v_lo) || !rgba_host)
+        return fail(MFA_ERR_INVALID_ARG, "tf / rgba_host");
+    if ((s = check_device(m)) != MFA_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t px = (size_t)cams[0].width * cams[0].height;
+    const size_t view_bytes = px * (prm->out_fp16 ? 8 : 16);
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    void* stage[2] = {nullptr, nullptr};
+    float* dtf = nullptr;
+    unsigned long long* dcnt = nullptr;
+    cudaError_t e;
+    auto done = [&](mfa_status r) {
+        if (cs) cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(st);
+        for (int i = 0; i < 2; ++i) {
+            if (stage[i]) cudaFreeAsync(stage[i], st);
+            if (ev[i]) cudaEventDestroy(ev[i]);
+        }
+        if (dtf) cudaFreeAsync(dtf, st);
+        if (dcnt) cudaFreeAsync(dcnt, st);
+        cudaStreamSynchronize(st);
+        if (cs) cudaStreamDestroy(cs);
+        return r;
+    };
+    if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess) return done(cuda_fail(e, "stream"));
+    for (int i = 0; i < 2; ++i) {
+        if ((e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming)) != cudaSuccess) return done(cuda_fail(e, "event"));
+        if ((e = cudaMallocAsync(&stage[i], view_bytes, st)) != cudaSuccess) return done(cuda_fail(e, "staging"));
+    }
+    if ((e = cudaMallocAsync((void**)&dtf, sizeof(float) * 4 * tf_n_entries, st)) != cudaSuccess) return done(cuda_fail(e, "tf"));
+    if ((e = cudaMallocAsync((void**)&dcnt, sizeof(unsigned long long), st)) != cudaSuccess) return done(cuda_fail(e, "count"));
+    cudaMemcpyAsync(dtf, tf_rgba_host, sizeof(float) * 4 * tf_n_entries, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long), st);
+    mfa_tf tf{dtf, tf_n_entries, v_lo, v_hi};
+    cudaEvent_t copied[2] = {nullptr, nullptr};
+    for (int i = 0; i < 2; ++i)
+        if ((e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming)) != cudaSuccess) return done(cuda_fail(e, "event"));
+    for (int v = 0; v < n_views; ++v) {
+        const int b = v & 1;
+        if (v >= 2) cudaStreamWaitEvent(st, copied[b], 0);  // staging buffer b free again
+        s = launch_render(m, 1, cams + v, &tf, prm, nullptr, stage[b], dcnt, st);
+        if (s != MFA_OK) break;
+        cudaEventRecord(ev[b], st);
+        cudaStreamWaitEvent(cs, ev[b], 0);
+        cudaMemcpyAsync((char*)rgba_host + v * view_bytes, stage[b], view_bytes, cudaMemcpyDeviceToHost, cs);
+        cudaEventRecord(copied[b], cs);
+    }
+    if (s == MFA_OK && samples_host) {
+        cudaStreamWaitEvent(st, copied[(n_views - 1) & 1], 0);
+        cudaMemcpyAsync(samples_host, dcnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+    }
+    mfa_status r = done(s);
+    for (int i = 0; i < 2; ++i)
+        if (copied[i]) cudaEventDestroy(copied[i]);
+    if (r == MFA_OK && (e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "render_host");
+    return r;
+}

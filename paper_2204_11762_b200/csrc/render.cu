@@ -1,0 +1,367 @@
+// mfa_render kernel: Algorithm 1 fused per ray.
+//
+//   CTA  = one 16x16 pixel tile of one view (8 warps; warp = 8x4 pixels, so a
+//          warp's rays stay spatially coherent and share control rows in L1).
+//   ray  = one thread.  a1-a2 ray setup in fp64; sample positions are kept in
+//          64-bit fixed point (the "fixed-point ray cast model"):
+//          uniform axes in span units * 2^40, non-uniform axes in parameter
+//          units * 2^62, advanced by an exact integer add per sample.
+//   loop = a3 position -> a4 span/t -> a5 basis -> a6/a7 gather+contract ->
+//          a8 TF (shared-memory table) -> a9 Phong -> a10 composite; the warp
+//          leaves the loop when no lane is live (__any_sync), i.e. early ray
+//          termination per ray with a warp-vote exit.
+//   out  = premultiplied RGBA (fp32 or fp16) to the image or to a packed tile.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace mfa {
+
+struct RenderArgs {
+    const float4* Q;
+    int nu, nv, nw;
+    AxisArgs ax[3];
+    const float4* tf;
+    int tf_n;
+    float v_lo, s_scale;          // s = (v - v_lo) / (v_hi - v_lo); f = s*(n-1) = (v - v_lo)*s_scale
+    double bmin[3], L[3];
+    double step;
+    float invL[3];
+    float o_max, ka, kd, ks, shin, eps2;
+    int shading;
+    int W, H, tiles_x, tiles_y;
+    const int* tiles;             // NULL: full frames
+    int64_t n_tiles;
+    int view_base;                // full frames: output view index of cams[0]
+    void* out;
+    int out_fp16;
+    unsigned long long* samples;
+    mfa_camera cams[kMaxViewsPerLaunch];
+};
+
+struct ViewFrame {
+    double eye[3], f[3], A[3], B[3];
+    int ortho;
+};
+
+__device__ __forceinline__ void compute_frame(const mfa_camera& c, ViewFrame& fr) {
+    double f[3] = {c.look_at[0] - c.eye[0], c.look_at[1] - c.eye[1], c.look_at[2] - c.eye[2]};
+    double lf = sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+    for (int i = 0; i < 3; ++i) f[i] /= lf;
+    double r[3] = {f[1] * c.up[2] - f[2] * c.up[1], f[2] * c.up[0] - f[0] * c.up[2], f[0] * c.up[1] - f[1] * c.up[0]};
+    double lr = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    for (int i = 0; i < 3; ++i) r[i] /= lr;
+    double u[3] = {r[1] * f[2] - r[2] * f[1], r[2] * f[0] - r[0] * f[2], r[0] * f[1] - r[1] * f[0]};
+    const double aspect = (double)c.width / (double)c.height;
+    double sx, sy;
+    if (c.fov_y_deg > 0.0) {
+        const double th = tan(0.5 * c.fov_y_deg * 3.14159265358979323846 / 180.0);
+        sx = aspect * th;
+        sy = th;
+        fr.ortho = 0;
+    } else {
+        sx = aspect * c.ortho_half_height;
+        sy = c.ortho_half_height;
+        fr.ortho = 1;
+    }
+    for (int i = 0; i < 3; ++i) {
+        fr.eye[i] = c.eye[i];
+        fr.f[i] = f[i];
+        fr.A[i] = sx * r[i];
+        fr.B[i] = sy * u[i];
+    }
+}
+
+template <int P, bool UNI, bool SHADE>
+__global__ void __launch_bounds__(256) render_kernel(const __grid_constant__ RenderArgs args) {
+    extern __shared__ float4 s_tf[];
+    __shared__ ViewFrame s_frame;
+    __shared__ unsigned long long s_count;
+
+    // ---- which tile --------------------------------------------------------
+    int view, tx, ty;
+    int64_t tile_id = blockIdx.x;
+    if (args.tiles) {
+        view = args.tiles[3 * tile_id];
+        tx = args.tiles[3 * tile_id + 1];
+        ty = args.tiles[3 * tile_id + 2];
+        if (view < 0) return;  // padding unit (multi-GPU equal-size buffers)
+    } else {
+        const int per_view = args.tiles_x * args.tiles_y;
+        view = (int)(tile_id / per_view);
+        const int t = (int)(tile_id % per_view);
+        ty = t / args.tiles_x;
+        tx = t % args.tiles_x;
+    }
+    if (threadIdx.x == 0) {
+        compute_frame(args.cams[view], s_frame);
+        s_count = 0ull;
+    }
+    for (int i = threadIdx.x; i < args.tf_n; i += blockDim.x) s_tf[i] = __ldg(args.tf + i);
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = (warp & 1) * 8 + (lane & 7);
+    const int ly = (warp >> 1) * 4 + (lane >> 3);
+    const int px = tx * MFA_TILE + lx, py = ty * MFA_TILE + ly;
+    const bool valid = px < args.W && py < args.H;
+
+    // ---- a1: ray through the pixel centre (fp64) ---------------------------
+    double o[3], d[3];
+    {
+        const double X = 2.0 * (px + 0.5) / args.W - 1.0;
+        const double Y = 1.0 - 2.0 * (py + 0.5) / args.H;
+        if (s_frame.ortho) {
+            for (int i = 0; i < 3; ++i) {
+                o[i] = s_frame.eye[i] + X * s_frame.A[i] + Y * s_frame.B[i];
+                d[i] = s_frame.f[i];
+            }
+        } else {
+            double l2 = 0.0;
+            for (int i = 0; i < 3; ++i) {
+                o[i] = s_frame.eye[i];
+                d[i] = s_frame.f[i] + X * s_frame.A[i] + Y * s_frame.B[i];
+                l2 += d[i] * d[i];
+            }
+            const double il = 1.0 / sqrt(l2);
+            for (int i = 0; i < 3; ++i) d[i] *= il;
+        }
+    }
+    // ---- a2: slab clip, K samples at t_in + (k+1/2) step (R-7) -------------
+    int K = 0;
+    double t_in = 0.0;
+    {
+        double tn = -1e300, tf = 1e300;
+        bool hit = valid;
+        for (int i = 0; i < 3; ++i) {
+            const double bmax = args.bmin[i] + args.L[i];
+            if (d[i] == 0.0) {
+                if (o[i] < args.bmin[i] || o[i] > bmax) hit = false;
+                continue;
+            }
+            const double t0 = (args.bmin[i] - o[i]) / d[i], t1 = (bmax - o[i]) / d[i];
+            tn = fmax(tn, fmin(t0, t1));
+            tf = fmin(tf, fmax(t0, t1));
+        }
+        t_in = fmax(tn, 0.0);
+        if (hit && tf > t_in) {
+            const double fr = (tf - t_in) / args.step - 0.5;
+            K = fr > 0.0 ? (int)ceil(fr) : 0;
+        }
+    }
+    // ---- a3 setup: fixed-point sample coordinates per axis ----------------
+    long long F[3], DF[3];
+    int s_nu[3] = {0, 0, 0};
+    {
+        const double t0 = t_in + 0.5 * args.step;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double u0 = (o[i] + t0 * d[i] - args.bmin[i]) / args.L[i];
+            const double du = args.step * d[i] / args.L[i];
+            if (UNI) {
+                const double S = (double)args.ax[i].nsp;
+                F[i] = llrint(ldexp(u0 * S, kUniFracBits));
+                DF[i] = llrint(ldexp(du * S, kUniFracBits));
+            } else {
+                F[i] = llrint(ldexp(u0, kNonUniFracBits));
+                DF[i] = llrint(ldexp(du, kNonUniFracBits));
+                if (K > 0) s_nu[i] = nonuni_first_span_fx(args.ax[i], F[i]);
+            }
+        }
+    }
+    const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
+    const int row_v = args.nu, row_w = args.nu * args.nv;
+
+    float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+    int k = 0;
+    bool live = K > 0;
+    while (__any_sync(0xffffffffu, live)) {
+        if (live) {
+            // a4: span + local coordinate per axis
+            int s[3];
+            float t[3], sc[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (UNI) {
+                    uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
+                    sc[i] = args.ax[i].S;
+                } else {
+                    nonuni_span_fx(args.ax[i], F[i], s_nu[i], t[i], sc[i]);
+                    s[i] = s_nu[i];
+                }
+            }
+            const float4* base = args.Q + ((int64_t)s[2] * args.nv + s[1]) * args.nu + s[0];
+            float val, gu = 0.f, gv = 0.f, gw = 0.f;
+            if (SHADE) {  // a5 + a6/a7 with derivatives (Alg.1 l.6 and l.9)
+                float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], sc[0], Bu);
+                axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], sc[1], Bv);
+                axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], sc[2], Bw);
+                contract_vg<P>(base, row_v, row_w, Bu, Bv, Bw, val, gu, gv, gw);
+            } else {      // value only (Alg.1 l.8 ShadingOn == false)
+                float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+                axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+                axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+                val = contract_v<P>(base, row_v, row_w, Nu, Nv, Nw);
+            }
+            // a8: transfer function (l.7)
+            float f = (val - args.v_lo) * args.s_scale;
+            f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
+            const int i0 = min((int)f, args.tf_n - 2);
+            const float wt = f - (float)i0;
+            const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
+            float cr = fmaf(wt, T1.x - T0.x, T0.x);
+            float cg = fmaf(wt, T1.y - T0.y, T0.y);
+            float cb = fmaf(wt, T1.z - T0.z, T0.z);
+            const float a = fmaf(wt, T1.w - T0.w, T0.w);
+            // a9: Phong with a headlight (l.10-11; R-11)
+            if (SHADE) {
+                const float gx = gu * args.invL[0], gy = gv * args.invL[1], gz = gw * args.invL[2];
+                const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
+                if (n2 <= args.eps2) {
+                    cr *= args.ka;
+                    cg *= args.ka;
+                    cb *= args.ka;
+                } else {
+                    const float ndl = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * rsqrtf(n2);
+                    const float dif = fmaxf(ndl, 0.f);
+                    const float rv = fmaxf(fmaf(2.f * ndl, ndl, -1.f), 0.f);
+                    float spe = 0.f;
+                    if (ndl > 0.f) spe = rv > 0.f ? exp2f(args.shin * __log2f(rv)) : (args.shin == 0.f ? 1.f : 0.f);
+                    const float lit = fmaf(args.kd, dif, args.ka);
+                    const float add = args.ks * spe;
+                    cr = __saturatef(fmaf(cr, lit, add));
+                    cg = __saturatef(fmaf(cg, lit, add));
+                    cb = __saturatef(fmaf(cb, lit, add));
+                }
+            }
+            // a10: front-to-back compositing + ERT (l.13-15; R-13)
+            const float wgt = (1.f - A) * a;
+            C0 = fmaf(wgt, cr, C0);
+            C1 = fmaf(wgt, cg, C1);
+            C2 = fmaf(wgt, cb, C2);
+            A += wgt;
+            ++k;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) F[i] += DF[i];
+            live = !(A > args.o_max) && k < K;
+        }
+    }
+    // ---- a11: pixel write ---------------------------------------------------
+    if (valid) {
+        int64_t idx;
+        if (args.tiles)
+            idx = tile_id * (MFA_TILE * MFA_TILE) + ly * MFA_TILE + lx;
+        else
+            idx = ((int64_t)(args.view_base + view) * args.H + py) * args.W + px;
+        if (args.out_fp16) {
+            __half2* o2 = reinterpret_cast<__half2*>(args.out) + 2 * idx;
+            o2[0] = __floats2half2_rn(C0, C1);
+            o2[1] = __floats2half2_rn(C2, A);
+        } else {
+            reinterpret_cast<float4*>(args.out)[idx] = make_float4(C0, C1, C2, A);
+        }
+    }
+    if (args.samples) {
+        unsigned c = (unsigned)k;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0 && c) atomicAdd(&s_count, (unsigned long long)c);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_count) atomicAdd(args.samples, s_count);
+    }
+}
+
+template <int P, bool UNI, bool SHADE>
+static cudaError_t launch_render_t(const RenderArgs& a, int64_t nblocks, cudaStream_t st) {
+    const size_t smem = sizeof(float4) * a.tf_n;
+    if (nblocks >= (1ll << 31)) return cudaErrorInvalidConfiguration;
+    render_kernel<P, UNI, SHADE><<<(unsigned)nblocks, 256, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int P>
+static cudaError_t dispatch_render(const RenderArgs& a, int64_t nb, bool uni, bool shade, cudaStream_t st) {
+    if (uni) return shade ? launch_render_t<P, true, true>(a, nb, st) : launch_render_t<P, true, false>(a, nb, st);
+    return shade ? launch_render_t<P, false, true>(a, nb, st) : launch_render_t<P, false, false>(a, nb, st);
+}
+
+mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
+                         const mfa_render_params* prm, const mfa_tiles* tiles, void* out,
+                         unsigned long long* samples, cudaStream_t st) {
+    RenderArgs* a = new RenderArgs();  // ~7 KB: keep it off the caller's stack
+    a->Q = m->Q;
+    a->nu = (int)m->n[0];
+    a->nv = (int)m->n[1];
+    a->nw = (int)m->n[2];
+    for (int d = 0; d < 3; ++d) a->ax[d] = make_axis_args(m->ax[d]);
+    a->tf = reinterpret_cast<const float4*>(tf->rgba);
+    a->tf_n = tf->n_entries;
+    a->v_lo = tf->v_lo;
+    a->s_scale = (float)((double)(tf->n_entries - 1) / ((double)tf->v_hi - (double)tf->v_lo));
+    for (int d = 0; d < 3; ++d) {
+        a->bmin[d] = prm->box_min[d];
+        a->L[d] = prm->box_max[d] - prm->box_min[d];
+        a->invL[d] = (float)(1.0 / a->L[d]);
+    }
+    a->step = prm->step;
+    a->o_max = (float)prm->o_max;
+    a->ka = (float)prm->ka;
+    a->kd = (float)prm->kd;
+    a->ks = (float)prm->ks;
+    a->shin = (float)prm->shininess;
+    a->eps2 = (float)(prm->grad_eps * prm->grad_eps);
+    a->shading = prm->shading;
+    a->W = cams[0].width;
+    a->H = cams[0].height;
+    a->tiles_x = (a->W + MFA_TILE - 1) / MFA_TILE;
+    a->tiles_y = (a->H + MFA_TILE - 1) / MFA_TILE;
+    a->out = out;
+    a->out_fp16 = prm->out_fp16;
+    a->samples = samples;
+    const bool uni = m->uniform[0] && m->uniform[1] && m->uniform[2];
+    const bool shade = prm->shading != 0;
+    cudaError_t e = cudaSuccess;
+    if (tiles) {
+        // tiles reference views 0..n_views-1 of cams; one launch per <=64-view group
+        if (n_views > kMaxViewsPerLaunch) {
+            delete a;
+            return fail(MFA_ERR_UNSUPPORTED, "tiled render supports at most 64 views per call");
+        }
+        for (int v = 0; v < n_views; ++v) a->cams[v] = cams[v];
+        a->tiles = tiles->tiles;
+        a->n_tiles = tiles->n_tiles;
+        a->view_base = 0;
+        if (tiles->n_tiles > 0) {
+            switch (m->p) {
+                case 1: e = dispatch_render<1>(*a, tiles->n_tiles, uni, shade, st); break;
+                case 2: e = dispatch_render<2>(*a, tiles->n_tiles, uni, shade, st); break;
+                case 3: e = dispatch_render<3>(*a, tiles->n_tiles, uni, shade, st); break;
+                case 4: e = dispatch_render<4>(*a, tiles->n_tiles, uni, shade, st); break;
+                default: e = dispatch_render<5>(*a, tiles->n_tiles, uni, shade, st); break;
+            }
+        }
+    } else {
+        a->tiles = nullptr;
+        a->n_tiles = 0;
+        for (int v0 = 0; v0 < n_views && e == cudaSuccess; v0 += kMaxViewsPerLaunch) {
+            const int nv = std::min(kMaxViewsPerLaunch, n_views - v0);
+            for (int v = 0; v < nv; ++v) a->cams[v] = cams[v0 + v];
+            a->view_base = v0;
+            const int64_t nb = (int64_t)nv * a->tiles_x * a->tiles_y;
+            switch (m->p) {
+                case 1: e = dispatch_render<1>(*a, nb, uni, shade, st); break;
+                case 2: e = dispatch_render<2>(*a, nb, uni, shade, st); break;
+                case 3: e = dispatch_render<3>(*a, nb, uni, shade, st); break;
+                case 4: e = dispatch_render<4>(*a, nb, uni, shade, st); break;
+                default: e = dispatch_render<5>(*a, nb, uni, shade, st); break;
+            }
+        }
+    }
+    delete a;
+    return e == cudaSuccess ? MFA_OK : cuda_fail(e, "render launch");
+}
+
+}  // namespace mfa

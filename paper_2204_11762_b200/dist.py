@@ -1,0 +1,73 @@
+"""Multi-GPU screen-tile sharding (north_star "the control
+points are replicated and the image is sharded by screen tiles, with an NCCL
+gather of RGBA tiles over NVLink").
+
+Every ray is independent given the replicated model (Algorithm 1 splits rows
+over threads; "computation for all pixel values ... can also be
+parallelized").  The work unit is a (view, 16x16 tile).  Units are
+dealt to ranks with a diagonal interleave (unit j of view-row r goes to rank
+(j + r) mod G) so that empty, cheap and ERT-heavy regions spread evenly.
+Each rank renders its units into a packed tile buffer; one collective
+(all_gather_into_tensor over equal, padded buffers; NCCL over NVLink /
+NVSwitch on GPUs) brings all tiles to every rank and rank 0 scatters them
+into the image with the unpack kernel.  Per-pixel arithmetic does not depend
+on the assignment, so the G-GPU image is bit-identical to the 1-GPU image.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+TILE = 16
+
+
+def tile_grid(width: int, height: int):
+    return (width + TILE - 1) // TILE, (height + TILE - 1) // TILE
+
+
+def all_units(n_views: int, width: int, height: int) -> np.ndarray:
+    """Every (view, tx, ty) unit in raster order, int32 (n, 3)."""
+    tx, ty = tile_grid(width, height)
+    v, y, x = np.meshgrid(np.arange(n_views), np.arange(ty), np.arange(tx), indexing="ij")
+    return np.stack([v.ravel(), x.ravel(), y.ravel()], axis=1).astype(np.int32)
+
+
+def assign_units(n_views: int, width: int, height: int, world: int) -> list[np.ndarray]:
+    """Per-rank unit lists, padded to equal length with view = -1 entries
+    (skipped by the render and unpack kernels)."""
+    u = all_units(n_views, width, height)
+    tx, _ = tile_grid(width, height)
+    j = np.arange(len(u))
+    row = j // tx
+    owner = (j + row) % world
+    lists = [u[owner == r] for r in range(world)]
+    n = max((len(x) for x in lists), default=0)
+    out = []
+    for x in lists:
+        pad = np.full((n - len(x), 3), -1, np.int32)
+        out.append(np.ascontiguousarray(np.concatenate([x, pad])) if len(pad) else np.ascontiguousarray(x))
+    return out
+
+
+def render_sharded(render_tiles, unpack, n_views, width, height, rank, world, device=None,
+                   channels=4, dtype=None, group=None):
+    """Render this rank's units, gather every rank's packed tiles, unpack on rank 0.
+
+    render_tiles(tiles_int32_tensor) -> packed tensor [n, 16, 16, channels]
+    unpack(packed_all, tiles_all) -> image (rank 0 only)
+    Returns (image or None, n_local_units)."""
+    import torch
+    import torch.distributed as dist
+    lists = assign_units(n_views, width, height, world)
+    mine = torch.from_numpy(lists[rank])
+    if device is not None:
+        mine = mine.to(device)
+    packed = render_tiles(mine)
+    if world == 1:
+        return unpack(packed, mine), len(lists[rank])
+    gathered = torch.empty((world * packed.shape[0],) + tuple(packed.shape[1:]), dtype=packed.dtype,
+                           device=packed.device)
+    dist.all_gather_into_tensor(gathered, packed.contiguous(), group=group)
+    if rank != 0:
+        return None, len(lists[rank])
+    tiles_all = torch.from_numpy(np.concatenate(lists)).to(packed.device)
+    return unpack(gathered, tiles_all), len(lists[rank])

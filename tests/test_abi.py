@@ -1,0 +1,50 @@
+"""The C-ABI library builds, loads without a GPU, and exports every entry
+point include/mfa.h declares (no compute calls here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "mfa.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mfa_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_north_star_calls():
+    syms = declared_symbols()
+    for s in ("mfa_model_create", "mfa_eval_batch", "mfa_render"):
+        assert s in syms
+
+
+def test_library_exports_all_declared_symbols():
+    from paper_2204_11762_b200 import build
+    lib = build.build()
+    L = ctypes.CDLL(lib)
+    for s in declared_symbols():
+        assert hasattr(L, s), s
+    out = subprocess.check_output(["nm", "-D", "--defined-only", lib]).decode()
+    exported = set(re.findall(r" T (mfa_\w+)", out))
+    assert set(declared_symbols()) <= exported
+    from paper_2204_11762_b200 import _lib
+    assert set(_lib.EXPORTS) == set(declared_symbols())
+
+
+def test_version_and_error_string_without_gpu():
+    from paper_2204_11762_b200 import _lib
+    assert _lib.version().startswith("mfa-b200")
+    L = _lib.lib()
+    # validation errors are synchronous and need no device
+    h = ctypes.c_void_p(0)
+    st = L.mfa_model_create(None, None, None, None, 0, None, ctypes.byref(h))
+    assert st == 1 and b"NULL" in L.mfa_last_error()
+
+
+def test_sm100a_cubin():
+    from paper_2204_11762_b200 import build
+    lib = build.build()
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib]).decode()
+    assert "sm_100a" in out

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C ABI, via the ctypes binding)
+against the fp64 oracle on the same seeded inputs, on all five configs.
+Marked gpu: run on a B200 with `pytest -m gpu`."""
+import functools
+
+import numpy as np
+import pytest
+
+import oracle as O
+import parity
+from paper_2204_11762_b200 import workloads as WL
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@functools.lru_cache(maxsize=None)
+def workload(c, **kw):
+    return WL.make_config(c, **kw)
+
+
+@functools.lru_cache(maxsize=None)
+def gpu_model(c):
+    from paper_2204_11762_b200 import Model
+    return Model.from_workload(workload(c))
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_model(c):
+    return O.Model.from_workload(workload(c))
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_eval(m, u, v, w, grad=True):
+    outs = m.eval(cuda(u), cuda(v), cuda(w), grad=grad)
+    torch.cuda.synchronize()
+    return np.stack([o.cpu().numpy() for o in outs], axis=1)
+
+
+EVAL_N = {1: 1 << 16, 2: 1 << 18, 3: 1 << 24, 4: 1 << 16, 5: 1 << 19}
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_eval_parity(c):
+    """Random points (C3: the full 2^24 set of BASELINE.json) plus the
+    boundary set (u in {0, 1, 1-ulp, knots}), value + gradient."""
+    w = workload(c)
+    u, v, ww = WL.query_points(c, EVAL_N[c])
+    bu, bv, bw = WL.boundary_points(w)
+    u, v, ww = (np.concatenate([a, b]) for a, b in ((u, bu), (v, bv), (ww, bw)))
+    got = gpu_eval(gpu_model(c), u, v, ww)
+    ref, sig, errs = oracle_model(c).eval_batch(u, v, ww)
+    assert errs == 0
+    wv, wg = parity.check_eval(got, ref, sig, f"C{c}")
+    print(f"C{c}: n={len(u)} worst value {wv:.2e} sigma, worst gradient {wg:.2e} sigma")
+
+
+def test_eval_value_only_matches():
+    c = 2
+    u, v, w = WL.query_points(c, 1 << 14)
+    full = gpu_eval(gpu_model(c), u, v, w)
+    vo = gpu_eval(gpu_model(c), u, v, w, grad=False)
+    ref, sig, _ = oracle_model(c).eval_batch(u, v, w)
+    parity.check_eval(vo, ref[:, :1], sig[:, :1], "value-only")
+    assert np.abs(vo[:, 0] - full[:, 0]).max() <= 1e-5 * max(1.0, np.abs(ref[:, 0]).max())
+
+
+def test_eval_domain_errors_and_empty():
+    m = gpu_model(1)
+    u = np.array([0.5, 1.5, np.nan, -0.0, 1.0, -1e-7], np.float32)
+    v = np.full(6, 0.25, np.float32)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    outs = m.eval(cuda(u), cuda(v), cuda(v), n_domain_errors=cnt)
+    torch.cuda.synchronize()
+    val = outs[0].cpu().numpy()
+    assert int(cnt.item()) == 3
+    assert np.isnan(val[[1, 2, 5]]).all() and np.isfinite(val[[0, 3, 4]]).all()
+    e = torch.empty(0, device="cuda")
+    m.eval(e, e, e)   # n == 0 is valid
+    torch.cuda.synchronize()
+
+
+def render_gpu(c, w=None, pixels=None, **kw):
+    w = w or workload(c)
+    m = gpu_model(c)
+    samples = torch.zeros(1, dtype=torch.int64, device="cuda")
+    img = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params, samples=samples, **kw)
+    torch.cuda.synchronize()
+    return img.float().cpu().numpy(), int(samples.item())
+
+
+@pytest.mark.parametrize("c", [1, 2, 3])
+def test_render_full_frame_parity(c):
+    """Full frames (C1 64^2 ortho, C2 512^2, C3 1024^2)."""
+    w = workload(c)
+    img, ns = render_gpu(c)
+    ref = O.render(oracle_model(c), w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
+    st = parity.check_image(img[0].reshape(-1, 4), ref, f"C{c}")
+    tot = int(ref["count"].sum())
+    assert abs(ns - tot) <= max(1e-4 * tot, parity.count_window(ref)), (ns, tot)
+    print(f"C{c}: {st} samples gpu {ns} oracle {tot}")
+
+
+@pytest.mark.parametrize("c,views,frac", [(4, (0,), 0.05), (5, (0, 21, 42, 63), 0.0125)])
+def test_render_subset_parity_full_size(c, views, frac):
+    """Full-size C4 / C5 in the launch configuration the bench times (all
+    views of the batch in one call), checked on a seeded 5% tile subset
+    (C5: 5% over 4 views)."""
+    w = workload(c)
+    img, ns = render_gpu(c)
+    H, W = w.cameras[0].height, w.cameras[0].width
+    sub = WL.tile_subset(c, W, H, frac, views=views)
+    for v, pix in sub.items():
+        ref = O.render(oracle_model(c), w.cameras[v], w.tf, w.v_lo, w.v_hi, w.params, pixels=pix)
+        st = parity.check_image(img[v].reshape(-1, 4)[pix], ref, f"C{c} view {v}")
+        print(f"C{c} view {v}: {st}")
+
+
+def test_tiled_render_bit_identical_and_unpack():
+    """Screen-tile sharding invariant: rendering any tile list gives the
+    same pixels as the full frame (bit-identical); unpack_tiles rebuilds it."""
+    from paper_2204_11762_b200 import unpack_tiles
+    c = 2
+    w = workload(c)
+    full, ns_full = render_gpu(c)
+    tx = (w.cameras[0].width + 15) // 16
+    ty = (w.cameras[0].height + 15) // 16
+    allt = np.array([(0, x, y) for y in range(ty) for x in range(tx)], np.int32)
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(len(allt))
+    halves = [allt[perm[: len(perm) // 2]], allt[perm[len(perm) // 2:]]]
+    img = torch.zeros((1, w.cameras[0].height, w.cameras[0].width, 4), device="cuda")
+    m = gpu_model(c)
+    tot = 0
+    for h in halves:
+        t = cuda(h)
+        s = torch.zeros(1, dtype=torch.int64, device="cuda")
+        packed = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params, tiles=t, samples=s)
+        unpack_tiles(packed, t, 1, w.cameras[0].width, w.cameras[0].height, out=img)
+        torch.cuda.synchronize()
+        tot += int(s.item())
+    np.testing.assert_array_equal(img.cpu().numpy(), full)
+    assert tot == ns_full
+
+
+def test_ragged_image_and_fp16():
+    """Image sizes that are not multiples of the 16x16 tile, fp16 output."""
+    c = 2
+    w = workload(c, width=100, height=75)
+    img, _ = render_gpu(c, w=w)
+    ref = O.render(oracle_model(c), w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
+    parity.check_image(img[0].reshape(-1, 4), ref, "C2 100x75")
+    img16, _ = render_gpu(c, w=w, out_fp16=True)
+    assert np.abs(img16 - img).max() <= 1e-3
+
+
+def test_multiview_batch_matches_single_views():
+    c = 5
+    w = workload(c, width=64, height=48, n_views=3)
+    img, _ = render_gpu(c, w=w)
+    for v in range(3):
+        one = WL.make_config(c, width=64, height=48, n_views=3)
+        one.cameras = [w.cameras[v]]
+        iv, _ = render_gpu(c, w=one)
+        np.testing.assert_array_equal(iv[0], img[v])
+
+
+def test_render_host_matches_device():
+    c = 1
+    w = workload(c)
+    dev, ns = render_gpu(c)
+    out = torch.empty((1, 64, 64, 4), dtype=torch.float32).pin_memory()
+    n2 = gpu_model(c).render_host(w.cameras, w.tf, w.v_lo, w.v_hi, w.params, out)
+    np.testing.assert_array_equal(out.numpy(), dev)
+    assert n2 == ns
+
+
+def test_shading_off_parity():
+    import dataclasses
+    c = 2
+    w = workload(c)
+    prm = dataclasses.replace(w.params, shading=0)
+    m = gpu_model(c)
+    img = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, prm)
+    torch.cuda.synchronize()
+    ref = O.render(oracle_model(c), w.cameras[0], w.tf, w.v_lo, w.v_hi, prm)
+    parity.check_image(img[0].cpu().numpy().reshape(-1, 4), ref, "C2 shading off")
+
+
+def test_camera_inside_volume_and_ortho_axis_aligned():
+    """Degenerate geometry: eye inside the box (t_in = 0); axis-aligned
+    orthographic rays (d components exactly 0)."""
+    c = 1
+    w = WL.make_config(c)
+    w.cameras = [WL.Camera(eye=(0.05, -0.1, 0.02), look_at=(0.3, 0.2, -0.1), up=(0, 0, 1), fov_y_deg=60.0,
+                           ortho_half_height=0.0, width=40, height=30),
+                 WL.Camera(eye=(0.0, 0.0, 2.0), look_at=(0.0, 0.0, 0.0), up=(0, 1, 0), fov_y_deg=0.0,
+                           ortho_half_height=0.6, width=40, height=30)]
+    img, _ = render_gpu(c, w=w)
+    for v in range(2):
+        ref = O.render(oracle_model(c), w.cameras[v], w.tf, w.v_lo, w.v_hi, w.params)
+        parity.check_image(img[v].reshape(-1, 4), ref, f"geometry view {v}")
+
+
+def test_invalid_models_raise():
+    from paper_2204_11762_b200 import MfaError, Model
+    p = 2
+    good = np.concatenate([np.zeros(3), [0.5], np.ones(3)])
+    ctrl = np.zeros((4, 4, 4), np.float32)
+    bad = good.copy()
+    bad[3] = 1.5
+    with pytest.raises(MfaError, match="KNOTS"):
+        Model(p, [good, bad, good], ctrl)
+    with pytest.raises(MfaError, match="UNSUPPORTED"):
+        Model((2, 3, 2), [good, good, good], ctrl)
+    nanc = ctrl.copy()
+    nanc[1, 2, 3] = np.nan
+    with pytest.raises(MfaError, match="DOMAIN"):
+        Model(p, [good, good, good], nanc)
+    m = Model(p, [good, good, good], ctrl + 2)
+    info = m.info()
+    assert info["v_min"] == 2 and info["v_max"] == 2 and info["uniform"] == (1, 1, 1)
