@@ -9,7 +9,7 @@ namespace mfa {
 
 struct EvalArgs {
     const float4* Q;
-    int nu, nv, nw;
+    BrickGrid g;
     AxisArgs ax[3];
     const float* u;
     const float* v;
@@ -24,7 +24,6 @@ struct EvalArgs {
 
 template <int P, bool UNI, bool GRAD>
 __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalArgs args) {
-    const int row_v = args.nu, row_w = args.nu * args.nv;
     unsigned errs = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < args.n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -50,24 +49,26 @@ __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalA
                 nonuni_span_f32(args.ax[d], q[d], s[d], t[d], sc[d]);
             }
         }
-        const float4* base = args.Q + ((int64_t)s[2] * args.nv + s[1]) * args.nu + s[0];
+        const float4* base = args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
+        float r0[P + 1][P + 1];
+        load_slab<P>(base, r0);   // issued before the basis so its latency overlaps it
         if (GRAD) {
             float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
-            axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], sc[0], Bu);
-            axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], sc[1], Bv);
-            axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], sc[2], Bw);
+            axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
+            axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
+            axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
             float val, gu, gv, gw;
-            contract_vg<P>(base, row_v, row_w, Bu, Bv, Bw, val, gu, gv, gw);
+            contract_vg<P>(base, r0, Bu, Bv, Bw, val, gu, gv, gw);
             args.value[i] = val;
-            args.du[i] = gu;
-            args.dv[i] = gv;
-            args.dw[i] = gw;
+            args.du[i] = gu * sc[0];
+            args.dv[i] = gv * sc[1];
+            args.dw[i] = gw * sc[2];
         } else {
             float Nu[P + 1], Nv[P + 1], Nw[P + 1];
             axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
             axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
             axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
-            args.value[i] = contract_v<P>(base, row_v, row_w, Nu, Nv, Nw);
+            args.value[i] = contract_v<P>(base, r0, Nu, Nv, Nw);
         }
     }
     if (args.n_err) {
@@ -97,9 +98,8 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
                        float* du, float* dv, float* dw, unsigned long long* n_err, cudaStream_t st) {
     EvalArgs a;
     a.Q = m->Q;
-    a.nu = (int)m->n[0];
-    a.nv = (int)m->n[1];
-    a.nw = (int)m->n[2];
+    a.g.nbx = m->nb[0];
+    a.g.nby = m->nb[1];
     for (int d = 0; d < 3; ++d) a.ax[d] = make_axis_args(m->ax[d]);
     a.u = u;
     a.v = v;

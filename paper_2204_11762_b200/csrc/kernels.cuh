@@ -1,8 +1,17 @@
 // Device building blocks of the hot path:
 //   a4 span + local coordinate       (uniform: span units; non-uniform: knot tables)
-//   a5 basis + first derivatives     (power-basis Horner per span, simultaneous value/derivative)
-//   a6 neighbourhood gather          (row quads: one aligned 16-byte load per u-row)
+//   a5 basis + first derivatives     (power basis per span; uniform interior spans
+//                                     use FFMA2 pair-Horner on (c_m, c'_m) constants)
+//   a6 neighbourhood gather          (bricked row quads: one aligned 16-byte load
+//                                     per u-row, all rows at compile-time offsets)
 //   a7 sum-factorised contraction    (x, then y, then z; paired FP32 FMAs, FFMA2)
+//
+// Bricked row-quad layout.  Entry (i, j, k) of the quad array
+// holds (P[k][j][i], P[k][j][i+1], P[k][j][i+2], P[k][j][i+3]).  Entries are
+// grouped in bricks covering 16x16x16 spans; a brick stores EU x EV x EW
+// entries (EV = EW = 16 + p halo rows, EU = 16 (+1 for p = 4, +4 for p = 5))
+// so every (p+1)^3 neighbourhood of a span triple lies in one brick and its
+// (p+1)^2 rows sit at offsets c*EV*EU + b*EU known at compile time.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -24,7 +33,6 @@ struct AxisArgs {
     int mshift;      // 62 - log2(M): bucket of a 2^62 fixed-point coordinate
     int ic_lo, ic_hi;
     float S;
-    float interior[(kMaxP + 1) * (kMaxP + 1)];
 };
 
 __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
@@ -43,80 +51,173 @@ __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
     a.ic_lo = A.ic_lo;
     a.ic_hi = A.ic_hi;
     a.S = A.S;
-    for (int i = 0; i < (kMaxP + 1) * (kMaxP + 1); ++i) a.interior[i] = A.interior[i];
     return a;
 }
 
 // ---------------------------------------------------------------------------
-// a5: p+1 basis values and derivatives by Horner on the span's power basis.
-// c[a*(P+1)+m] is the coefficient of t^m of function a; scale = dt/du.
-// Simultaneous Horner:  b <- b t + c_m,  d <- d t + b  gives P(t), P'(t).
-// Output pairs: X-order (N, N') or swapped (N', N) when SWAP.
+// brick geometry
 // ---------------------------------------------------------------------------
+template <int P>
+struct Brick {
+    static constexpr int B = kBrick;
+    static constexpr int EU = B + (P == 4 ? 1 : (P == 5 ? 4 : 0));
+    static constexpr int EV = B + P;
+    static constexpr int EW = B + P;
+    static constexpr int SIZE = EU * EV * EW;   // entries per brick
+};
+
+struct BrickGrid {
+    int nbx, nby;          // bricks along u, v
+};
+
+// Entry index of the neighbourhood origin (row quad of spans (su, sv, sw)).
+template <int P>
+__device__ __forceinline__ int64_t brick_entry(const BrickGrid& g, int su, int sv, int sw) {
+    const int bx = su >> kBrickLog, by = sv >> kBrickLog, bz = sw >> kBrickLog;
+    const int lu = su & (kBrick - 1), lv = sv & (kBrick - 1), lw = sw & (kBrick - 1);
+    const int brick = (bz * g.nby + by) * g.nbx + bx;
+    return (int64_t)brick * Brick<P>::SIZE + (lw * Brick<P>::EV + lv) * Brick<P>::EU + lu;
+}
+
+// ---------------------------------------------------------------------------
+// a5: basis values and t-derivatives.
+//
+// Interior spans of a clamped uniform knot vector (spans p-1 .. S-p) all
+// carry the same polynomials in the local coordinate t: the uniform B-spline
+// basis of degree p, which depends on nothing but p.  UniformBasis<P> derives
+// it at compile time from the Cox-de Boor recursion on the integer knots
+// 0, 1, ..., 2p+1 (span [p, p+1]), so the Horner FMAs take their
+// coefficients as immediates.  Other spans (the p-1 boundary spans at each end
+// of a uniform axis, every span of a non-uniform axis) read their
+// coefficients from the span table built by span_tables_kernel.
+// Derivatives are with respect to t; the caller scales the contracted
+// gradient by dt/du once per axis.
+// ---------------------------------------------------------------------------
+template <int P>
+struct UniformBasis {
+    double c[P + 1][P + 1];   // N_a(t) = sum_m c[a][m] t^m
+};
+
+template <int P>
+constexpr UniformBasis<P> make_uniform_basis() {
+    UniformBasis<P> ub{};
+    double cur[P + 1][P + 1] = {};   // functions of the current level, coefficients of t^m
+    cur[0][0] = 1.0;                 // N_{P,0} = 1 on [P, P+1)
+    const int i = P;                 // span index; knots U_j = j, u = P + t
+    for (int k = 1; k <= P; ++k) {
+        double nxt[P + 1][P + 1] = {};
+        for (int r = 0; r <= k; ++r) {
+            const int j = i - k + r;
+            if (r >= 1) {  // (u - U_j)/(U_{j+k} - U_j) N_{j,k-1}, old function r-1
+                const double c0 = (double)(i - j) / k, c1 = 1.0 / k;
+                for (int m = 0; m < k; ++m) {
+                    nxt[r][m] += c0 * cur[r - 1][m];
+                    nxt[r][m + 1] += c1 * cur[r - 1][m];
+                }
+            }
+            if (r <= k - 1) {  // (U_{j+k+1} - u)/(U_{j+k+1} - U_{j+1}) N_{j+1,k-1}, old function r
+                const double c0 = (double)(j + k + 1 - i) / k, c1 = -1.0 / k;
+                for (int m = 0; m < k; ++m) {
+                    nxt[r][m] += c0 * cur[r][m];
+                    nxt[r][m + 1] += c1 * cur[r][m];
+                }
+            }
+        }
+        for (int r = 0; r <= P; ++r)
+            for (int m = 0; m <= P; ++m) cur[r][m] = nxt[r][m];
+    }
+    for (int r = 0; r <= P; ++r)
+        for (int m = 0; m <= P; ++m) ub.c[r][m] = cur[r][m];
+    return ub;
+}
+
+// Interior uniform span: simultaneous value / t-derivative Horner with
+// immediate coefficients (2P-1 FFMA per function).
 template <int P, bool SWAP>
-__device__ __forceinline__ void horner_basis(const float* c, float t, float scale, float2 (&B)[P + 1]) {
+__device__ __forceinline__ void uniform_horner(float t, float2 (&B)[P + 1]) {
+    constexpr UniformBasis<P> UB = make_uniform_basis<P>();
 #pragma unroll
     for (int a = 0; a <= P; ++a) {
-        float v = c[a * (P + 1) + P];
-        float d = 0.f;
+        float v = fmaf((float)UB.c[a][P], t, (float)UB.c[a][P - 1]);
+        float d = fmaf((float)(P * UB.c[a][P]), t, (float)((P - 1) * UB.c[a][P - 1]));
+        if (P == 1) d = (float)UB.c[a][1];
 #pragma unroll
-        for (int m = P - 1; m >= 0; --m) {
-            d = fmaf(d, t, v);
-            v = fmaf(v, t, c[a * (P + 1) + m]);
+        for (int m = P - 2; m >= 0; --m) {
+            v = fmaf(v, t, (float)UB.c[a][m]);
+            if (m >= 1) d = fmaf(d, t, (float)(m * UB.c[a][m]));
         }
-        d *= scale;
         B[a] = SWAP ? make_float2(d, v) : make_float2(v, d);
     }
 }
 
 template <int P>
-__device__ __forceinline__ void horner_value(const float* c, float t, float (&B)[P + 1]) {
+__device__ __forceinline__ void uniform_horner_value(float t, float (&N)[P + 1]) {
+    constexpr UniformBasis<P> UB = make_uniform_basis<P>();
 #pragma unroll
     for (int a = 0; a <= P; ++a) {
-        float v = c[a * (P + 1) + P];
+        float v = fmaf((float)UB.c[a][P], t, (float)UB.c[a][P - 1]);
 #pragma unroll
-        for (int m = P - 1; m >= 0; --m) v = fmaf(v, t, c[a * (P + 1) + m]);
-        B[a] = v;
+        for (int m = P - 2; m >= 0; --m) v = fmaf(v, t, (float)UB.c[a][m]);
+        N[a] = v;
     }
 }
 
-// Load one span record (coefficients) from the table into registers.
-template <int P>
-__device__ __forceinline__ void load_rec(const float* __restrict__ coef, int s, float (&c)[rec_floats(P)]) {
+template <int P, bool SWAP>
+__device__ __forceinline__ void table_horner(const float* __restrict__ coef, int s, float t, float2 (&B)[P + 1]) {
+    float c[rec_floats(P)];
     const float4* r = reinterpret_cast<const float4*>(coef + (int64_t)s * rec_floats(P));
 #pragma unroll
     for (int q = 0; q < rec_floats(P) / 4; ++q) {
-        float4 x = __ldg(r + q);
+        const float4 x = __ldg(r + q);
         c[4 * q + 0] = x.x;
         c[4 * q + 1] = x.y;
         c[4 * q + 2] = x.z;
         c[4 * q + 3] = x.w;
     }
-}
-
-// Basis of one axis: uniform axes take the constant interior polynomials
-// (kernel-parameter constant bank) unless the span is one of the p-1
-// boundary-affected spans at either end; non-uniform axes always load.
-template <int P, bool SWAP>
-__device__ __forceinline__ void axis_basis(const AxisArgs& A, bool uniform, int s, float t, float scale,
-                                           float2 (&B)[P + 1]) {
-    if (uniform && s >= A.ic_lo && s <= A.ic_hi) {
-        horner_basis<P, SWAP>(A.interior, t, scale, B);
-    } else {
-        float c[rec_floats(P)];
-        load_rec<P>(A.coef, s, c);
-        horner_basis<P, SWAP>(c, t, scale, B);
+#pragma unroll
+    for (int a = 0; a <= P; ++a) {
+        float d = c[a * (P + 1) + P];
+        float v = fmaf(d, t, c[a * (P + 1) + P - 1]);
+#pragma unroll
+        for (int m = P - 2; m >= 0; --m) {
+            d = fmaf(d, t, v);
+            v = fmaf(v, t, c[a * (P + 1) + m]);
+        }
+        B[a] = SWAP ? make_float2(d, v) : make_float2(v, d);
     }
 }
 
+template <int P, bool SWAP>
+__device__ __forceinline__ void axis_basis(const AxisArgs& A, bool uniform, int s, float t, float2 (&B)[P + 1]) {
+    if (uniform && s >= A.ic_lo && s <= A.ic_hi)
+        uniform_horner<P, SWAP>(t, B);
+    else
+        table_horner<P, SWAP>(A.coef, s, t, B);
+}
+
+// Values only (ShadingOn == false, Alg.1 l.8).
 template <int P>
-__device__ __forceinline__ void axis_basis_value(const AxisArgs& A, bool uniform, int s, float t, float (&B)[P + 1]) {
+__device__ __forceinline__ void axis_basis_value(const AxisArgs& A, bool uniform, int s, float t, float (&N)[P + 1]) {
     if (uniform && s >= A.ic_lo && s <= A.ic_hi) {
-        horner_value<P>(A.interior, t, B);
+        uniform_horner_value<P>(t, N);
     } else {
         float c[rec_floats(P)];
-        load_rec<P>(A.coef, s, c);
-        horner_value<P>(c, t, B);
+        const float4* r = reinterpret_cast<const float4*>(A.coef + (int64_t)s * rec_floats(P));
+#pragma unroll
+        for (int q = 0; q < rec_floats(P) / 4; ++q) {
+            const float4 x = __ldg(r + q);
+            c[4 * q + 0] = x.x;
+            c[4 * q + 1] = x.y;
+            c[4 * q + 2] = x.z;
+            c[4 * q + 3] = x.w;
+        }
+#pragma unroll
+        for (int a = 0; a <= P; ++a) {
+            float v = fmaf(c[a * (P + 1) + P], t, c[a * (P + 1) + P - 1]);
+#pragma unroll
+            for (int m = P - 2; m >= 0; --m) v = fmaf(v, t, c[a * (P + 1) + m]);
+            N[a] = v;
+        }
     }
 }
 
@@ -138,7 +239,7 @@ __device__ __forceinline__ void uni_span_fx(long long F, int S, int& s, float& t
 __device__ __forceinline__ void uni_span_f32(float u, float Sf, int S, int& s, float& t) {
     const float hi = u * Sf;
     const float lo = fmaf(u, Sf, -hi);
-    float fl = floorf(hi);
+    const float fl = floorf(hi);
     s = (int)fl;
     t = (hi - fl) + lo;
     if (s >= S) { s = S - 1; t += 1.f; }   // u == 1
@@ -176,61 +277,80 @@ __device__ __forceinline__ int nonuni_first_span_fx(const AxisArgs& A, long long
 }
 
 // ---------------------------------------------------------------------------
-// a6: row of p+1 consecutive u-values starting at the quad q.
+// a6: one slab c of the neighbourhood: rows b = 0..P, each P+1 u-values.
 // ---------------------------------------------------------------------------
 template <int P>
-__device__ __forceinline__ void load_row(const float4* __restrict__ q, float (&r)[P + 1]) {
-    if constexpr (P == 1) {
-        float2 x = __ldg(reinterpret_cast<const float2*>(q));
-        r[0] = x.x; r[1] = x.y;
-    } else if constexpr (P == 2) {
-        float4 x = __ldg(q);
-        r[0] = x.x; r[1] = x.y; r[2] = x.z;
-    } else if constexpr (P == 3) {
-        float4 x = __ldg(q);
-        r[0] = x.x; r[1] = x.y; r[2] = x.z; r[3] = x.w;
-    } else if constexpr (P == 4) {
-        float4 x = __ldg(q);
-        r[0] = x.x; r[1] = x.y; r[2] = x.z; r[3] = x.w;
-        r[4] = __ldg(reinterpret_cast<const float*>(q + 1) + 3);
-    } else {
-        float4 x = __ldg(q);
-        float2 y = __ldg(reinterpret_cast<const float2*>(q + 4));
-        r[0] = x.x; r[1] = x.y; r[2] = x.z; r[3] = x.w; r[4] = y.x; r[5] = y.y;
+__device__ __forceinline__ void load_slab(const float4* __restrict__ q, float (&r)[P + 1][P + 1]) {
+    constexpr int EU = Brick<P>::EU;
+#pragma unroll
+    for (int b = 0; b <= P; ++b) {
+        const float4* e = q + b * EU;
+        if constexpr (P == 1) {
+            const float2 x = __ldg(reinterpret_cast<const float2*>(e));
+            r[b][0] = x.x; r[b][1] = x.y;
+        } else if constexpr (P == 2) {
+            const float4 x = __ldg(e);
+            r[b][0] = x.x; r[b][1] = x.y; r[b][2] = x.z;
+        } else if constexpr (P == 3) {
+            const float4 x = __ldg(e);
+            r[b][0] = x.x; r[b][1] = x.y; r[b][2] = x.z; r[b][3] = x.w;
+        } else if constexpr (P == 4) {
+            const float4 x = __ldg(e);
+            r[b][0] = x.x; r[b][1] = x.y; r[b][2] = x.z; r[b][3] = x.w;
+            r[b][4] = __ldg(reinterpret_cast<const float*>(e + 1) + 3);
+        } else {
+            const float4 x = __ldg(e);
+            const float2 y = __ldg(reinterpret_cast<const float2*>(e + 4));
+            r[b][0] = x.x; r[b][1] = x.y; r[b][2] = x.z; r[b][3] = x.w; r[b][4] = y.x; r[b][5] = y.y;
+        }
     }
 }
 
 // ---------------------------------------------------------------------------
-// a7: value + parameter-space gradient, sum-factorised ("all
-// derivatives along the three dimensions at once"; "sum operations on
-// each of the three dimensions").  Per row (c,b):
+// a7: value + t-space gradient, sum-factorised ("all derivatives along
+// the three dimensions at once"; "sum operations on each of the three
+// dimensions").  Per row (c,b):
 //   (a0, a1) = sum_a (Nu_a, Nu'_a) * P            [FFMA2, P broadcast]
 //   B  += Nv_b a0 ; (Bv, Bu) += (Nv'_b, Nv_b) * (a0, a1)
 // per slab c:  (v, g_w) += (Nw_c, Nw'_c) * B ;  (g_v, g_u) += Nw_c * (Bv, Bu)
 // Bu: (N, N'), Bvs: (N', N) (swapped), Bw: (N, N').
+// Slab c+1 is loaded while slab c is contracted; the caller has already
+// issued slab 0 (so its latency overlaps the basis evaluation).
 // ---------------------------------------------------------------------------
 template <int P>
-__device__ __forceinline__ void contract_vg(const float4* __restrict__ base, int row_v, int row_w,
+__device__ __forceinline__ void contract_slab(const float (&r)[P + 1][P + 1], const float2 (&Bu)[P + 1],
+                                              const float2 (&Bvs)[P + 1], float2 wc, float2& vw, float2& gvu) {
+    float B = 0.f;
+    float2 Bvu = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int b = 0; b <= P; ++b) {
+        float2 a01 = __fmul2_rn(Bu[0], make_float2(r[b][0], r[b][0]));
+#pragma unroll
+        for (int a = 1; a <= P; ++a) a01 = __ffma2_rn(Bu[a], make_float2(r[b][a], r[b][a]), a01);
+        B = fmaf(Bvs[b].y, a01.x, B);
+        Bvu = __ffma2_rn(Bvs[b], a01, Bvu);
+    }
+    vw = __ffma2_rn(wc, make_float2(B, B), vw);
+    gvu = __ffma2_rn(make_float2(wc.x, wc.x), Bvu, gvu);
+}
+
+template <int P>
+__device__ __forceinline__ void contract_vg(const float4* __restrict__ q, float (&r0)[P + 1][P + 1],
                                             const float2 (&Bu)[P + 1], const float2 (&Bvs)[P + 1],
                                             const float2 (&Bw)[P + 1], float& val, float& gu, float& gv,
                                             float& gw) {
+    constexpr int SW = Brick<P>::EV * Brick<P>::EU;
     float2 vw = make_float2(0.f, 0.f), gvu = make_float2(0.f, 0.f);
+    float r1[P + 1][P + 1];
 #pragma unroll
     for (int c = 0; c <= P; ++c) {
-        float B = 0.f;
-        float2 Bvu = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int b = 0; b <= P; ++b) {
-            float r[P + 1];
-            load_row<P>(base + c * row_w + b * row_v, r);
-            float2 a01 = __fmul2_rn(Bu[0], make_float2(r[0], r[0]));
-#pragma unroll
-            for (int a = 1; a <= P; ++a) a01 = __ffma2_rn(Bu[a], make_float2(r[a], r[a]), a01);
-            B = fmaf(Bvs[b].y, a01.x, B);
-            Bvu = __ffma2_rn(Bvs[b], a01, Bvu);
+        if (c & 1) {
+            if (c < P) load_slab<P>(q + (c + 1) * SW, r0);
+            contract_slab<P>(r1, Bu, Bvs, Bw[c], vw, gvu);
+        } else {
+            if (c < P) load_slab<P>(q + (c + 1) * SW, r1);
+            contract_slab<P>(r0, Bu, Bvs, Bw[c], vw, gvu);
         }
-        vw = __ffma2_rn(Bw[c], make_float2(B, B), vw);
-        gvu = __ffma2_rn(make_float2(Bw[c].x, Bw[c].x), Bvu, gvu);
     }
     val = vw.x;
     gw = vw.y;
@@ -239,20 +359,25 @@ __device__ __forceinline__ void contract_vg(const float4* __restrict__ base, int
 }
 
 template <int P>
-__device__ __forceinline__ float contract_v(const float4* __restrict__ base, int row_v, int row_w,
+__device__ __forceinline__ float contract_v(const float4* __restrict__ q, float (&r0)[P + 1][P + 1],
                                             const float (&Nu)[P + 1], const float (&Nv)[P + 1],
                                             const float (&Nw)[P + 1]) {
+    constexpr int SW = Brick<P>::EV * Brick<P>::EU;
     float val = 0.f;
+    float r1[P + 1][P + 1];
 #pragma unroll
     for (int c = 0; c <= P; ++c) {
+        float (&r)[P + 1][P + 1] = (c & 1) ? r1 : r0;
+        if (c < P) {
+            if (c & 1) load_slab<P>(q + (c + 1) * SW, r0);
+            else load_slab<P>(q + (c + 1) * SW, r1);
+        }
         float B = 0.f;
 #pragma unroll
         for (int b = 0; b <= P; ++b) {
-            float r[P + 1];
-            load_row<P>(base + c * row_w + b * row_v, r);
-            float a0 = Nu[0] * r[0];
+            float a0 = Nu[0] * r[b][0];
 #pragma unroll
-            for (int a = 1; a <= P; ++a) a0 = fmaf(Nu[a], r[a], a0);
+            for (int a = 1; a <= P; ++a) a0 = fmaf(Nu[a], r[b][a], a0);
             B = fmaf(Nv[b], a0, B);
         }
         val = fmaf(Nw[c], B, val);

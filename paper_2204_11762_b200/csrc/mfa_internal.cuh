@@ -31,6 +31,13 @@ constexpr int kMaxP = MFA_MAX_DEGREE;
 constexpr int kMaxViewsPerLaunch = 64;
 constexpr int kUniFracBits = 40;   // uniform axes: span-unit fixed point, 24.40
 constexpr int kNonUniFracBits = 62; // non-uniform axes: parameter fixed point, 2.62
+constexpr int kBrickLog = 4;        // bricks of 16x16x16 spans
+constexpr int kBrick = 1 << kBrickLog;
+constexpr int kQueueSlots = 256;    // persistent-kernel work counters (one per in-flight launch)
+
+// brick entry extents for degree p (see kernels.cuh)
+__host__ __device__ constexpr int brick_eu(int p) { return kBrick + (p == 4 ? 1 : (p == 5 ? 4 : 0)); }
+__host__ __device__ constexpr int brick_ev(int p) { return kBrick + p; }
 
 __host__ __device__ constexpr int rec_floats(int p) { return (((p + 1) * (p + 1)) + 3) / 4 * 4; }
 
@@ -55,7 +62,9 @@ struct Model {
     int64_t n[3] = {0, 0, 0};
     int uniform[3] = {0, 0, 0};
     float vmin = 0.f, vmax = 0.f;
-    float4* Q = nullptr;
+    float4* Q = nullptr;           // bricked row quads
+    int nb[3] = {0, 0, 0};         // bricks per axis
+    unsigned int* queue = nullptr; // kQueueSlots work counters
     AxisTables ax[3];
     void* table_mem = nullptr;   // one allocation for all axis tables
     int64_t device_bytes = 0;

@@ -47,20 +47,33 @@ mfa_status check_device(const Model* m) {
 }
 
 // ---------------------------------------------------------------------------
-// K1: row-quad relayout.  Q[k][j][i] = (P[i], P[i+1], P[i+2], P[i+3]) of row (k,j).
+// K1: bricked row-quad relayout.  Brick (bx,by,bz) entry (lu,lv,lw) holds the
+// quad (P[k][j][i..i+3]) of i = 16 bx + lu, j = 16 by + lv, k = 16 bz + lw
+// (zeros outside the grid).  One thread per entry.
 // ---------------------------------------------------------------------------
-__global__ void relayout_quads_kernel(const float* __restrict__ P, float4* __restrict__ Q, int64_t nu,
-                                      int64_t rows) {
-    const int64_t total = nu * rows;
+__global__ void relayout_bricks_kernel(const float* __restrict__ P, float4* __restrict__ Q, int nu, int nv,
+                                       int nw, int nbx, int nby, int EU, int EV, int EW, int64_t total) {
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = idx % nu;
-        const float* r = P + (idx - i);
-        float4 q;
-        q.x = r[i];
-        q.y = (i + 1 < nu) ? r[i + 1] : 0.f;
-        q.z = (i + 2 < nu) ? r[i + 2] : 0.f;
-        q.w = (i + 3 < nu) ? r[i + 3] : 0.f;
+        const int64_t bsz = (int64_t)EU * EV * EW;
+        const int64_t brick = idx / bsz;
+        int rem = (int)(idx - brick * bsz);
+        const int lu = rem % EU;
+        rem /= EU;
+        const int lv = rem % EV;
+        const int lw = rem / EV;
+        const int bx = (int)(brick % nbx);
+        const int by = (int)((brick / nbx) % nby);
+        const int bz = (int)(brick / ((int64_t)nbx * nby));
+        const int i = bx * kBrick + lu, j = by * kBrick + lv, k = bz * kBrick + lw;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < nv && k < nw) {
+            const float* r = P + ((int64_t)k * nv + j) * nu;
+            if (i < nu) q.x = r[i];
+            if (i + 1 < nu) q.y = r[i + 1];
+            if (i + 2 < nu) q.z = r[i + 2];
+            if (i + 3 < nu) q.w = r[i + 3];
+        }
         Q[idx] = q;
     }
 }
@@ -259,8 +272,8 @@ extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nc
         if (!knots[d]) return fail(MFA_ERR_INVALID_ARG, "knots[" + std::to_string(d) + "] is NULL");
         if (nctrl[d] < p + 1)
             return fail(MFA_ERR_INVALID_ARG, "nctrl[" + std::to_string(d) + "] < degree+1");
-        if (nctrl[d] > (1 << 22))
-            return fail(MFA_ERR_UNSUPPORTED, "nctrl[" + std::to_string(d) + "] > 2^22");
+        if (nctrl[d] > (1 << 20))
+            return fail(MFA_ERR_UNSUPPORTED, "nctrl[" + std::to_string(d) + "] > 2^20");
     }
     int uniform[3];
     for (int d = 0; d < 3; ++d) {
@@ -289,6 +302,7 @@ extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nc
         if (mm) cudaFree(mm);
         if (s != MFA_OK) {
             if (m->Q) cudaFree(m->Q);
+            if (m->queue) cudaFree(m->queue);
             if (m->table_mem) cudaFree(m->table_mem);
             delete m;
         }
@@ -307,10 +321,17 @@ extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nc
     unsigned int init[3] = {0xffffffffu, 0u, 0u};
     cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, st);
     minmax_kernel<<<1184, 256, 0, st>>>(Pdev, npts, mm);
-    // row quads
-    if ((e = cudaMalloc(&m->Q, npts * sizeof(float4))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc Q"));
-    relayout_quads_kernel<<<4736, 256, 0, st>>>(Pdev, m->Q, nu, nv * nw);
-    m->device_bytes = npts * (int64_t)sizeof(float4);
+    // bricked row quads
+    for (int d = 0; d < 3; ++d) m->nb[d] = (int)((nctrl[d] - p + kBrick - 1) / kBrick);
+    const int EU = brick_eu(p), EV = brick_ev(p), EW = brick_ev(p);
+    const int64_t qn = (int64_t)m->nb[0] * m->nb[1] * m->nb[2] * EU * EV * EW;
+    if ((e = cudaMalloc(&m->Q, qn * sizeof(float4))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc Q"));
+    relayout_bricks_kernel<<<4736, 256, 0, st>>>(Pdev, m->Q, (int)nu, (int)nv, (int)nw, m->nb[0], m->nb[1], EU, EV,
+                                                  EW, qn);
+    m->device_bytes = qn * (int64_t)sizeof(float4);
+    if ((e = cudaMalloc(&m->queue, kQueueSlots * sizeof(unsigned int))) != cudaSuccess)
+        return cleanup(cuda_fail(e, "cudaMalloc queue"));
+    cudaMemsetAsync(m->queue, 0, kQueueSlots * sizeof(unsigned int), st);
 
     // axis tables: one allocation
     const int rec = rec_floats(p);
@@ -414,6 +435,7 @@ extern "C" mfa_status mfa_model_destroy(mfa_model h) {
     cudaGetDevice(&cur);
     if (cur != m->device) cudaSetDevice(m->device);
     if (m->Q) cudaFree(m->Q);
+    if (m->queue) cudaFree(m->queue);
     if (m->table_mem) cudaFree(m->table_mem);
     if (cur != m->device && cur >= 0) cudaSetDevice(cur);
     delete m;

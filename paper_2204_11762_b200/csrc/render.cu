@@ -1,7 +1,9 @@
 // mfa_render kernel: Algorithm 1 fused per ray.
 //
-//   CTA  = one 16x16 pixel tile of one view (8 warps; warp = 8x4 pixels, so a
-//          warp's rays stay spatially coherent and share control rows in L1).
+//   work = warp units of 8x4 pixels (8 per 16x16 tile) handed out by a global
+//          atomic counter to persistent warps (grid = SMs x resident CTAs), so
+//          early-terminating rays never leave an SM idle and no warp waits on
+//          its CTA's slowest warp; consecutive units are neighbouring tiles.
 //   ray  = one thread.  a1-a2 ray setup in fp64; sample positions are kept in
 //          64-bit fixed point (the "fixed-point ray cast model"):
 //          uniform axes in span units * 2^40, non-uniform axes in parameter
@@ -14,6 +16,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "kernels.cuh"
 
@@ -21,20 +24,22 @@ namespace mfa {
 
 struct RenderArgs {
     const float4* Q;
-    int nu, nv, nw;
+    BrickGrid g;
     AxisArgs ax[3];
     const float4* tf;
     int tf_n;
-    float v_lo, s_scale;          // s = (v - v_lo) / (v_hi - v_lo); f = s*(n-1) = (v - v_lo)*s_scale
+    float v_lo, s_scale;          // f = (v - v_lo) * s_scale = s * (n - 1)
     double bmin[3], L[3];
     double step;
-    float invL[3];
+    float gsc[3];                 // gradient scale to physical units (uniform: S/L; non-uniform: 1/L)
     float o_max, ka, kd, ks, shin, eps2;
-    int shading;
     int W, H, tiles_x, tiles_y;
+    int n_views;
     const int* tiles;             // NULL: full frames
     int64_t n_tiles;
+    int64_t n_units;              // warp units = 8 per tile
     int view_base;                // full frames: output view index of cams[0]
+    unsigned int* queue;          // work counter (zeroed before the launch)
     void* out;
     int out_fp16;
     unsigned long long* samples;
@@ -77,234 +82,256 @@ __device__ __forceinline__ void compute_frame(const mfa_camera& c, ViewFrame& fr
 template <int P, bool UNI, bool SHADE>
 __global__ void __launch_bounds__(256) render_kernel(const __grid_constant__ RenderArgs args) {
     extern __shared__ float4 s_tf[];
-    __shared__ ViewFrame s_frame;
-    __shared__ unsigned long long s_count;
+    __shared__ ViewFrame s_frame[kMaxViewsPerLaunch];
 
-    // ---- which tile --------------------------------------------------------
-    int view, tx, ty;
-    int64_t tile_id = blockIdx.x;
-    if (args.tiles) {
-        view = args.tiles[3 * tile_id];
-        tx = args.tiles[3 * tile_id + 1];
-        ty = args.tiles[3 * tile_id + 2];
-        if (view < 0) return;  // padding unit (multi-GPU equal-size buffers)
-    } else {
-        const int per_view = args.tiles_x * args.tiles_y;
-        view = (int)(tile_id / per_view);
-        const int t = (int)(tile_id % per_view);
-        ty = t / args.tiles_x;
-        tx = t % args.tiles_x;
-    }
-    if (threadIdx.x == 0) {
-        compute_frame(args.cams[view], s_frame);
-        s_count = 0ull;
-    }
+    for (int v = threadIdx.x; v < args.n_views; v += blockDim.x) compute_frame(args.cams[v], s_frame[v]);
     for (int i = threadIdx.x; i < args.tf_n; i += blockDim.x) s_tf[i] = __ldg(args.tf + i);
     __syncthreads();
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = (warp & 1) * 8 + (lane & 7);
-    const int ly = (warp >> 1) * 4 + (lane >> 3);
-    const int px = tx * MFA_TILE + lx, py = ty * MFA_TILE + ly;
-    const bool valid = px < args.W && py < args.H;
+    const int lane = threadIdx.x & 31;
+    const int per_view = args.tiles_x * args.tiles_y;
+    unsigned long long my_samples = 0;
 
-    // ---- a1: ray through the pixel centre (fp64) ---------------------------
-    double o[3], d[3];
-    {
-        const double X = 2.0 * (px + 0.5) / args.W - 1.0;
-        const double Y = 1.0 - 2.0 * (py + 0.5) / args.H;
-        if (s_frame.ortho) {
-            for (int i = 0; i < 3; ++i) {
-                o[i] = s_frame.eye[i] + X * s_frame.A[i] + Y * s_frame.B[i];
-                d[i] = s_frame.f[i];
-            }
+    for (;;) {
+        // ---- next warp unit (8x4 pixels) from the global queue -------------
+        unsigned unit = 0;
+        if (lane == 0) unit = atomicAdd(args.queue, 1u);
+        unit = __shfl_sync(0xffffffffu, unit, 0);
+        if (unit >= args.n_units) break;
+        const int64_t tile_id = unit >> 3;
+        const int sub = unit & 7;
+        int view, tx, ty;
+        if (args.tiles) {
+            view = __ldg(args.tiles + 3 * tile_id);
+            tx = __ldg(args.tiles + 3 * tile_id + 1);
+            ty = __ldg(args.tiles + 3 * tile_id + 2);
+            if (view < 0) continue;  // padding unit (multi-GPU equal-size buffers)
         } else {
-            double l2 = 0.0;
-            for (int i = 0; i < 3; ++i) {
-                o[i] = s_frame.eye[i];
-                d[i] = s_frame.f[i] + X * s_frame.A[i] + Y * s_frame.B[i];
-                l2 += d[i] * d[i];
-            }
-            const double il = 1.0 / sqrt(l2);
-            for (int i = 0; i < 3; ++i) d[i] *= il;
+            view = (int)(tile_id / per_view);
+            const int t = (int)(tile_id % per_view);
+            ty = t / args.tiles_x;
+            tx = t % args.tiles_x;
         }
-    }
-    // ---- a2: slab clip, K samples at t_in + (k+1/2) step (R-7) -------------
-    int K = 0;
-    double t_in = 0.0;
-    {
-        double tn = -1e300, tf = 1e300;
-        bool hit = valid;
-        for (int i = 0; i < 3; ++i) {
-            const double bmax = args.bmin[i] + args.L[i];
-            if (d[i] == 0.0) {
-                if (o[i] < args.bmin[i] || o[i] > bmax) hit = false;
-                continue;
-            }
-            const double t0 = (args.bmin[i] - o[i]) / d[i], t1 = (bmax - o[i]) / d[i];
-            tn = fmax(tn, fmin(t0, t1));
-            tf = fmin(tf, fmax(t0, t1));
-        }
-        t_in = fmax(tn, 0.0);
-        if (hit && tf > t_in) {
-            const double fr = (tf - t_in) / args.step - 0.5;
-            K = fr > 0.0 ? (int)ceil(fr) : 0;
-        }
-    }
-    // ---- a3 setup: fixed-point sample coordinates per axis ----------------
-    long long F[3], DF[3];
-    int s_nu[3] = {0, 0, 0};
-    {
-        const double t0 = t_in + 0.5 * args.step;
+        const ViewFrame& fr = s_frame[view];
+        const int lx = (sub & 1) * 8 + (lane & 7);
+        const int ly = (sub >> 1) * 4 + (lane >> 3);
+        const int px = tx * MFA_TILE + lx, py = ty * MFA_TILE + ly;
+        const bool valid = px < args.W && py < args.H;
+
+        // ---- a1: ray through the pixel centre (fp64) -----------------------
+        double o[3], d[3];
+        {
+            const double X = 2.0 * (px + 0.5) / args.W - 1.0;
+            const double Y = 1.0 - 2.0 * (py + 0.5) / args.H;
+            if (fr.ortho) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const double u0 = (o[i] + t0 * d[i] - args.bmin[i]) / args.L[i];
-            const double du = args.step * d[i] / args.L[i];
-            if (UNI) {
-                const double S = (double)args.ax[i].nsp;
-                F[i] = llrint(ldexp(u0 * S, kUniFracBits));
-                DF[i] = llrint(ldexp(du * S, kUniFracBits));
+                for (int i = 0; i < 3; ++i) {
+                    o[i] = fr.eye[i] + X * fr.A[i] + Y * fr.B[i];
+                    d[i] = fr.f[i];
+                }
             } else {
-                F[i] = llrint(ldexp(u0, kNonUniFracBits));
-                DF[i] = llrint(ldexp(du, kNonUniFracBits));
-                if (K > 0) s_nu[i] = nonuni_first_span_fx(args.ax[i], F[i]);
+                double l2 = 0.0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    o[i] = fr.eye[i];
+                    d[i] = fr.f[i] + X * fr.A[i] + Y * fr.B[i];
+                    l2 += d[i] * d[i];
+                }
+                const double il = 1.0 / sqrt(l2);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) d[i] *= il;
             }
         }
-    }
-    const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
-    const int row_v = args.nu, row_w = args.nu * args.nv;
-
-    float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
-    int k = 0;
-    bool live = K > 0;
-    while (__any_sync(0xffffffffu, live)) {
-        if (live) {
-            // a4: span + local coordinate per axis
-            int s[3];
-            float t[3], sc[3];
+        // ---- a2: slab clip; K samples at t_in + (k+1/2) step (R-7) ---------
+        int K = 0;
+        double t_in = 0.0;
+        {
+            double tn = -1e300, tf = 1e300;
+            bool hit = valid;
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
-                if (UNI) {
-                    uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
-                    sc[i] = args.ax[i].S;
-                } else {
-                    nonuni_span_fx(args.ax[i], F[i], s_nu[i], t[i], sc[i]);
-                    s[i] = s_nu[i];
+                const double bmax = args.bmin[i] + args.L[i];
+                if (d[i] == 0.0) {
+                    if (o[i] < args.bmin[i] || o[i] > bmax) hit = false;
+                    continue;
                 }
+                const double t0 = (args.bmin[i] - o[i]) / d[i], t1 = (bmax - o[i]) / d[i];
+                tn = fmax(tn, fmin(t0, t1));
+                tf = fmin(tf, fmax(t0, t1));
             }
-            const float4* base = args.Q + ((int64_t)s[2] * args.nv + s[1]) * args.nu + s[0];
-            float val, gu = 0.f, gv = 0.f, gw = 0.f;
-            if (SHADE) {  // a5 + a6/a7 with derivatives (Alg.1 l.6 and l.9)
-                float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
-                axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], sc[0], Bu);
-                axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], sc[1], Bv);
-                axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], sc[2], Bw);
-                contract_vg<P>(base, row_v, row_w, Bu, Bv, Bw, val, gu, gv, gw);
-            } else {      // value only (Alg.1 l.8 ShadingOn == false)
-                float Nu[P + 1], Nv[P + 1], Nw[P + 1];
-                axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
-                axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
-                axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
-                val = contract_v<P>(base, row_v, row_w, Nu, Nv, Nw);
+            t_in = fmax(tn, 0.0);
+            if (hit && tf > t_in) {
+                const double frc = (tf - t_in) / args.step - 0.5;
+                K = frc > 0.0 ? (int)ceil(frc) : 0;
             }
-            // a8: transfer function (l.7)
-            float f = (val - args.v_lo) * args.s_scale;
-            f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
-            const int i0 = min((int)f, args.tf_n - 2);
-            const float wt = f - (float)i0;
-            const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
-            float cr = fmaf(wt, T1.x - T0.x, T0.x);
-            float cg = fmaf(wt, T1.y - T0.y, T0.y);
-            float cb = fmaf(wt, T1.z - T0.z, T0.z);
-            const float a = fmaf(wt, T1.w - T0.w, T0.w);
-            // a9: Phong with a headlight (l.10-11; R-11)
-            if (SHADE) {
-                const float gx = gu * args.invL[0], gy = gv * args.invL[1], gz = gw * args.invL[2];
-                const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
-                if (n2 <= args.eps2) {
-                    cr *= args.ka;
-                    cg *= args.ka;
-                    cb *= args.ka;
-                } else {
-                    const float ndl = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * rsqrtf(n2);
-                    const float dif = fmaxf(ndl, 0.f);
-                    const float rv = fmaxf(fmaf(2.f * ndl, ndl, -1.f), 0.f);
-                    float spe = 0.f;
-                    if (ndl > 0.f) spe = rv > 0.f ? exp2f(args.shin * __log2f(rv)) : (args.shin == 0.f ? 1.f : 0.f);
-                    const float lit = fmaf(args.kd, dif, args.ka);
-                    const float add = args.ks * spe;
-                    cr = __saturatef(fmaf(cr, lit, add));
-                    cg = __saturatef(fmaf(cg, lit, add));
-                    cb = __saturatef(fmaf(cb, lit, add));
-                }
-            }
-            // a10: front-to-back compositing + ERT (l.13-15; R-13)
-            const float wgt = (1.f - A) * a;
-            C0 = fmaf(wgt, cr, C0);
-            C1 = fmaf(wgt, cg, C1);
-            C2 = fmaf(wgt, cb, C2);
-            A += wgt;
-            ++k;
+        }
+        // ---- a3 setup: fixed-point sample coordinates per axis --------------
+        long long F[3], DF[3];
+        int s_nu[3] = {0, 0, 0};
+        {
+            const double t0 = t_in + 0.5 * args.step;
 #pragma unroll
-            for (int i = 0; i < 3; ++i) F[i] += DF[i];
-            live = !(A > args.o_max) && k < K;
+            for (int i = 0; i < 3; ++i) {
+                const double u0 = (o[i] + t0 * d[i] - args.bmin[i]) / args.L[i];
+                const double du = args.step * d[i] / args.L[i];
+                if (UNI) {
+                    const double S = (double)args.ax[i].nsp;
+                    F[i] = llrint(ldexp(u0 * S, kUniFracBits));
+                    DF[i] = llrint(ldexp(du * S, kUniFracBits));
+                } else {
+                    F[i] = llrint(ldexp(u0, kNonUniFracBits));
+                    DF[i] = llrint(ldexp(du, kNonUniFracBits));
+                    if (K > 0) s_nu[i] = nonuni_first_span_fx(args.ax[i], F[i]);
+                }
+            }
         }
-    }
-    // ---- a11: pixel write ---------------------------------------------------
-    if (valid) {
-        int64_t idx;
-        if (args.tiles)
-            idx = tile_id * (MFA_TILE * MFA_TILE) + ly * MFA_TILE + lx;
-        else
-            idx = ((int64_t)(args.view_base + view) * args.H + py) * args.W + px;
-        if (args.out_fp16) {
-            __half2* o2 = reinterpret_cast<__half2*>(args.out) + 2 * idx;
-            o2[0] = __floats2half2_rn(C0, C1);
-            o2[1] = __floats2half2_rn(C2, A);
-        } else {
-            reinterpret_cast<float4*>(args.out)[idx] = make_float4(C0, C1, C2, A);
+        const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
+
+        float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+        int k = 0;
+        bool live = K > 0;
+        while (__any_sync(0xffffffffu, live)) {
+            if (live) {
+                // a4: span + local coordinate per axis
+                int s[3];
+                float t[3], gs[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    if (UNI) {
+                        uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
+                        gs[i] = args.gsc[i];
+                    } else {
+                        float invh;
+                        nonuni_span_fx(args.ax[i], F[i], s_nu[i], t[i], invh);
+                        s[i] = s_nu[i];
+                        gs[i] = invh * args.gsc[i];
+                    }
+                }
+                // a6: issue slab 0 of the neighbourhood before the basis math
+                const float4* q = args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
+                float r0[P + 1][P + 1];
+                load_slab<P>(q, r0);
+                float val, gu = 0.f, gv = 0.f, gw = 0.f;
+                if (SHADE) {  // a5 + a7 with derivatives (Alg.1 l.6 and l.9)
+                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                    axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
+                    axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
+                    axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
+                    contract_vg<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
+                } else {      // value only (Alg.1 l.8 ShadingOn == false)
+                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                    axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+                    axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+                    axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+                    val = contract_v<P>(q, r0, Nu, Nv, Nw);
+                }
+                // a8: transfer function (l.7)
+                float f = (val - args.v_lo) * args.s_scale;
+                f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
+                const int i0 = min((int)f, args.tf_n - 2);
+                const float wt = f - (float)i0;
+                const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
+                float cr = fmaf(wt, T1.x - T0.x, T0.x);
+                float cg = fmaf(wt, T1.y - T0.y, T0.y);
+                float cb = fmaf(wt, T1.z - T0.z, T0.z);
+                const float a = fmaf(wt, T1.w - T0.w, T0.w);
+                // a9: Phong with a headlight (l.10-11; R-11)
+                if (SHADE) {
+                    const float gx = gu * gs[0], gy = gv * gs[1], gz = gw * gs[2];
+                    const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
+                    if (n2 <= args.eps2) {
+                        cr *= args.ka;
+                        cg *= args.ka;
+                        cb *= args.ka;
+                    } else {
+                        const float ndl = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * rsqrtf(n2);
+                        const float dif = fmaxf(ndl, 0.f);
+                        const float rv = fmaxf(fmaf(2.f * ndl, ndl, -1.f), 0.f);
+                        float spe = 0.f;
+                        if (ndl > 0.f) spe = rv > 0.f ? exp2f(args.shin * __log2f(rv)) : (args.shin == 0.f ? 1.f : 0.f);
+                        const float lit = fmaf(args.kd, dif, args.ka);
+                        const float add = args.ks * spe;
+                        cr = __saturatef(fmaf(cr, lit, add));
+                        cg = __saturatef(fmaf(cg, lit, add));
+                        cb = __saturatef(fmaf(cb, lit, add));
+                    }
+                }
+                // a10: front-to-back compositing + ERT (l.13-15; R-13)
+                const float wgt = (1.f - A) * a;
+                C0 = fmaf(wgt, cr, C0);
+                C1 = fmaf(wgt, cg, C1);
+                C2 = fmaf(wgt, cb, C2);
+                A += wgt;
+                ++k;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) F[i] += DF[i];
+                live = !(A > args.o_max) && k < K;
+            }
         }
+        // ---- a11: pixel write ---------------------------------------------
+        if (valid) {
+            int64_t idx;
+            if (args.tiles)
+                idx = tile_id * (MFA_TILE * MFA_TILE) + ly * MFA_TILE + lx;
+            else
+                idx = ((int64_t)(args.view_base + view) * args.H + py) * args.W + px;
+            if (args.out_fp16) {
+                __half2* o2 = reinterpret_cast<__half2*>(args.out) + 2 * idx;
+                o2[0] = __floats2half2_rn(C0, C1);
+                o2[1] = __floats2half2_rn(C2, A);
+            } else {
+                reinterpret_cast<float4*>(args.out)[idx] = make_float4(C0, C1, C2, A);
+            }
+        }
+        my_samples += (unsigned)k;
     }
     if (args.samples) {
-        unsigned c = (unsigned)k;
-        c = __reduce_add_sync(0xffffffffu, c);
-        if (lane == 0 && c) atomicAdd(&s_count, (unsigned long long)c);
-        __syncthreads();
-        if (threadIdx.x == 0 && s_count) atomicAdd(args.samples, s_count);
+        my_samples = __reduce_add_sync(0xffffffffu, (unsigned)my_samples);
+        if (lane == 0 && my_samples) atomicAdd(args.samples, my_samples);
     }
 }
 
 template <int P, bool UNI, bool SHADE>
-static cudaError_t launch_render_t(const RenderArgs& a, int64_t nblocks, cudaStream_t st) {
+static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(float4) * a.tf_n;
-    if (nblocks >= (1ll << 31)) return cudaErrorInvalidConfiguration;
-    render_kernel<P, UNI, SHADE><<<(unsigned)nblocks, 256, smem, st>>>(a);
+    auto kern = render_kernel<P, UNI, SHADE>;
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    if (occ < 1) occ = 1;
+    int64_t grid = (int64_t)sms * occ;
+    const int64_t need = (a.n_units + 7) / 8;  // 8 warps per CTA
+    if (grid > need) grid = need > 0 ? need : 1;
+    kern<<<(unsigned)grid, 256, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 template <int P>
-static cudaError_t dispatch_render(const RenderArgs& a, int64_t nb, bool uni, bool shade, cudaStream_t st) {
-    if (uni) return shade ? launch_render_t<P, true, true>(a, nb, st) : launch_render_t<P, true, false>(a, nb, st);
-    return shade ? launch_render_t<P, false, true>(a, nb, st) : launch_render_t<P, false, false>(a, nb, st);
+static cudaError_t dispatch_render(const RenderArgs& a, bool uni, bool shade, cudaStream_t st) {
+    if (uni) return shade ? launch_render_t<P, true, true>(a, st) : launch_render_t<P, true, false>(a, st);
+    return shade ? launch_render_t<P, false, true>(a, st) : launch_render_t<P, false, false>(a, st);
 }
+
+static std::atomic<unsigned> g_slot{0};
 
 mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                          const mfa_render_params* prm, const mfa_tiles* tiles, void* out,
                          unsigned long long* samples, cudaStream_t st) {
     RenderArgs* a = new RenderArgs();  // ~7 KB: keep it off the caller's stack
     a->Q = m->Q;
-    a->nu = (int)m->n[0];
-    a->nv = (int)m->n[1];
-    a->nw = (int)m->n[2];
+    a->g.nbx = m->nb[0];
+    a->g.nby = m->nb[1];
     for (int d = 0; d < 3; ++d) a->ax[d] = make_axis_args(m->ax[d]);
     a->tf = reinterpret_cast<const float4*>(tf->rgba);
     a->tf_n = tf->n_entries;
     a->v_lo = tf->v_lo;
     a->s_scale = (float)((double)(tf->n_entries - 1) / ((double)tf->v_hi - (double)tf->v_lo));
+    const bool uni = m->uniform[0] && m->uniform[1] && m->uniform[2];
     for (int d = 0; d < 3; ++d) {
         a->bmin[d] = prm->box_min[d];
         a->L[d] = prm->box_max[d] - prm->box_min[d];
-        a->invL[d] = (float)(1.0 / a->L[d]);
+        a->gsc[d] = (float)((uni ? (double)m->ax[d].nsp : 1.0) / a->L[d]);
     }
     a->step = prm->step;
     a->o_max = (float)prm->o_max;
@@ -313,7 +340,6 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->ks = (float)prm->ks;
     a->shin = (float)prm->shininess;
     a->eps2 = (float)(prm->grad_eps * prm->grad_eps);
-    a->shading = prm->shading;
     a->W = cams[0].width;
     a->H = cams[0].height;
     a->tiles_x = (a->W + MFA_TILE - 1) / MFA_TILE;
@@ -321,43 +347,44 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->out = out;
     a->out_fp16 = prm->out_fp16;
     a->samples = samples;
-    const bool uni = m->uniform[0] && m->uniform[1] && m->uniform[2];
     const bool shade = prm->shading != 0;
     cudaError_t e = cudaSuccess;
+    auto run = [&]() -> cudaError_t {
+        if (a->n_units == 0) return cudaSuccess;
+        if (a->n_units >= (int64_t)0xffffffffu) return cudaErrorInvalidValue;
+        a->queue = m->queue + (g_slot.fetch_add(1) % kQueueSlots);
+        cudaError_t r = cudaMemsetAsync(a->queue, 0, sizeof(unsigned int), st);
+        if (r != cudaSuccess) return r;
+        switch (m->p) {
+            case 1: return dispatch_render<1>(*a, uni, shade, st);
+            case 2: return dispatch_render<2>(*a, uni, shade, st);
+            case 3: return dispatch_render<3>(*a, uni, shade, st);
+            case 4: return dispatch_render<4>(*a, uni, shade, st);
+            default: return dispatch_render<5>(*a, uni, shade, st);
+        }
+    };
     if (tiles) {
-        // tiles reference views 0..n_views-1 of cams; one launch per <=64-view group
         if (n_views > kMaxViewsPerLaunch) {
             delete a;
             return fail(MFA_ERR_UNSUPPORTED, "tiled render supports at most 64 views per call");
         }
         for (int v = 0; v < n_views; ++v) a->cams[v] = cams[v];
+        a->n_views = n_views;
         a->tiles = tiles->tiles;
         a->n_tiles = tiles->n_tiles;
+        a->n_units = tiles->n_tiles * 8;
         a->view_base = 0;
-        if (tiles->n_tiles > 0) {
-            switch (m->p) {
-                case 1: e = dispatch_render<1>(*a, tiles->n_tiles, uni, shade, st); break;
-                case 2: e = dispatch_render<2>(*a, tiles->n_tiles, uni, shade, st); break;
-                case 3: e = dispatch_render<3>(*a, tiles->n_tiles, uni, shade, st); break;
-                case 4: e = dispatch_render<4>(*a, tiles->n_tiles, uni, shade, st); break;
-                default: e = dispatch_render<5>(*a, tiles->n_tiles, uni, shade, st); break;
-            }
-        }
+        e = run();
     } else {
         a->tiles = nullptr;
         a->n_tiles = 0;
         for (int v0 = 0; v0 < n_views && e == cudaSuccess; v0 += kMaxViewsPerLaunch) {
             const int nv = std::min(kMaxViewsPerLaunch, n_views - v0);
             for (int v = 0; v < nv; ++v) a->cams[v] = cams[v0 + v];
+            a->n_views = nv;
             a->view_base = v0;
-            const int64_t nb = (int64_t)nv * a->tiles_x * a->tiles_y;
-            switch (m->p) {
-                case 1: e = dispatch_render<1>(*a, nb, uni, shade, st); break;
-                case 2: e = dispatch_render<2>(*a, nb, uni, shade, st); break;
-                case 3: e = dispatch_render<3>(*a, nb, uni, shade, st); break;
-                case 4: e = dispatch_render<4>(*a, nb, uni, shade, st); break;
-                default: e = dispatch_render<5>(*a, nb, uni, shade, st); break;
-            }
+            a->n_units = (int64_t)nv * a->tiles_x * a->tiles_y * 8;
+            e = run();
         }
     }
     delete a;
