@@ -282,6 +282,14 @@ def run_ours(args):
     if clocks.get("sm_mhz"):
         pk_clk, _ = RL.fp32_peak_tflops(clocks["sm_mhz"])
         roof["frac_at_observed_clock"] = achieved_tf / pk_clk
+    try:  # DRAM bytes per launch from the committed ncu --set full capture
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(w.name)
+        if tr and world == 1:
+            roof["traffic"] = tr["bytes_per_launch"]
+            roof["traffic_unit"] = "bytes/launch (dram read+write)"
+            roof["traffic_source"] = f"{tr['source']} ({tr['kernel']})"
+    except Exception:
+        pass
 
     # ---- end to end through the C ABI with host buffers --------------------
     e2e = None

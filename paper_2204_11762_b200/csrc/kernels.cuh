@@ -385,4 +385,49 @@ __device__ __forceinline__ float contract_v(const float4* __restrict__ q, float 
     return val;
 }
 
+// ---------------------------------------------------------------------------
+// a6/a7 with a per-lane neighbourhood cache (p <= 3): the (p+1)^3 control
+// values stay in registers while consecutive samples of a ray share a span
+// triple (about 57% of steps at 0.25 span per step); only lanes whose triple
+// changed reload, which cuts L1 wavefronts.
+// ---------------------------------------------------------------------------
+template <int P>
+__device__ __forceinline__ void load_block(const float4* __restrict__ q, float (&nb)[P + 1][P + 1][P + 1]) {
+    constexpr int SW = Brick<P>::EV * Brick<P>::EU;
+#pragma unroll
+    for (int c = 0; c <= P; ++c) load_slab<P>(q + c * SW, nb[c]);
+}
+
+template <int P>
+__device__ __forceinline__ void contract_vg_cached(const float (&nb)[P + 1][P + 1][P + 1], const float2 (&Bu)[P + 1],
+                                                   const float2 (&Bvs)[P + 1], const float2 (&Bw)[P + 1],
+                                                   float& val, float& gu, float& gv, float& gw) {
+    float2 vw = make_float2(0.f, 0.f), gvu = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c <= P; ++c) contract_slab<P>(nb[c], Bu, Bvs, Bw[c], vw, gvu);
+    val = vw.x;
+    gw = vw.y;
+    gv = gvu.x;
+    gu = gvu.y;
+}
+
+template <int P>
+__device__ __forceinline__ float contract_v_cached(const float (&nb)[P + 1][P + 1][P + 1], const float (&Nu)[P + 1],
+                                                   const float (&Nv)[P + 1], const float (&Nw)[P + 1]) {
+    float val = 0.f;
+#pragma unroll
+    for (int c = 0; c <= P; ++c) {
+        float B = 0.f;
+#pragma unroll
+        for (int b = 0; b <= P; ++b) {
+            float a0 = Nu[0] * nb[c][b][0];
+#pragma unroll
+            for (int a = 1; a <= P; ++a) a0 = fmaf(Nu[a], nb[c][b][a], a0);
+            B = fmaf(Nv[b], a0, B);
+        }
+        val = fmaf(Nw[c], B, val);
+    }
+    return val;
+}
+
 }  // namespace mfa

@@ -79,8 +79,22 @@ __device__ __forceinline__ void compute_frame(const mfa_camera& c, ViewFrame& fr
     }
 }
 
+#ifndef MFA_RENDER_THREADS   // persistent CTA size (warps fetch work independently)
+#define MFA_RENDER_THREADS 128
+#endif
+#ifdef MFA_RENDER_MINB   // tuning experiments: force min resident CTAs per SM
+#define MFA_RENDER_BOUNDS __launch_bounds__(MFA_RENDER_THREADS, MFA_RENDER_MINB)
+#else
+#define MFA_RENDER_BOUNDS __launch_bounds__(MFA_RENDER_THREADS)
+#endif
+
+#ifndef MFA_RENDER_CACHE
+#define MFA_RENDER_CACHE 1
+#endif
+
 template <int P, bool UNI, bool SHADE>
-__global__ void __launch_bounds__(256) render_kernel(const __grid_constant__ RenderArgs args) {
+__global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderArgs args) {
+    constexpr bool CACHE = MFA_RENDER_CACHE && P <= 3;
     extern __shared__ float4 s_tf[];
     __shared__ ViewFrame s_frame[kMaxViewsPerLaunch];
 
@@ -190,6 +204,8 @@ __global__ void __launch_bounds__(256) render_kernel(const __grid_constant__ Ren
         float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
         int k = 0;
         bool live = K > 0;
+        float nb[CACHE ? P + 1 : 1][P + 1][P + 1];   // cached neighbourhood (CACHE)
+        int64_t nb_key = -1;
         while (__any_sync(0xffffffffu, live)) {
             if (live) {
                 // a4: span + local coordinate per axis
@@ -207,23 +223,45 @@ __global__ void __launch_bounds__(256) render_kernel(const __grid_constant__ Ren
                         gs[i] = invh * args.gsc[i];
                     }
                 }
-                // a6: issue slab 0 of the neighbourhood before the basis math
-                const float4* q = args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
-                float r0[P + 1][P + 1];
-                load_slab<P>(q, r0);
+                // a6: neighbourhood of the span triple
+                const int64_t e = brick_entry<P>(args.g, s[0], s[1], s[2]);
+                const float4* q = args.Q + e;
                 float val, gu = 0.f, gv = 0.f, gw = 0.f;
-                if (SHADE) {  // a5 + a7 with derivatives (Alg.1 l.6 and l.9)
-                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
-                    axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
-                    axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
-                    axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
-                    contract_vg<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
-                } else {      // value only (Alg.1 l.8 ShadingOn == false)
-                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
-                    axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
-                    axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
-                    axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
-                    val = contract_v<P>(q, r0, Nu, Nv, Nw);
+                if constexpr (CACHE) {
+                    if (e != nb_key) {       // reload only when the span triple changed
+                        load_block<P>(q, nb);
+                        nb_key = e;
+                    }
+                    if (SHADE) {
+                        float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                        axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
+                        axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
+                        axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
+                        contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                    } else {
+                        float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                        axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+                        axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+                        axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+                        val = contract_v_cached<P>(nb, Nu, Nv, Nw);
+                    }
+                } else {
+                    // issue slab 0 before the basis math; slabs stream through a double buffer
+                    float r0[P + 1][P + 1];
+                    load_slab<P>(q, r0);
+                    if (SHADE) {  // a5 + a7 with derivatives (Alg.1 l.6 and l.9)
+                        float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                        axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
+                        axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
+                        axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
+                        contract_vg<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
+                    } else {      // value only (Alg.1 l.8 ShadingOn == false)
+                        float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                        axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+                        axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+                        axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+                        val = contract_v<P>(q, r0, Nu, Nv, Nw);
+                    }
                 }
                 // a8: transfer function (l.7)
                 float f = (val - args.v_lo) * args.s_scale;
@@ -298,12 +336,13 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    constexpr int kThreads = MFA_RENDER_THREADS;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
     if (occ < 1) occ = 1;
     int64_t grid = (int64_t)sms * occ;
-    const int64_t need = (a.n_units + 7) / 8;  // 8 warps per CTA
+    const int64_t need = (a.n_units + kThreads / 32 - 1) / (kThreads / 32);
     if (grid > need) grid = need > 0 ? need : 1;
-    kern<<<(unsigned)grid, 256, smem, st>>>(a);
+    kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -5,8 +5,9 @@ gather of RGBA tiles over NVLink").
 Every ray is independent given the replicated model (Algorithm 1 splits rows
 over threads; "computation for all pixel values ... can also be
 parallelized").  The work unit is a (view, 16x16 tile).  Units are
-dealt to ranks with a diagonal interleave (unit j of view-row r goes to rank
-(j + r) mod G) so that empty, cheap and ERT-heavy regions spread evenly.
+dealt round-robin to ranks along a diagonal order (each tile-row visited with
+its columns rotated by the row index), so counts differ by at most one and
+empty, cheap and ERT-heavy regions spread evenly.
 Each rank renders its units into a packed tile buffer; one collective
 (all_gather_into_tensor over equal, padded buffers; NCCL over NVLink /
 NVSwitch on GPUs) brings all tiles to every rank and rank 0 scatters them
@@ -38,7 +39,12 @@ def assign_units(n_views: int, width: int, height: int, world: int) -> list[np.n
     tx, _ = tile_grid(width, height)
     j = np.arange(len(u))
     row = j // tx
-    owner = (j + row) % world
+    col = j % tx
+    # within tile-row r visit columns rotated by r, then deal round-robin:
+    # balanced to one unit, and a rank's tiles form diagonals, not columns
+    order = np.lexsort(((col + row) % tx, row))
+    owner = np.empty(len(u), np.int64)
+    owner[order] = np.arange(len(u)) % world
     lists = [u[owner == r] for r in range(world)]
     n = max((len(x) for x in lists), default=0)
     out = []
