@@ -33,6 +33,8 @@ struct AxisArgs {
     int mshift;      // 62 - log2(M): bucket of a 2^62 fixed-point coordinate
     int ic_lo, ic_hi;
     float S;
+    int dshift;      // non-uniform render: (F - U_s) >> dshift fits 23 bits on every span
+    float dscale;    // 2^(dshift - 62)
 };
 
 __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
@@ -51,6 +53,8 @@ __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
     a.ic_lo = A.ic_lo;
     a.ic_hi = A.ic_hi;
     a.S = A.S;
+    a.dshift = A.dshift;
+    a.dscale = ldexpf(1.0f, A.dshift - kNonUniFracBits);
     return a;
 }
 
@@ -256,24 +260,49 @@ __device__ __forceinline__ void nonuni_span_f32(const AxisArgs& A, float u, int&
     t = ((u - __ldg(A.kh + s)) - __ldg(A.kl + s)) * invh;
 }
 
-// a4 (non-uniform axis, render): 2^62 fixed point, incremental search from
-// the previous sample's span (spans are monotone along a ray).
-__device__ __forceinline__ void nonuni_span_fx(const AxisArgs& A, long long F, int& s, float& t, float& invh) {
-    F = max(F, 0LL);
-    F = min(F, 1LL << kNonUniFracBits);
-    while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
-    while (s > 0 && F < __ldg(A.kfx + s)) --s;
-    invh = __ldg(A.invh + s);
-    const long long d = F - __ldg(A.kfx + s);
-    t = __ll2float_rn(d) * (invh * 0x1p-62f);
+// a4 (non-uniform axis, render): u in 2^62 fixed point.  The current span's
+// bounds [lo, hi) and scales stay in registers; only when the sample leaves
+// them (spans are monotone along a ray) is the knot table read.  The offset
+// F - lo (< h * 2^62) is shifted to < 2^23 and converted exactly with the
+// 2^23 magic number, so t costs no int64 -> float conversion.
+struct NUAxis {
+    long long lo, hi;   // knot bounds of span s (2^62 fixed point)
+    float tsc;          // 2^(dshift-62) / h_s
+    float invh;         // 1 / h_s
+    int s;
+};
+
+__device__ __forceinline__ void nu_load(const AxisArgs& A, NUAxis& st) {
+    st.lo = __ldg(A.kfx + st.s);
+    st.hi = (st.s + 1 < A.nsp) ? __ldg(A.kfx + st.s + 1) : 0x7fffffffffffffffLL;
+    st.invh = __ldg(A.invh + st.s);
+    st.tsc = st.invh * A.dscale;
 }
 
-__device__ __forceinline__ int nonuni_first_span_fx(const AxisArgs& A, long long F) {
+__device__ __forceinline__ void nu_init(const AxisArgs& A, long long F, NUAxis& st) {
     F = max(F, 0LL);
     F = min(F, (1LL << kNonUniFracBits) - 1);
     int b = (int)(F >> A.mshift);
     b = min(max(b, 0), A.M - 1);
-    return __ldg(A.bucket + b);
+    int s = __ldg(A.bucket + b);
+    while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
+    st.s = s;
+    nu_load(A, st);
+}
+
+__device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis& st) {
+    F = max(F, 0LL);
+    F = min(F, 1LL << kNonUniFracBits);
+    if (F >= st.hi || F < st.lo) {
+        int s = st.s;
+        while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
+        while (s > 0 && F < __ldg(A.kfx + s)) --s;
+        st.s = s;
+        nu_load(A, st);
+    }
+    const unsigned long long d = (unsigned long long)(F - st.lo) >> A.dshift;   // < 2^23
+    const float fd = __uint_as_float(0x4b000000u | (unsigned)d) - 8388608.0f;
+    return fd * st.tsc;
 }
 
 // ---------------------------------------------------------------------------

@@ -52,6 +52,7 @@ struct AxisTables {
     int M = 0;                        // bucket count
     int ic_lo = 0, ic_hi = -1;        // uniform: spans [ic_lo, ic_hi] use the interior constants
     int uniform = 0;
+    int dshift = 0;                   // see kernels.cuh nu_span
     float S = 0.f;                    // uniform: number of spans as float
     float interior[(kMaxP + 1) * (kMaxP + 1)] = {};  // uniform interior span coefficients
 };

@@ -378,6 +378,13 @@ extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nc
         A.bucket = (int*)(base + off[d][5]);
         A.nsp = nsp;
         A.M = Mb[d];
+        {   // smallest shift with (max span width * 2^62) >> shift < 2^23
+            double hmax = 0.0;
+            for (int64_t i = p; i < nctrl[d]; ++i) hmax = std::max(hmax, knots[d][i + 1] - knots[d][i]);
+            int sh = 0;
+            while (sh < 62 && ldexp(hmax, kNonUniFracBits - sh) >= 8388607.0) ++sh;
+            A.dshift = sh;
+        }
         A.uniform = uniform[d];
         A.S = (float)nsp;
         span_tables_kernel<<<(nsp + 127) / 128, 128, 0, st>>>(Ud, p, nsp, rec, (float*)A.coef, (float*)A.invh);

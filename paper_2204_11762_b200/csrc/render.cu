@@ -181,7 +181,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         }
         // ---- a3 setup: fixed-point sample coordinates per axis --------------
         long long F[3], DF[3];
-        int s_nu[3] = {0, 0, 0};
+        NUAxis nu[UNI ? 1 : 3];
         {
             const double t0 = t_in + 0.5 * args.step;
 #pragma unroll
@@ -195,7 +195,9 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 } else {
                     F[i] = llrint(ldexp(u0, kNonUniFracBits));
                     DF[i] = llrint(ldexp(du, kNonUniFracBits));
-                    if (K > 0) s_nu[i] = nonuni_first_span_fx(args.ax[i], F[i]);
+                    if constexpr (!UNI) {
+                        if (K > 0) nu_init(args.ax[i], F[i], nu[i]);
+                    }
                 }
             }
         }
@@ -217,10 +219,9 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                         uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
                         gs[i] = args.gsc[i];
                     } else {
-                        float invh;
-                        nonuni_span_fx(args.ax[i], F[i], s_nu[i], t[i], invh);
-                        s[i] = s_nu[i];
-                        gs[i] = invh * args.gsc[i];
+                        t[i] = nu_span(args.ax[i], F[i], nu[i]);
+                        s[i] = nu[i].s;
+                        gs[i] = nu[i].invh * args.gsc[i];
                     }
                 }
                 // a6: neighbourhood of the span triple
