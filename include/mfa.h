@@ -72,12 +72,35 @@ typedef enum {
  *             before returning.
  * out         receives the model handle (NULL on failure).
  *
- * Device memory: 4*(4 n_u n_v n_w) bytes for the row-quad layout (DESIGN.md
- * §5) plus per-axis span tables (< 1 MB).
+ * Device memory: bricked row quads ~ 16 (1 + p/16)^2 n_u n_v n_w bytes, or
+ * Bezier blocks (see mfa_model_create_ex), plus per-axis span tables (< 1 MB).
  * ---------------------------------------------------------------------- */
 mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3],
                             const double* const knots[3], const float* ctrl,
                             int32_t ctrl_on_device, mfa_stream stream, mfa_model* out);
+
+/*
+ * mfa_model_create_ex -- as mfa_model_create, with options (NULL = defaults).
+ * layout: MFA_LAYOUT_AUTO chooses Bezier blocks for models with a non-uniform
+ *   axis and degree <= 3 (falling back to quads if the blocks do not fit in
+ *   device memory), else bricked row quads.  MFA_LAYOUT_QUADS / _BEZIER force
+ *   one (Bezier needs degree <= 3: MFA_ERR_UNSUPPORTED otherwise).
+ *   Bezier blocks: for every knot-span triple the (p+1)^3 Bernstein
+ *   coefficients of the spline there (Bezier extraction; 256 B per triple for
+ *   p = 3), so evaluation needs no per-span basis tables.  Device memory:
+ *   4 (p+1)^2 * 4 * S_u S_v S_w bytes (C5: 16.7 GB).
+ */
+#define MFA_LAYOUT_AUTO 0
+#define MFA_LAYOUT_QUADS 1
+#define MFA_LAYOUT_BEZIER 2
+typedef struct {
+    int32_t layout;
+} mfa_model_options;
+
+mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t nctrl[3],
+                               const double* const knots[3], const float* ctrl,
+                               int32_t ctrl_on_device, const mfa_model_options* opt,
+                               mfa_stream stream, mfa_model* out);
 
 typedef struct {
     int32_t degree[3];
@@ -86,6 +109,7 @@ typedef struct {
     float v_min, v_max;     /* min / max control value (a TF domain default) */
     int64_t device_bytes;   /* device memory owned by the model */
     int32_t device;         /* CUDA ordinal the model lives on */
+    int32_t layout;         /* MFA_LAYOUT_QUADS or MFA_LAYOUT_BEZIER */
 } mfa_model_desc;
 
 mfa_status mfa_model_info(mfa_model m, mfa_model_desc* out);

@@ -18,9 +18,10 @@ MFA_OK = 0
 STATUS = {0: "MFA_OK", 1: "MFA_ERR_INVALID_ARG", 2: "MFA_ERR_KNOTS", 3: "MFA_ERR_UNSUPPORTED",
           4: "MFA_ERR_DOMAIN", 5: "MFA_ERR_CUDA", 6: "MFA_ERR_OOM", 7: "MFA_ERR_DEVICE"}
 TILE = 16
+LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2}
 
 # C-ABI symbols declared in include/mfa.h (checked by tests/test_abi.py)
-EXPORTS = ("mfa_model_create", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
+EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
            "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version")
 
 
@@ -54,7 +55,11 @@ class Tiles_t(C.Structure):
 class ModelDesc_t(C.Structure):
     _fields_ = [("degree", C.c_int32 * 3), ("nctrl", C.c_int64 * 3), ("uniform", C.c_int32 * 3),
                 ("v_min", C.c_float), ("v_max", C.c_float), ("device_bytes", C.c_int64),
-                ("device", C.c_int32)]
+                ("device", C.c_int32), ("layout", C.c_int32)]
+
+
+class ModelOptions_t(C.Structure):
+    _fields_ = [("layout", C.c_int32)]
 
 
 _lib = None
@@ -72,6 +77,9 @@ def lib():
         L.mfa_model_create.restype = C.c_int
         L.mfa_model_create.argtypes = [C.POINTER(i32), C.POINTER(i64), C.POINTER(C.POINTER(C.c_double)), vp, i32,
                                        vp, C.POINTER(vp)]
+        L.mfa_model_create_ex.restype = C.c_int
+        L.mfa_model_create_ex.argtypes = [C.POINTER(i32), C.POINTER(i64), C.POINTER(C.POINTER(C.c_double)), vp,
+                                          i32, C.POINTER(ModelOptions_t), vp, C.POINTER(vp)]
         L.mfa_model_info.restype = C.c_int
         L.mfa_model_info.argtypes = [vp, C.POINTER(ModelDesc_t)]
         L.mfa_model_destroy.restype = C.c_int
@@ -140,7 +148,7 @@ def params_t(p, out_fp16=False):
 class Model:
     """An MFA model resident on the current CUDA device (mfa_model_create)."""
 
-    def __init__(self, degree, knots, ctrl, stream=None):
+    def __init__(self, degree, knots, ctrl, stream=None, layout: str = "auto"):
         import torch
         if np.isscalar(degree):
             degree = (int(degree),) * 3
@@ -162,14 +170,15 @@ class Model:
         self._knots = [np.ascontiguousarray(k, dtype=np.float64) for k in knots]
         kp = (C.POINTER(C.c_double) * 3)(*[k.ctypes.data_as(C.POINTER(C.c_double)) for k in self._knots])
         h = C.c_void_p(0)
-        _check(L.mfa_model_create(deg, n, kp, cptr, on_dev, _stream_ptr(stream), C.byref(h)))
+        opt = ModelOptions_t(LAYOUTS[layout])
+        _check(L.mfa_model_create_ex(deg, n, kp, cptr, on_dev, C.byref(opt), _stream_ptr(stream), C.byref(h)))
         self._h = h
         self.degree = tuple(int(x) for x in degree)
         self.nctrl = (nu, nv, nw)
 
     @classmethod
-    def from_workload(cls, w, stream=None):
-        return cls(w.degree, w.knots, w.ctrl, stream=stream)
+    def from_workload(cls, w, stream=None, layout: str = "auto"):
+        return cls(w.degree, w.knots, w.ctrl, stream=stream, layout=layout)
 
     @property
     def handle(self):
@@ -179,7 +188,8 @@ class Model:
         d = ModelDesc_t()
         _check(lib().mfa_model_info(self._h, C.byref(d)))
         return dict(degree=tuple(d.degree), nctrl=tuple(d.nctrl), uniform=tuple(d.uniform),
-                    v_min=d.v_min, v_max=d.v_max, device_bytes=d.device_bytes, device=d.device)
+                    v_min=d.v_min, v_max=d.v_max, device_bytes=d.device_bytes, device=d.device,
+                    layout={1: "quads", 2: "bezier"}.get(d.layout, d.layout))
 
     def close(self):
         if self._h and self._h.value:

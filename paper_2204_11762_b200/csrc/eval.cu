@@ -10,6 +10,7 @@ namespace mfa {
 struct EvalArgs {
     const float4* Q;
     BrickGrid g;
+    BezGrid bg;
     AxisArgs ax[3];
     const float* u;
     const float* v;
@@ -22,8 +23,9 @@ struct EvalArgs {
     int64_t n;
 };
 
-template <int P, bool UNI, bool GRAD>
+template <int P, int LAYOUT, bool UNI, bool GRAD>
 __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalArgs args) {
+    constexpr bool BEZ = LAYOUT == kBezier;
     unsigned errs = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < args.n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -48,6 +50,32 @@ __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalA
             } else {
                 nonuni_span_f32(args.ax[d], q[d], s[d], t[d], sc[d]);
             }
+        }
+        if constexpr (BEZ) {
+            const float4* base = bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]);
+            if (GRAD) {
+                float r0[P + 1][P + 1];
+                load_bslab<P>(base, r0);
+                float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                bernstein<P, false>(t[0], Bu);
+                bernstein<P, true>(t[1], Bv);
+                bernstein<P, false>(t[2], Bw);
+                float val, gu, gv, gw;
+                contract_vg_bez<P>(base, r0, Bu, Bv, Bw, val, gu, gv, gw);
+                args.value[i] = val;
+                args.du[i] = gu * sc[0];
+                args.dv[i] = gv * sc[1];
+                args.dw[i] = gw * sc[2];
+            } else {
+                float nb[P + 1][P + 1][P + 1];
+                load_bblock<P>(base, nb);
+                float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                bernstein_value<P>(t[0], Nu);
+                bernstein_value<P>(t[1], Nv);
+                bernstein_value<P>(t[2], Nw);
+                args.value[i] = contract_v_cached<P>(nb, Nu, Nv, Nw);
+            }
+            continue;
         }
         const float4* base = args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
         float r0[P + 1][P + 1];
@@ -77,21 +105,30 @@ __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalA
     }
 }
 
-template <int P, bool UNI, bool GRAD>
+template <int P, int LAYOUT, bool UNI, bool GRAD>
 static cudaError_t launch_eval_t(const EvalArgs& a, cudaStream_t st) {
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t want = (a.n + 255) / 256;
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * 16);
-    eval_kernel<P, UNI, GRAD><<<(unsigned)grid, 256, 0, st>>>(a);
+    eval_kernel<P, LAYOUT, UNI, GRAD><<<(unsigned)grid, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
+template <int P, int LAYOUT>
+static cudaError_t dispatch_eval_l(const EvalArgs& a, bool uni, bool grad, cudaStream_t st) {
+    if (uni)
+        return grad ? launch_eval_t<P, LAYOUT, true, true>(a, st) : launch_eval_t<P, LAYOUT, true, false>(a, st);
+    return grad ? launch_eval_t<P, LAYOUT, false, true>(a, st) : launch_eval_t<P, LAYOUT, false, false>(a, st);
+}
+
 template <int P>
-static cudaError_t dispatch_eval(const EvalArgs& a, bool uni, bool grad, cudaStream_t st) {
-    if (uni) return grad ? launch_eval_t<P, true, true>(a, st) : launch_eval_t<P, true, false>(a, st);
-    return grad ? launch_eval_t<P, false, true>(a, st) : launch_eval_t<P, false, false>(a, st);
+static cudaError_t dispatch_eval(const EvalArgs& a, int layout, bool uni, bool grad, cudaStream_t st) {
+    if constexpr (P <= 3) {
+        if (layout == kBezier) return dispatch_eval_l<P, kBezier>(a, uni, grad, st);
+    }
+    return dispatch_eval_l<P, kQuads>(a, uni, grad, st);
 }
 
 mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v, const float* w, float* value,
@@ -100,6 +137,8 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
     a.Q = m->Q;
     a.g.nbx = m->nb[0];
     a.g.nby = m->nb[1];
+    a.bg.S0 = (int)(m->n[0] - m->p);
+    a.bg.S1 = (int)(m->n[1] - m->p);
     for (int d = 0; d < 3; ++d) a.ax[d] = make_axis_args(m->ax[d]);
     a.u = u;
     a.v = v;
@@ -114,11 +153,11 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
     const bool grad = du != nullptr;
     cudaError_t e;
     switch (m->p) {
-        case 1: e = dispatch_eval<1>(a, uni, grad, st); break;
-        case 2: e = dispatch_eval<2>(a, uni, grad, st); break;
-        case 3: e = dispatch_eval<3>(a, uni, grad, st); break;
-        case 4: e = dispatch_eval<4>(a, uni, grad, st); break;
-        default: e = dispatch_eval<5>(a, uni, grad, st); break;
+        case 1: e = dispatch_eval<1>(a, m->layout, uni, grad, st); break;
+        case 2: e = dispatch_eval<2>(a, m->layout, uni, grad, st); break;
+        case 3: e = dispatch_eval<3>(a, m->layout, uni, grad, st); break;
+        case 4: e = dispatch_eval<4>(a, m->layout, uni, grad, st); break;
+        default: e = dispatch_eval<5>(a, m->layout, uni, grad, st); break;
     }
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "eval launch");
 }

@@ -294,11 +294,17 @@ __device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis&
     F = max(F, 0LL);
     F = min(F, 1LL << kNonUniFracBits);
     if (F >= st.hi || F < st.lo) {
-        int s = st.s;
-        while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
-        while (s > 0 && F < __ldg(A.kfx + s)) --s;
-        st.s = s;
+        // common case: the sample moved into the neighbouring span; the new
+        // bounds and scale are three independent loads (one round trip)
+        st.s += (F >= st.hi) ? 1 : -1;
         nu_load(A, st);
+        if (F >= st.hi || F < st.lo) {   // rare: crossed more than one span this step
+            int s = st.s;
+            while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
+            while (s > 0 && F < __ldg(A.kfx + s)) --s;
+            st.s = s;
+            nu_load(A, st);
+        }
     }
     const unsigned long long d = (unsigned long long)(F - st.lo) >> A.dshift;   // < 2^23
     const float fd = __uint_as_float(0x4b000000u | (unsigned)d) - 8388608.0f;
@@ -457,6 +463,149 @@ __device__ __forceinline__ float contract_v_cached(const float (&nb)[P + 1][P + 
         val = fmaf(Nw[c], B, val);
     }
     return val;
+}
+
+// ---------------------------------------------------------------------------
+// Bezier-block layout (non-uniform models, p <= 3): the spline on span triple
+// (su, sv, sw) is sum_{jkl} B_j(t_u) B_k(t_v) B_l(t_w) Z[l][k][j] with the
+// Bernstein polynomials B_j(t) = C(p,j) t^j (1-t)^(p-j), the same on every
+// span, evaluated here in product form (all terms non-negative).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr float binomf(int n, int k) {
+    float r = 1.f;
+    for (int i = 1; i <= k; ++i) r = r * (float)(n - k + i) / (float)i;
+    return r;
+}
+
+template <int P, bool SWAP>
+__device__ __forceinline__ void bernstein(float t, float2 (&B)[P + 1]) {
+    const float s = 1.f - t;
+    float tp[P + 1], sp[P + 1];
+    tp[0] = 1.f;
+    sp[0] = 1.f;
+#pragma unroll
+    for (int m = 1; m <= P; ++m) {
+        tp[m] = tp[m - 1] * t;
+        sp[m] = sp[m - 1] * s;
+    }
+    float lo[P + 1];   // degree P-1 Bernstein, b_j = C(P-1, j) t^j s^(P-1-j), j = 0..P-1
+#pragma unroll
+    for (int j = 0; j < P; ++j) lo[j] = binomf(P - 1, j) * (tp[j] * sp[P - 1 - j]);
+#pragma unroll
+    for (int j = 0; j <= P; ++j) {
+        const float v = binomf(P, j) * (tp[j] * sp[P - j]);
+        float d;                                  // B_j' = P (b_{j-1} - b_j)
+        if (j == 0) d = -(float)P * lo[0];
+        else if (j == P) d = (float)P * lo[P - 1];
+        else d = (float)P * (lo[j - 1] - lo[j]);
+        B[j] = SWAP ? make_float2(d, v) : make_float2(v, d);
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void bernstein_value(float t, float (&N)[P + 1]) {
+    const float s = 1.f - t;
+    float tp[P + 1], sp[P + 1];
+    tp[0] = 1.f;
+    sp[0] = 1.f;
+#pragma unroll
+    for (int m = 1; m <= P; ++m) {
+        tp[m] = tp[m - 1] * t;
+        sp[m] = sp[m - 1] * s;
+    }
+#pragma unroll
+    for (int j = 0; j <= P; ++j) N[j] = binomf(P, j) * (tp[j] * sp[P - j]);
+}
+
+struct BezGrid {
+    int S0, S1;            // spans along u, v
+};
+
+template <int P>
+struct BezBlock {
+    static constexpr int ROW = bez_row(P);                 // floats per stored row
+    static constexpr int F4 = (P + 1) * (P + 1) * ROW / 4;  // float4 per block (p >= 2)
+    static constexpr int FLOATS = (P + 1) * (P + 1) * ROW;
+};
+
+template <int P>
+__device__ __forceinline__ const float4* bez_block(const float4* Q, const BezGrid& g, int su, int sv, int sw) {
+    const int64_t b = ((int64_t)sw * g.S1 + sv) * g.S0 + su;
+    return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Q) + b * BezBlock<P>::FLOATS);
+}
+
+// slab c of a Bezier block: rows b = 0..P at consecutive compile-time offsets
+template <int P>
+__device__ __forceinline__ void load_bslab(const float4* __restrict__ q, float (&r)[P + 1][P + 1]) {
+#pragma unroll
+    for (int b = 0; b <= P; ++b) {
+        if constexpr (P == 1) {
+            const float2 x = __ldg(reinterpret_cast<const float2*>(q) + b);
+            r[b][0] = x.x; r[b][1] = x.y;
+        } else {
+            const float4 x = __ldg(q + b);
+            r[b][0] = x.x; r[b][1] = x.y; r[b][2] = x.z;
+            if constexpr (P == 3) r[b][3] = x.w;
+        }
+    }
+}
+
+template <int P>
+__device__ __forceinline__ const float4* bslab_ptr(const float4* q, int c) {
+    return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + c * (P + 1) * BezBlock<P>::ROW);
+}
+
+template <int P>
+__device__ __forceinline__ void load_bblock(const float4* __restrict__ q, float (&nb)[P + 1][P + 1][P + 1]) {
+#pragma unroll
+    for (int c = 0; c <= P; ++c) load_bslab<P>(bslab_ptr<P>(q, c), nb[c]);
+}
+
+template <int P>
+__device__ __forceinline__ void contract_vg_bez(const float4* __restrict__ q, float (&r0)[P + 1][P + 1],
+                                                const float2 (&Bu)[P + 1], const float2 (&Bvs)[P + 1],
+                                                const float2 (&Bw)[P + 1], float& val, float& gu, float& gv,
+                                                float& gw) {
+    float2 vw = make_float2(0.f, 0.f), gvu = make_float2(0.f, 0.f);
+    float r1[P + 1][P + 1];
+#pragma unroll
+    for (int c = 0; c <= P; ++c) {
+        if (c & 1) {
+            if (c < P) load_bslab<P>(bslab_ptr<P>(q, c + 1), r0);
+            contract_slab<P>(r1, Bu, Bvs, Bw[c], vw, gvu);
+        } else {
+            if (c < P) load_bslab<P>(bslab_ptr<P>(q, c + 1), r1);
+            contract_slab<P>(r0, Bu, Bvs, Bw[c], vw, gvu);
+        }
+    }
+    val = vw.x;
+    gw = vw.y;
+    gv = gvu.x;
+    gu = gvu.y;
+}
+
+// L1 prefetch of one Bezier block (the next sample's) -- a hint, no registers.
+template <int P>
+__device__ __forceinline__ void prefetch_bblock(const float4* q) {
+    constexpr int BYTES = BezBlock<P>::FLOATS * 4;
+#pragma unroll
+    for (int off = 0; off < BYTES; off += 128)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(q) + off));
+}
+
+// Span of the next sample on a uniform axis (prefetch prediction only).
+__device__ __forceinline__ int uni_span_only(long long F, int S) {
+    int s = (int)(F >> kUniFracBits);
+    return min(max(s, 0), S - 1);
+}
+
+// Span of the next sample on a non-uniform axis: one step past the cached
+// bounds at most (prefetch prediction only).
+__device__ __forceinline__ int nu_span_only(const NUAxis& st, long long F, int nsp) {
+    int s = st.s;
+    if (F >= st.hi) s = min(s + 1, nsp - 1);
+    else if (F < st.lo) s = max(s - 1, 0);
+    return s;
 }
 
 }  // namespace mfa

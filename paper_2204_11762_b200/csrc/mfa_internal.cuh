@@ -34,6 +34,7 @@ constexpr int kNonUniFracBits = 62; // non-uniform axes: parameter fixed point, 
 constexpr int kBrickLog = 4;        // bricks of 16x16x16 spans
 constexpr int kBrick = 1 << kBrickLog;
 constexpr int kQueueSlots = 256;    // persistent-kernel work counters (one per in-flight launch)
+__host__ __device__ constexpr int bez_row(int p) { return p == 1 ? 2 : 4; }  // floats per stored block row
 
 // brick entry extents for degree p (see kernels.cuh)
 __host__ __device__ constexpr int brick_eu(int p) { return kBrick + (p == 4 ? 1 : (p == 5 ? 4 : 0)); }
@@ -54,16 +55,18 @@ struct AxisTables {
     int uniform = 0;
     int dshift = 0;                   // see kernels.cuh nu_span
     float S = 0.f;                    // uniform: number of spans as float
-    float interior[(kMaxP + 1) * (kMaxP + 1)] = {};  // uniform interior span coefficients
 };
+
+enum Layout { kQuads = 0, kBezier = 1 };
 
 struct Model {
     int device = 0;
     int p = 0;
+    int layout = kQuads;           // kBezier: per-span-triple Bernstein blocks (non-uniform, p <= 3)
     int64_t n[3] = {0, 0, 0};
     int uniform[3] = {0, 0, 0};
     float vmin = 0.f, vmax = 0.f;
-    float4* Q = nullptr;           // bricked row quads
+    float4* Q = nullptr;           // bricked row quads (kQuads) or Bezier blocks (kBezier)
     int nb[3] = {0, 0, 0};         // bricks per axis
     unsigned int* queue = nullptr; // kQueueSlots work counters
     AxisTables ax[3];

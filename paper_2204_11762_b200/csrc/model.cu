@@ -119,20 +119,11 @@ __global__ void minmax_kernel(const float* __restrict__ P, int64_t n, unsigned i
 //                    + (U_{j+k+1}-u)/(U_{j+k+1}-U_{j+1}) N_{j+1,k-1}
 // applied to polynomials in t (u = U_i + h t), in fp64.
 // ---------------------------------------------------------------------------
-__global__ void span_tables_kernel(const double* __restrict__ U, int p, int nsp, int rec,
-                                   float* __restrict__ coef, float* __restrict__ invh) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nsp) return;
-    const int i = p + s;
+// Power-basis coefficients of the p+1 non-zero basis functions on knot span
+// i (local t = (u - U_i)/h, u = U_i + h t): P[r][m] = coefficient of t^m of
+// N_{i-p+r,p}.  Cox-de Boor recursion on polynomials in t, fp64.
+__device__ void span_poly(const double* __restrict__ U, int p, int i, double (&P)[kMaxP + 1][kMaxP + 1]) {
     const double Ui = U[i], h = U[i + 1] - U[i];
-    float* out = coef + (int64_t)s * rec;
-    for (int q = 0; q < rec; ++q) out[q] = 0.f;
-    if (!(h > 0.0)) {
-        invh[s] = 0.f;
-        return;
-    }
-    invh[s] = (float)(1.0 / h);
-    double P[kMaxP + 1][kMaxP + 1];  // P[r][m]: function r of the current level, coefficient of t^m
     double Nx[kMaxP + 1][kMaxP + 1];
     for (int r = 0; r <= kMaxP; ++r)
         for (int m = 0; m <= kMaxP; ++m) P[r][m] = 0.0;
@@ -161,8 +152,100 @@ __global__ void span_tables_kernel(const double* __restrict__ U, int p, int nsp,
         for (int r = 0; r <= k; ++r)
             for (int m = 0; m <= kMaxP; ++m) P[r][m] = Nx[r][m];
     }
+}
+
+__global__ void span_tables_kernel(const double* __restrict__ U, int p, int nsp, int rec,
+                                   float* __restrict__ coef, float* __restrict__ invh) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nsp) return;
+    const int i = p + s;
+    const double h = U[i + 1] - U[i];
+    float* out = coef + (int64_t)s * rec;
+    for (int q = 0; q < rec; ++q) out[q] = 0.f;
+    if (!(h > 0.0)) {
+        invh[s] = 0.f;
+        return;
+    }
+    invh[s] = (float)(1.0 / h);
+    double P[kMaxP + 1][kMaxP + 1];
+    span_poly(U, p, i, P);
     for (int a = 0; a <= p; ++a)
         for (int m = 0; m <= p; ++m) out[a * (p + 1) + m] = (float)P[a][m];
+}
+
+// Bezier extraction operator of span s: N_{s+a}(t) = sum_j D[a][j] B_j(t) with
+// the Bernstein polynomials B_j(t) = C(p,j) t^j (1-t)^(p-j).  From the power
+// form: t^m = sum_{j>=m} C(j,m)/C(p,m) B_j(t).  All D >= 0 (convex weights).
+__device__ double binom_d(int n, int k) {
+    double r = 1.0;
+    for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+    return r;
+}
+
+__global__ void bezier_tables_kernel(const double* __restrict__ U, int p, int nsp, double* __restrict__ D) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nsp) return;
+    const int i = p + s;
+    double* out = D + (int64_t)s * (p + 1) * (p + 1);
+    for (int q = 0; q < (p + 1) * (p + 1); ++q) out[q] = 0.0;
+    if (!(U[i + 1] - U[i] > 0.0)) return;
+    double P[kMaxP + 1][kMaxP + 1];
+    span_poly(U, p, i, P);
+    for (int a = 0; a <= p; ++a)
+        for (int j = 0; j <= p; ++j) {
+            double acc = 0.0;
+            for (int m = 0; m <= j; ++m) acc += binom_d(j, m) / binom_d(p, m) * P[a][m];
+            out[a * (p + 1) + j] = acc;
+        }
+}
+
+// K1b: Bezier blocks.  Block (su,sv,sw) holds the (p+1)^3 Bernstein
+// coefficients of the spline on that span triple:
+//   Z[l][k][j] = sum_{c,b,a} Dw[c][l] Dv[b][k] Du[a][j] P[sw+c][sv+b][su+a]
+// (sum-factorised, fp64), stored as rows of bez_row(p) floats, j fastest.
+template <int P>
+__global__ void bezier_blocks_kernel(const float* __restrict__ Pg, int nu, int nv, const double* __restrict__ Du,
+                                     const double* __restrict__ Dv, const double* __restrict__ Dw, int Su, int Sv,
+                                     int64_t nblocks, float* __restrict__ out) {
+    constexpr int Q = P + 1, R = bez_row(P);
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < nblocks;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int su = (int)(idx % Su);
+        const int sv = (int)((idx / Su) % Sv);
+        const int sw = (int)(idx / ((int64_t)Su * Sv));
+        const double* du = Du + (int64_t)su * Q * Q;
+        const double* dv = Dv + (int64_t)sv * Q * Q;
+        const double* dw = Dw + (int64_t)sw * Q * Q;
+        double X[Q][Q][Q], Y[Q][Q][Q];
+        for (int c = 0; c < Q; ++c)
+            for (int b = 0; b < Q; ++b) {
+                const float* row = Pg + ((int64_t)(sw + c) * nv + (sv + b)) * nu + su;
+                double g[Q];
+                for (int a = 0; a < Q; ++a) g[a] = (double)row[a];
+                for (int j = 0; j < Q; ++j) {
+                    double acc = 0.0;
+                    for (int a = 0; a < Q; ++a) acc += du[a * Q + j] * g[a];
+                    X[c][b][j] = acc;
+                }
+            }
+        for (int c = 0; c < Q; ++c)
+            for (int k = 0; k < Q; ++k)
+                for (int j = 0; j < Q; ++j) {
+                    double acc = 0.0;
+                    for (int b = 0; b < Q; ++b) acc += dv[b * Q + k] * X[c][b][j];
+                    Y[c][k][j] = acc;
+                }
+        float* o = out + idx * (Q * Q * R);
+        for (int l = 0; l < Q; ++l)
+            for (int k = 0; k < Q; ++k) {
+                for (int j = 0; j < Q; ++j) {
+                    double acc = 0.0;
+                    for (int c = 0; c < Q; ++c) acc += dw[c * Q + l] * Y[c][k][j];
+                    o[(l * Q + k) * R + j] = (float)acc;
+                }
+                for (int j = Q; j < R; ++j) o[(l * Q + k) * R + j] = 0.f;
+            }
+    }
 }
 
 __global__ void knot_tables_kernel(const double* __restrict__ U, int p, int nsp, float* __restrict__ kh,
@@ -257,10 +340,13 @@ static mfa_status validate_knots(int d, int p, int64_t n, const double* U, int* 
     return MFA_OK;
 }
 
-extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3], const double* const knots[3],
-                                       const float* ctrl, int32_t ctrl_on_device, mfa_stream stream,
-                                       mfa_model* out) {
+extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t nctrl[3],
+                                          const double* const knots[3], const float* ctrl, int32_t ctrl_on_device,
+                                          const mfa_model_options* opt, mfa_stream stream, mfa_model* out) {
     if (!out) return fail(MFA_ERR_INVALID_ARG, "out is NULL");
+    const int want_layout = opt ? opt->layout : MFA_LAYOUT_AUTO;
+    if (want_layout < MFA_LAYOUT_AUTO || want_layout > MFA_LAYOUT_BEZIER)
+        return fail(MFA_ERR_INVALID_ARG, "options.layout out of range");
     *out = nullptr;
     if (!degree || !nctrl || !knots || !ctrl) return fail(MFA_ERR_INVALID_ARG, "NULL argument");
     const int p = degree[0];
@@ -321,14 +407,6 @@ extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nc
     unsigned int init[3] = {0xffffffffu, 0u, 0u};
     cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, st);
     minmax_kernel<<<1184, 256, 0, st>>>(Pdev, npts, mm);
-    // bricked row quads
-    for (int d = 0; d < 3; ++d) m->nb[d] = (int)((nctrl[d] - p + kBrick - 1) / kBrick);
-    const int EU = brick_eu(p), EV = brick_ev(p), EW = brick_ev(p);
-    const int64_t qn = (int64_t)m->nb[0] * m->nb[1] * m->nb[2] * EU * EV * EW;
-    if ((e = cudaMalloc(&m->Q, qn * sizeof(float4))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc Q"));
-    relayout_bricks_kernel<<<4736, 256, 0, st>>>(Pdev, m->Q, (int)nu, (int)nv, (int)nw, m->nb[0], m->nb[1], EU, EV,
-                                                  EW, qn);
-    m->device_bytes = qn * (int64_t)sizeof(float4);
     if ((e = cudaMalloc(&m->queue, kQueueSlots * sizeof(unsigned int))) != cudaSuccess)
         return cleanup(cuda_fail(e, "cudaMalloc queue"));
     cudaMemsetAsync(m->queue, 0, kQueueSlots * sizeof(unsigned int), st);
@@ -396,20 +474,65 @@ extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nc
         A.ic_hi = nsp - p;
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(cuda_fail(e, "model ingest kernels"));
-    unsigned int hmm[3];
-    if ((e = cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
-        return cleanup(cuda_fail(e, "copy range"));
     for (int d = 0; d < 3; ++d) {
         AxisTables& A = m->ax[d];
-        if (A.uniform && A.ic_hi >= A.ic_lo) {
-            if ((e = cudaMemcpyAsync(A.interior, A.coef + (int64_t)A.ic_lo * rec, sizeof(float) * (p + 1) * (p + 1),
-                                     cudaMemcpyDeviceToHost, st)) != cudaSuccess)
-                return cleanup(cuda_fail(e, "copy interior"));
-        } else {
+        if (!(A.uniform && A.ic_hi >= A.ic_lo)) {
             A.ic_lo = 0;
             A.ic_hi = -1;
         }
     }
+
+    // ---- control-point layout ----------------------------
+    const bool nonuni = !(uniform[0] && uniform[1] && uniform[2]);
+    bool bez = want_layout == MFA_LAYOUT_BEZIER || (want_layout == MFA_LAYOUT_AUTO && nonuni && p <= 3);
+    if (bez && p > 3) return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs degree <= 3"));
+    if (bez) {
+        const int64_t S0 = nctrl[0] - p, S1 = nctrl[1] - p, S2 = nctrl[2] - p;
+        const int64_t nblk = S0 * S1 * S2;
+        const int64_t bfl = (int64_t)(p + 1) * (p + 1) * bez_row(p);      // floats per block
+        e = cudaMalloc(&m->Q, nblk * bfl * sizeof(float));
+        if (e != cudaSuccess) {
+            m->Q = nullptr;
+            if (want_layout == MFA_LAYOUT_BEZIER) return cleanup(cuda_fail(e, "cudaMalloc Bezier blocks"));
+            cudaGetLastError();   // AUTO: fall back to the quad layout
+            bez = false;
+        } else {
+            double* D = nullptr;
+            const int64_t q2 = (int64_t)(p + 1) * (p + 1);
+            if ((e = cudaMalloc(&D, sizeof(double) * q2 * (S0 + S1 + S2))) != cudaSuccess)
+                return cleanup(cuda_fail(e, "cudaMalloc extraction"));
+            double* Dax[3] = {D, D + q2 * S0, D + q2 * (S0 + S1)};
+            for (int d = 0; d < 3; ++d) {
+                const int nsp = (int)(nctrl[d] - p);
+                bezier_tables_kernel<<<(nsp + 127) / 128, 128, 0, st>>>((const double*)((char*)Udev + uoff[d]), p, nsp,
+                                                                       Dax[d]);
+            }
+            float* out = reinterpret_cast<float*>(m->Q);
+            switch (p) {
+                case 1: bezier_blocks_kernel<1><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out); break;
+                case 2: bezier_blocks_kernel<2><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out); break;
+                default: bezier_blocks_kernel<3><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out); break;
+            }
+            cudaStreamSynchronize(st);
+            cudaFree(D);
+            m->device_bytes += nblk * bfl * (int64_t)sizeof(float);
+            m->layout = kBezier;
+        }
+    }
+    if (!bez) {   // bricked row quads
+        for (int d = 0; d < 3; ++d) m->nb[d] = (int)((nctrl[d] - p + kBrick - 1) / kBrick);
+        const int EU = brick_eu(p), EV = brick_ev(p), EW = brick_ev(p);
+        const int64_t qn = (int64_t)m->nb[0] * m->nb[1] * m->nb[2] * EU * EV * EW;
+        if ((e = cudaMalloc(&m->Q, qn * sizeof(float4))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc Q"));
+        relayout_bricks_kernel<<<4736, 256, 0, st>>>(Pdev, m->Q, (int)nu, (int)nv, (int)nw, m->nb[0], m->nb[1], EU, EV,
+                                                      EW, qn);
+        m->device_bytes += qn * (int64_t)sizeof(float4);
+        m->layout = kQuads;
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(cuda_fail(e, "layout kernels"));
+    unsigned int hmm[3];
+    if ((e = cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "copy range"));
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cleanup(cuda_fail(e, "model ingest"));
     if (hmm[2] != 0)
         return cleanup(fail(MFA_ERR_DOMAIN, std::to_string(hmm[2]) + " non-finite control values"));
@@ -418,6 +541,12 @@ extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nc
     cleanup(MFA_OK);
     *out = reinterpret_cast<mfa_model>(m);
     return MFA_OK;
+}
+
+extern "C" mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3], const double* const knots[3],
+                                       const float* ctrl, int32_t ctrl_on_device, mfa_stream stream,
+                                       mfa_model* out) {
+    return mfa_model_create_ex(degree, nctrl, knots, ctrl, ctrl_on_device, nullptr, stream, out);
 }
 
 extern "C" mfa_status mfa_model_info(mfa_model h, mfa_model_desc* out) {
@@ -432,6 +561,7 @@ extern "C" mfa_status mfa_model_info(mfa_model h, mfa_model_desc* out) {
     out->v_max = m->vmax;
     out->device_bytes = m->device_bytes;
     out->device = m->device;
+    out->layout = m->layout == kBezier ? MFA_LAYOUT_BEZIER : MFA_LAYOUT_QUADS;
     return MFA_OK;
 }
 

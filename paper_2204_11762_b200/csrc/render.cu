@@ -25,6 +25,7 @@ namespace mfa {
 struct RenderArgs {
     const float4* Q;
     BrickGrid g;
+    BezGrid bg;
     AxisArgs ax[3];
     const float4* tf;
     int tf_n;
@@ -91,10 +92,14 @@ __device__ __forceinline__ void compute_frame(const mfa_camera& c, ViewFrame& fr
 #ifndef MFA_RENDER_CACHE
 #define MFA_RENDER_CACHE 1
 #endif
+#ifndef MFA_RENDER_PREFETCH
+#define MFA_RENDER_PREFETCH 0
+#endif
 
-template <int P, bool UNI, bool SHADE>
+template <int P, int LAYOUT, bool UNI, bool SHADE>
 __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderArgs args) {
-    constexpr bool CACHE = MFA_RENDER_CACHE && P <= 3;
+    constexpr bool BEZ = LAYOUT == kBezier;
+    constexpr bool CACHE = (MFA_RENDER_CACHE && P <= 3) || BEZ;
     extern __shared__ float4 s_tf[];
     __shared__ ViewFrame s_frame[kMaxViewsPerLaunch];
 
@@ -225,12 +230,30 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                     }
                 }
                 // a6: neighbourhood of the span triple
-                const int64_t e = brick_entry<P>(args.g, s[0], s[1], s[2]);
-                const float4* q = args.Q + e;
                 float val, gu = 0.f, gv = 0.f, gw = 0.f;
-                if constexpr (CACHE) {
+                if constexpr (BEZ) {
+                    const int64_t e = ((int64_t)s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
                     if (e != nb_key) {       // reload only when the span triple changed
-                        load_block<P>(q, nb);
+                        load_bblock<P>(bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]), nb);
+                        nb_key = e;
+                    }
+                    if (SHADE) {  // a5: Bernstein basis, the same polynomials on every span
+                        float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                        bernstein<P, false>(t[0], Bu);
+                        bernstein<P, true>(t[1], Bv);
+                        bernstein<P, false>(t[2], Bw);
+                        contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                    } else {
+                        float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                        bernstein_value<P>(t[0], Nu);
+                        bernstein_value<P>(t[1], Nv);
+                        bernstein_value<P>(t[2], Nw);
+                        val = contract_v_cached<P>(nb, Nu, Nv, Nw);
+                    }
+                } else if constexpr (CACHE) {
+                    const int64_t e = brick_entry<P>(args.g, s[0], s[1], s[2]);
+                    if (e != nb_key) {       // reload only when the span triple changed
+                        load_block<P>(args.Q + e, nb);
                         nb_key = e;
                     }
                     if (SHADE) {
@@ -247,6 +270,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                         val = contract_v_cached<P>(nb, Nu, Nv, Nw);
                     }
                 } else {
+                    const float4* q = args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
                     // issue slab 0 before the basis math; slabs stream through a double buffer
                     float r0[P + 1][P + 1];
                     load_slab<P>(q, r0);
@@ -305,6 +329,20 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 #pragma unroll
                 for (int i = 0; i < 3; ++i) F[i] += DF[i];
                 live = !(A > args.o_max) && k < K;
+                if constexpr (BEZ && MFA_RENDER_PREFETCH) {
+                    // bring the next sample's block into L1 while this warp's
+                    // other work (and other warps) proceed
+                    if (live) {
+                        int sn[3];
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            if constexpr (UNI) sn[i] = uni_span_only(F[i], args.ax[i].nsp);
+                            else sn[i] = nu_span_only(nu[i], F[i], args.ax[i].nsp);
+                        }
+                        const int64_t en = ((int64_t)sn[2] * args.bg.S1 + sn[1]) * args.bg.S0 + sn[0];
+                        if (en != nb_key) prefetch_bblock<P>(bez_block<P>(args.Q, args.bg, sn[0], sn[1], sn[2]));
+                    }
+                }
             }
         }
         // ---- a11: pixel write ---------------------------------------------
@@ -330,10 +368,10 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
     }
 }
 
-template <int P, bool UNI, bool SHADE>
+template <int P, int LAYOUT, bool UNI, bool SHADE>
 static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(float4) * a.tf_n;
-    auto kern = render_kernel<P, UNI, SHADE>;
+    auto kern = render_kernel<P, LAYOUT, UNI, SHADE>;
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -347,10 +385,19 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+template <int P, int LAYOUT>
+static cudaError_t dispatch_render_l(const RenderArgs& a, bool uni, bool shade, cudaStream_t st) {
+    if (uni)
+        return shade ? launch_render_t<P, LAYOUT, true, true>(a, st) : launch_render_t<P, LAYOUT, true, false>(a, st);
+    return shade ? launch_render_t<P, LAYOUT, false, true>(a, st) : launch_render_t<P, LAYOUT, false, false>(a, st);
+}
+
 template <int P>
-static cudaError_t dispatch_render(const RenderArgs& a, bool uni, bool shade, cudaStream_t st) {
-    if (uni) return shade ? launch_render_t<P, true, true>(a, st) : launch_render_t<P, true, false>(a, st);
-    return shade ? launch_render_t<P, false, true>(a, st) : launch_render_t<P, false, false>(a, st);
+static cudaError_t dispatch_render(const RenderArgs& a, int layout, bool uni, bool shade, cudaStream_t st) {
+    if constexpr (P <= 3) {
+        if (layout == kBezier) return dispatch_render_l<P, kBezier>(a, uni, shade, st);
+    }
+    return dispatch_render_l<P, kQuads>(a, uni, shade, st);
 }
 
 static std::atomic<unsigned> g_slot{0};
@@ -362,6 +409,8 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->Q = m->Q;
     a->g.nbx = m->nb[0];
     a->g.nby = m->nb[1];
+    a->bg.S0 = (int)(m->n[0] - m->p);
+    a->bg.S1 = (int)(m->n[1] - m->p);
     for (int d = 0; d < 3; ++d) a->ax[d] = make_axis_args(m->ax[d]);
     a->tf = reinterpret_cast<const float4*>(tf->rgba);
     a->tf_n = tf->n_entries;
@@ -396,11 +445,11 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         cudaError_t r = cudaMemsetAsync(a->queue, 0, sizeof(unsigned int), st);
         if (r != cudaSuccess) return r;
         switch (m->p) {
-            case 1: return dispatch_render<1>(*a, uni, shade, st);
-            case 2: return dispatch_render<2>(*a, uni, shade, st);
-            case 3: return dispatch_render<3>(*a, uni, shade, st);
-            case 4: return dispatch_render<4>(*a, uni, shade, st);
-            default: return dispatch_render<5>(*a, uni, shade, st);
+            case 1: return dispatch_render<1>(*a, m->layout, uni, shade, st);
+            case 2: return dispatch_render<2>(*a, m->layout, uni, shade, st);
+            case 3: return dispatch_render<3>(*a, m->layout, uni, shade, st);
+            case 4: return dispatch_render<4>(*a, m->layout, uni, shade, st);
+            default: return dispatch_render<5>(*a, m->layout, uni, shade, st);
         }
     };
     if (tiles) {

@@ -20,9 +20,9 @@ def workload(c, **kw):
 
 
 @functools.lru_cache(maxsize=None)
-def gpu_model(c):
+def gpu_model(c, layout="auto"):
     from paper_2204_11762_b200 import Model
-    return Model.from_workload(workload(c))
+    return Model.from_workload(workload(c), layout=layout)
 
 
 @functools.lru_cache(maxsize=None)
@@ -223,3 +223,31 @@ def test_invalid_models_raise():
     m = Model(p, [good, good, good], ctrl + 2)
     info = m.info()
     assert info["v_min"] == 2 and info["v_max"] == 2 and info["uniform"] == (1, 1, 1)
+
+
+@pytest.mark.parametrize("c,layout", [(1, "bezier"), (2, "bezier"), (3, "bezier"), (5, "quads")])
+def test_both_layouts_eval_and_render(c, layout):
+    """Each model also through the other control-point layout (bricked quads
+    vs Bezier blocks): eval parity on random + boundary points and a render
+    parity check (a reduced image for C3/C5)."""
+    w = workload(c) if c in (1, 2) else workload(c, width=256, height=192, n_views=1)
+    m = gpu_model(c, layout)
+    assert m.info()["layout"] == layout
+    u, v, ww = WL.query_points(c, 1 << 16)
+    bu, bv, bw = WL.boundary_points(w)
+    u, v, ww = (np.concatenate([a, b]) for a, b in ((u, bu), (v, bv), (ww, bw)))
+    got = gpu_eval(m, u, v, ww)
+    ref, sig, _ = oracle_model(c).eval_batch(u, v, ww)
+    parity.check_eval(got, ref, sig, f"C{c} {layout}")
+    vo = gpu_eval(m, u, v, ww, grad=False)
+    parity.check_eval(vo, ref[:, :1], sig[:, :1], f"C{c} {layout} value-only")
+    samples = torch.zeros(1, dtype=torch.int64, device="cuda")
+    img = m.render(w.cameras[:1], cuda(w.tf), w.v_lo, w.v_hi, w.params, samples=samples)
+    torch.cuda.synchronize()
+    r = O.render(oracle_model(c), w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
+    parity.check_image(img[0].cpu().numpy().reshape(-1, 4), r, f"C{c} {layout} render")
+
+
+def test_default_layouts():
+    assert gpu_model(3).info()["layout"] == "quads"
+    assert gpu_model(5).info()["layout"] == "bezier"

@@ -13,10 +13,14 @@ ap.add_argument("workload")
 ap.add_argument("--views", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--eval", action="store_true", help="profile mfa_eval_batch on 2^24 points instead")
+ap.add_argument("--uniform-knots", action="store_true", help="diagnostic: replace the knots by uniform ones")
+ap.add_argument("--layout", default="auto")
 a = ap.parse_args()
 c = int(a.workload[1:])
 w = WL.make_config(c, **({"n_views": a.views} if a.views else {}))
-m = Model.from_workload(w)
+if a.uniform_knots:
+    w.knots = [WL.clamped_uniform_knots(n, w.degree) for n in w.nctrl]
+m = Model.from_workload(w, layout=a.layout)
 if a.eval:
     u, v, ww = (torch.from_numpy(x).cuda() for x in WL.query_points(c, 1 << 24))
     for _ in range(a.reps):
