@@ -80,26 +80,40 @@ __device__ __forceinline__ void compute_frame(const mfa_camera& c, ViewFrame& fr
     }
 }
 
-#ifndef MFA_RENDER_THREADS   // persistent CTA size (warps fetch work independently)
-#define MFA_RENDER_THREADS 128
-#endif
-#ifdef MFA_RENDER_MINB   // tuning experiments: force min resident CTAs per SM
-#define MFA_RENDER_BOUNDS __launch_bounds__(MFA_RENDER_THREADS, MFA_RENDER_MINB)
-#else
-#define MFA_RENDER_BOUNDS __launch_bounds__(MFA_RENDER_THREADS)
-#endif
-
+// Launch shape per instantiation (measured on B200):
+//   p <= 3 (neighbourhood cache, ~160-170 registers): 128-thread CTAs, >= 3 per SM
+//   p >= 4 (streamed slabs): 256-thread CTAs capped at 128 registers (2 per SM)
 #ifndef MFA_RENDER_CACHE
 #define MFA_RENDER_CACHE 1
+#endif
+#ifndef MFA_BEZ_CACHE
+#define MFA_BEZ_CACHE 1
 #endif
 #ifndef MFA_RENDER_PREFETCH
 #define MFA_RENDER_PREFETCH 0
 #endif
 
+template <int P, int LAYOUT>
+struct RenderShape {
+    static constexpr bool BEZ = LAYOUT == kBezier;
+    static constexpr bool CACHE = BEZ ? (bool)MFA_BEZ_CACHE : (MFA_RENDER_CACHE && P <= 3);
+#ifdef MFA_RENDER_THREADS
+    static constexpr int THREADS = MFA_RENDER_THREADS;
+#else
+    static constexpr int THREADS = P <= 3 ? 128 : 256;
+#endif
+#ifdef MFA_RENDER_MINB
+    static constexpr int MINB = MFA_RENDER_MINB;
+#else
+    static constexpr int MINB = P <= 3 ? (CACHE ? 3 : 4) : 2;
+#endif
+};
+
 template <int P, int LAYOUT, bool UNI, bool SHADE>
-__global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderArgs args) {
+__global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P, LAYOUT>::MINB)
+    render_kernel(const __grid_constant__ RenderArgs args) {
     constexpr bool BEZ = LAYOUT == kBezier;
-    constexpr bool CACHE = (MFA_RENDER_CACHE && P <= 3) || BEZ;
+    constexpr bool CACHE = RenderShape<P, LAYOUT>::CACHE;
     extern __shared__ float4 s_tf[];
     __shared__ ViewFrame s_frame[kMaxViewsPerLaunch];
 
@@ -231,7 +245,26 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 }
                 // a6: neighbourhood of the span triple
                 float val, gu = 0.f, gv = 0.f, gw = 0.f;
-                if constexpr (BEZ) {
+                if constexpr (BEZ && !CACHE) {   // stream the block slab by slab
+                    const float4* q = bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]);
+                    float r0[P + 1][P + 1];
+                    load_bslab<P>(q, r0);
+                    if (SHADE) {
+                        float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                        bernstein<P, false>(t[0], Bu);
+                        bernstein<P, true>(t[1], Bv);
+                        bernstein<P, false>(t[2], Bw);
+                        contract_vg_bez<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
+                    } else {
+                        float nbv[P + 1][P + 1][P + 1];
+                        load_bblock<P>(q, nbv);
+                        float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                        bernstein_value<P>(t[0], Nu);
+                        bernstein_value<P>(t[1], Nv);
+                        bernstein_value<P>(t[2], Nw);
+                        val = contract_v_cached<P>(nbv, Nu, Nv, Nw);
+                    }
+                } else if constexpr (BEZ) {
                     const int64_t e = ((int64_t)s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
                     if (e != nb_key) {       // reload only when the span triple changed
                         load_bblock<P>(bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]), nb);
@@ -329,7 +362,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 #pragma unroll
                 for (int i = 0; i < 3; ++i) F[i] += DF[i];
                 live = !(A > args.o_max) && k < K;
-                if constexpr (BEZ && MFA_RENDER_PREFETCH) {
+                if constexpr (BEZ && CACHE && MFA_RENDER_PREFETCH) {
                     // bring the next sample's block into L1 while this warp's
                     // other work (and other warps) proceed
                     if (live) {
@@ -375,7 +408,7 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    constexpr int kThreads = MFA_RENDER_THREADS;
+    constexpr int kThreads = RenderShape<P, LAYOUT>::THREADS;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
     if (occ < 1) occ = 1;
     int64_t grid = (int64_t)sms * occ;
