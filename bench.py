@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--out-fp16", action="store_true")
+    ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier"],
+                    help="control-point layout (default: the library's choice)")
     return ap.parse_args()
 
 
@@ -199,7 +201,7 @@ def run_ours(args):
     V = len(w.cameras)
     W, H = w.cameras[0].width, w.cameras[0].height
     stream = torch.cuda.current_stream()
-    m = Model.from_workload(w)
+    m = Model.from_workload(w, layout=args.layout)
     info = m.info()
     tf = torch.from_numpy(w.tf).cuda()
     out_dt = torch.float16 if args.out_fp16 else torch.float32
@@ -310,11 +312,12 @@ def run_ours(args):
             "data": "synthetic (seeded generator of the BASELINE.json config recipe; no dataset)",
             "config": {"workload": w.name, "views": V, "width": W, "height": H, "degree": p,
                        "nctrl": list(w.nctrl), "uniform_knots": bool(w.uniform), "step_spans": w.step_spans,
+                       "layout": info["layout"],
                        "shading": int(w.params.shading), "o_max": w.params.o_max,
                        "out": "fp16" if args.out_fp16 else "fp32",
                        "parallelism": f"screen-tile sharding x{world}, model replicated, NCCL all-gather"
                        if world > 1 else "single GPU",
-                       "l2": f"inputs larger than L2: row-quad grid {info['device_bytes'] / 2**20:.0f} MiB, "
+                       "l2": f"inputs larger than L2: {info['layout']} control-point layout {info['device_bytes'] / 2**20:.0f} MiB, "
                              f"image {V * H * W * (8 if args.out_fp16 else 16) / 2**20:.0f} MiB per step"},
             "frames_per_s": V * args.steps / (ms_max / 1e3),
             "samples_per_step": samples_all / args.steps,

@@ -291,14 +291,17 @@ __device__ __forceinline__ void nu_init(const AxisArgs& A, long long F, NUAxis& 
 }
 
 __device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis& st) {
-    F = max(F, 0LL);
-    F = min(F, 1LL << kNonUniFracBits);
-    if (F >= st.hi || F < st.lo) {
+    // F may leave [0, 2^62] by rounding at the entry/exit faces only; the span
+    // index is kept in range and the local offset is clamped below instead of
+    // clamping the 64-bit coordinate.
+    const bool fwd = F >= st.hi;                 // hi of the last span is INT64_MAX
+    const bool bwd = F < st.lo && st.s > 0;
+    if (fwd || bwd) {
         // common case: the sample moved into the neighbouring span; the new
         // bounds and scale are three independent loads (one round trip)
-        st.s += (F >= st.hi) ? 1 : -1;
+        st.s += fwd ? 1 : -1;
         nu_load(A, st);
-        if (F >= st.hi || F < st.lo) {   // rare: crossed more than one span this step
+        if (F >= st.hi || (F < st.lo && st.s > 0)) {   // rare: crossed more than one span this step
             int s = st.s;
             while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
             while (s > 0 && F < __ldg(A.kfx + s)) --s;
@@ -306,8 +309,9 @@ __device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis&
             nu_load(A, st);
         }
     }
-    const unsigned long long d = (unsigned long long)(F - st.lo) >> A.dshift;   // < 2^23
-    const float fd = __uint_as_float(0x4b000000u | (unsigned)d) - 8388608.0f;
+    int d = (int)((F - st.lo) >> A.dshift);     // < 2^23 inside the span
+    d = min(max(d, 0), 8388607);
+    const float fd = __int_as_float(0x4b000000 | d) - 8388608.0f;
     return fd * st.tsc;
 }
 
@@ -584,19 +588,35 @@ __device__ __forceinline__ void contract_vg_bez(const float4* __restrict__ q, fl
     gu = gvu.y;
 }
 
-// L1 prefetch of one Bezier block (the next sample's) -- a hint, no registers.
-template <int P>
+// Prefetch of one Bezier block -- a hint, no registers (L1 for the next
+// sample, L2 for one several samples ahead).
+template <int P, bool L2>
 __device__ __forceinline__ void prefetch_bblock(const float4* q) {
     constexpr int BYTES = BezBlock<P>::FLOATS * 4;
 #pragma unroll
-    for (int off = 0; off < BYTES; off += 128)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(q) + off));
+    for (int off = 0; off < BYTES; off += 128) {
+        if constexpr (L2)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(q) + off));
+        else
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(q) + off));
+    }
 }
 
 // Span of the next sample on a uniform axis (prefetch prediction only).
 __device__ __forceinline__ int uni_span_only(long long F, int S) {
     int s = (int)(F >> kUniFracBits);
     return min(max(s, 0), S - 1);
+}
+
+// Span a few samples ahead on a non-uniform axis (prefetch prediction only):
+// one step past the cached bounds, else the bucket of the coordinate.
+__device__ __forceinline__ int nu_span_ahead(const AxisArgs& A, const NUAxis& st, long long F) {
+    if (F < st.hi && F >= st.lo) return st.s;
+    F = max(F, 0LL);
+    F = min(F, (1LL << kNonUniFracBits) - 1);
+    int b = (int)(F >> A.mshift);
+    b = min(max(b, 0), A.M - 1);
+    return __ldg(A.bucket + b);
 }
 
 // Span of the next sample on a non-uniform axis: one step past the cached

@@ -35,6 +35,7 @@ struct RenderArgs {
     float gsc[3];                 // gradient scale to physical units (uniform: S/L; non-uniform: 1/L)
     float o_max, ka, kd, ks, shin, eps2;
     int W, H, tiles_x, tiles_y;
+    int st_x, st_y;               // supertiles (8x8 tiles) per view, full-frame order
     int n_views;
     const int* tiles;             // NULL: full frames
     int64_t n_tiles;
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
-    const int per_view = args.tiles_x * args.tiles_y;
+    const int per_view = args.st_x * args.st_y * 64;   // units are ordered by 8x8-tile supertiles
     unsigned long long my_samples = 0;
 
     for (;;) {
@@ -140,10 +141,14 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             ty = __ldg(args.tiles + 3 * tile_id + 2);
             if (view < 0) continue;  // padding unit (multi-GPU equal-size buffers)
         } else {
+            // supertile order: the ~200 tiles in flight form a compact image
+            // region, so neighbouring rays reuse control blocks from L1/L2
             view = (int)(tile_id / per_view);
             const int t = (int)(tile_id % per_view);
-            ty = t / args.tiles_x;
-            tx = t % args.tiles_x;
+            const int st = t >> 6, lt = t & 63;
+            tx = (st % args.st_x) * 8 + (lt & 7);
+            ty = (st / args.st_x) * 8 + (lt >> 3);
+            if (tx >= args.tiles_x || ty >= args.tiles_y) continue;
         }
         const ViewFrame& fr = s_frame[view];
         const int lx = (sub & 1) * 8 + (lane & 7);
@@ -324,7 +329,11 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 // a8: transfer function (l.7)
                 float f = (val - args.v_lo) * args.s_scale;
                 f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
-                const int i0 = min((int)f, args.tf_n - 2);
+                // i0 = round(f - 1/2) via the 2^23 magic number (no F2I): any
+                // i0 in {floor(f), f - 1 at integers} gives the same lerp
+                const float fm = f + 8388607.5f;
+                int i0 = __float_as_int(fm) - 0x4b000000;
+                i0 = min(max(i0, 0), args.tf_n - 2);
                 const float wt = f - (float)i0;
                 const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
                 float cr = fmaf(wt, T1.x - T0.x, T0.x);
@@ -362,18 +371,19 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
 #pragma unroll
                 for (int i = 0; i < 3; ++i) F[i] += DF[i];
                 live = !(A > args.o_max) && k < K;
-                if constexpr (BEZ && CACHE && MFA_RENDER_PREFETCH) {
-                    // bring the next sample's block into L1 while this warp's
-                    // other work (and other warps) proceed
+                if constexpr (BEZ && CACHE && MFA_RENDER_PREFETCH > 0) {
+                    // bring the block MFA_RENDER_PREFETCH samples ahead into L2 so
+                    // its first touch does not wait on DRAM
                     if (live) {
                         int sn[3];
 #pragma unroll
                         for (int i = 0; i < 3; ++i) {
-                            if constexpr (UNI) sn[i] = uni_span_only(F[i], args.ax[i].nsp);
-                            else sn[i] = nu_span_only(nu[i], F[i], args.ax[i].nsp);
+                            const long long Fa = F[i] + (long long)(MFA_RENDER_PREFETCH - 1) * DF[i];
+                            if constexpr (UNI) sn[i] = uni_span_only(Fa, args.ax[i].nsp);
+                            else sn[i] = nu_span_ahead(args.ax[i], nu[i], Fa);
                         }
                         const int64_t en = ((int64_t)sn[2] * args.bg.S1 + sn[1]) * args.bg.S0 + sn[0];
-                        if (en != nb_key) prefetch_bblock<P>(bez_block<P>(args.Q, args.bg, sn[0], sn[1], sn[2]));
+                        if (en != nb_key) prefetch_bblock<P, (MFA_RENDER_PREFETCH > 1)>(bez_block<P>(args.Q, args.bg, sn[0], sn[1], sn[2]));
                     }
                 }
             }
@@ -466,6 +476,8 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->H = cams[0].height;
     a->tiles_x = (a->W + MFA_TILE - 1) / MFA_TILE;
     a->tiles_y = (a->H + MFA_TILE - 1) / MFA_TILE;
+    a->st_x = (a->tiles_x + 7) / 8;
+    a->st_y = (a->tiles_y + 7) / 8;
     a->out = out;
     a->out_fp16 = prm->out_fp16;
     a->samples = samples;
@@ -505,7 +517,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
             for (int v = 0; v < nv; ++v) a->cams[v] = cams[v0 + v];
             a->n_views = nv;
             a->view_base = v0;
-            a->n_units = (int64_t)nv * a->tiles_x * a->tiles_y * 8;
+            a->n_units = (int64_t)nv * a->st_x * a->st_y * 64 * 8;
             e = run();
         }
     }
