@@ -284,6 +284,25 @@ def run_ours(args):
     if clocks.get("sm_mhz"):
         pk_clk, _ = RL.fp32_peak_tflops(clocks["sm_mhz"])
         roof["frac_at_observed_clock"] = achieved_tf / pk_clk
+    # north_star roofline: lesser of FP32-FMA peak / F(p) and L2 BW / B(p), both
+    # measured on this device by the K5 probes (include/mfa_probe.h)
+    try:
+        from paper_2204_11762_b200 import _lib as LB
+        p_fp32 = max(LB.probe_fp32("ffma"), LB.probe_fp32("ffma2"))
+        bw_l2 = max(LB.probe_read_bw(64 << 20, 50) for _ in range(2))
+        r_fp32 = p_fp32 * 1e12 / F
+        r_l2 = bw_l2 * 1e9 / Bs
+        per_gpu = value / world
+        roof["north_star"] = {
+            "fp32_peak_tflops_measured": p_fp32, "l2_read_gbps_measured": bw_l2,
+            "R_fp32_samples_per_s": r_fp32, "R_l2_samples_per_s": r_l2,
+            "frac_fp32": per_gpu / r_fp32, "frac_l2": per_gpu / r_l2,
+            "binding": "l2" if r_l2 < r_fp32 else "fp32", "frac": per_gpu / min(r_fp32, r_l2),
+            "note": "L2 term counts B(p) = 4(p+1)^3 bytes per sample; the kernel's register/L1 reuse "
+                    "moves far fewer bytes from L2, so the FP32 term (roofline above) is the physical ceiling",
+        }
+    except Exception as ex:  # probes are informational
+        roof["north_star"] = {"error": str(ex)}
     try:  # DRAM bytes per launch from the committed ncu --set full capture
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(w.name)
         if tr and world == 1:

@@ -22,7 +22,8 @@ LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2}
 
 # C-ABI symbols declared in include/mfa.h (checked by tests/test_abi.py)
 EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
-           "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version")
+           "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version",
+           "mfa_probe_fp32", "mfa_probe_read_bw")
 
 
 class MfaError(RuntimeError):
@@ -98,6 +99,10 @@ def lib():
         L.mfa_last_error.argtypes = []
         L.mfa_version.restype = C.c_char_p
         L.mfa_version.argtypes = []
+        L.mfa_probe_fp32.restype = C.c_int
+        L.mfa_probe_fp32.argtypes = [i32, C.POINTER(C.c_double)]
+        L.mfa_probe_read_bw.restype = C.c_int
+        L.mfa_probe_read_bw.argtypes = [i64, i32, C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -267,3 +272,17 @@ def unpack_tiles(packed, tiles, n_views, width, height, out=None, stream=None):
 
 def version() -> str:
     return lib().mfa_version().decode()
+
+
+def probe_fp32(mode: str = "ffma2") -> float:
+    """Measured FP32 FMA throughput (TFLOP/s) on the current device (K5)."""
+    v = C.c_double(0)
+    _check(lib().mfa_probe_fp32({"ffma": 0, "ffma2": 1, "ffma_imm": 2}[mode], C.byref(v)))
+    return v.value
+
+
+def probe_read_bw(nbytes: int, reps: int = 20) -> float:
+    """Measured read bandwidth (GB/s) of an nbytes buffer read reps times (K5)."""
+    v = C.c_double(0)
+    _check(lib().mfa_probe_read_bw(int(nbytes), int(reps), C.byref(v)))
+    return v.value

@@ -93,6 +93,12 @@ __device__ __forceinline__ void compute_frame(const mfa_camera& c, ViewFrame& fr
 #ifndef MFA_RENDER_PREFETCH
 #define MFA_RENDER_PREFETCH 0
 #endif
+#ifndef MFA_PREFETCH_L1
+#define MFA_PREFETCH_L1 0
+#endif
+#ifndef MFA_CTA_TILES    // -1: per shape (p >= 4), 0: off, 1: on
+#define MFA_CTA_TILES -1
+#endif
 
 template <int P, int LAYOUT>
 struct RenderShape {
@@ -108,6 +114,8 @@ struct RenderShape {
 #else
     static constexpr int MINB = P <= 3 ? (CACHE ? 3 : 4) : 2;
 #endif
+    // p >= 4: a CTA (8 warps) takes a whole 16x16 tile so its sub-tiles share L1
+    static constexpr bool CTA_TILES = MFA_CTA_TILES < 0 ? (P >= 4 && THREADS == 256) : (bool)MFA_CTA_TILES;
 };
 
 template <int P, int LAYOUT, bool UNI, bool SHADE>
@@ -126,12 +134,30 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
     const int per_view = args.st_x * args.st_y * 64;   // units are ordered by 8x8-tile supertiles
     unsigned long long my_samples = 0;
 
+    constexpr int kWarps = RenderShape<P, LAYOUT>::THREADS / 32;
+    __shared__ unsigned s_tile;
+    unsigned tile_base = 0;
+    int round_sub = 0;
     for (;;) {
-        // ---- next warp unit (8x4 pixels) from the global queue -------------
         unsigned unit = 0;
-        if (lane == 0) unit = atomicAdd(args.queue, 1u);
-        unit = __shfl_sync(0xffffffffu, unit, 0);
-        if (unit >= args.n_units) break;
+        if constexpr (RenderShape<P, LAYOUT>::CTA_TILES) {
+            // ---- the CTA takes a whole 16x16 tile; its warps share its 8
+            // sub-units, so neighbouring rays reuse blocks in this SM's L1
+            if (round_sub == 0) {
+                __syncthreads();
+                if (threadIdx.x == 0) s_tile = atomicAdd(args.queue, 1u);
+                __syncthreads();
+                tile_base = s_tile * 8u;
+            }
+            unit = tile_base + (unsigned)((threadIdx.x >> 5) + round_sub * kWarps);
+            round_sub = (round_sub + 1) % (8 / kWarps);
+            if (tile_base >= args.n_units) break;
+        } else {
+            // ---- next warp unit (8x4 pixels) from the global queue ---------
+            if (lane == 0) unit = atomicAdd(args.queue, 1u);
+            unit = __shfl_sync(0xffffffffu, unit, 0);
+            if (unit >= args.n_units) break;
+        }
         const int64_t tile_id = unit >> 3;
         const int sub = unit & 7;
         int view, tx, ty;
@@ -372,18 +398,21 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 for (int i = 0; i < 3; ++i) F[i] += DF[i];
                 live = !(A > args.o_max) && k < K;
                 if constexpr (BEZ && CACHE && MFA_RENDER_PREFETCH > 0) {
-                    // bring the block MFA_RENDER_PREFETCH samples ahead into L2 so
-                    // its first touch does not wait on DRAM
+                    // Hint the block MFA_RENDER_PREFETCH samples ahead into
+                    // L2 (MFA_PREFETCH_L1: into L1).  The span guess uses only
+                    // registers (cached bounds): s, or s +- 1 when the look-ahead
+                    // coordinate leaves them -- no dependent loads.
                     if (live) {
                         int sn[3];
 #pragma unroll
                         for (int i = 0; i < 3; ++i) {
                             const long long Fa = F[i] + (long long)(MFA_RENDER_PREFETCH - 1) * DF[i];
                             if constexpr (UNI) sn[i] = uni_span_only(Fa, args.ax[i].nsp);
-                            else sn[i] = nu_span_ahead(args.ax[i], nu[i], Fa);
+                            else sn[i] = nu_span_only(nu[i], Fa, args.ax[i].nsp);
                         }
                         const int64_t en = ((int64_t)sn[2] * args.bg.S1 + sn[1]) * args.bg.S0 + sn[0];
-                        if (en != nb_key) prefetch_bblock<P, (MFA_RENDER_PREFETCH > 1)>(bez_block<P>(args.Q, args.bg, sn[0], sn[1], sn[2]));
+                        if (en != nb_key)
+                            prefetch_bblock<P, !MFA_PREFETCH_L1>(bez_block<P>(args.Q, args.bg, sn[0], sn[1], sn[2]));
                     }
                 }
             }

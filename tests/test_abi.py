@@ -9,9 +9,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "mfa.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", f)).read() for f in ("mfa.h", "mfa_probe.h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(mfa_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(mfa_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_north_star_calls():
