@@ -137,6 +137,8 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
     a.Q = m->Q;
     a.g.nbx = m->nb[0];
     a.g.nby = m->nb[1];
+    a.g.q_f4 = m->q_f4;
+    a.bg.q_f4 = m->q_f4;
     a.bg.S0 = (int)(m->n[0] - m->p);
     a.bg.S1 = (int)(m->n[1] - m->p);
     for (int d = 0; d < 3; ++d) a.ax[d] = make_axis_args(m->ax[d]);

@@ -72,6 +72,7 @@ struct Brick {
 
 struct BrickGrid {
     int nbx, nby;          // bricks along u, v
+    int64_t q_f4;          // size of the quad array in float4 (debug bounds checks)
 };
 
 // Entry index of the neighbourhood origin (row quad of spans (su, sv, sw)).
@@ -80,7 +81,10 @@ __device__ __forceinline__ int64_t brick_entry(const BrickGrid& g, int su, int s
     const int bx = su >> kBrickLog, by = sv >> kBrickLog, bz = sw >> kBrickLog;
     const int lu = su & (kBrick - 1), lv = sv & (kBrick - 1), lw = sw & (kBrick - 1);
     const int brick = (bz * g.nby + by) * g.nbx + bx;
-    return (int64_t)brick * Brick<P>::SIZE + (lw * Brick<P>::EV + lv) * Brick<P>::EU + lu;
+    const int64_t e = (int64_t)brick * Brick<P>::SIZE + (lw * Brick<P>::EV + lv) * Brick<P>::EU + lu;
+    MFA_DCHECK(su >= 0 && sv >= 0 && sw >= 0 && e >= 0 &&
+               e + P * Brick<P>::EV * Brick<P>::EU + P * Brick<P>::EU + (P == 5 ? 5 : (P == 4 ? 2 : 1)) <= g.q_f4);
+    return e;
 }
 
 // ---------------------------------------------------------------------------
@@ -168,6 +172,7 @@ __device__ __forceinline__ void uniform_horner_value(float t, float (&N)[P + 1])
 
 template <int P, bool SWAP>
 __device__ __forceinline__ void table_horner(const float* __restrict__ coef, int s, float t, float2 (&B)[P + 1]) {
+    MFA_DCHECK(s >= 0);
     float c[rec_floats(P)];
     const float4* r = reinterpret_cast<const float4*>(coef + (int64_t)s * rec_floats(P));
 #pragma unroll
@@ -273,6 +278,7 @@ struct NUAxis {
 };
 
 __device__ __forceinline__ void nu_load(const AxisArgs& A, NUAxis& st) {
+    MFA_DCHECK(st.s >= 0 && st.s < A.nsp);
     st.lo = __ldg(A.kfx + st.s);
     st.hi = (st.s + 1 < A.nsp) ? __ldg(A.kfx + st.s + 1) : 0x7fffffffffffffffLL;
     st.invh = __ldg(A.invh + st.s);
@@ -523,6 +529,7 @@ __device__ __forceinline__ void bernstein_value(float t, float (&N)[P + 1]) {
 
 struct BezGrid {
     int S0, S1;            // spans along u, v
+    int64_t q_f4;          // size of the block array in float4 (debug bounds checks)
 };
 
 template <int P>
@@ -534,7 +541,9 @@ struct BezBlock {
 
 template <int P>
 __device__ __forceinline__ const float4* bez_block(const float4* Q, const BezGrid& g, int su, int sv, int sw) {
+    MFA_DCHECK(su >= 0 && su < g.S0 && sv >= 0 && sv < g.S1 && sw >= 0);
     const int64_t b = ((int64_t)sw * g.S1 + sv) * g.S0 + su;
+    MFA_DCHECK((b + 1) * (BezBlock<P>::FLOATS / 4) <= g.q_f4);
     return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Q) + b * BezBlock<P>::FLOATS);
 }
 

@@ -25,6 +25,23 @@
 
 #include "../../include/mfa.h"
 
+// Device bounds checks for debug builds (compute-sanitizer is unavailable on
+// this pool): build with MFA_EXTRA_NVCC_FLAGS=-DMFA_DEBUG_BOUNDS.
+#ifdef MFA_DEBUG_BOUNDS
+#include <cstdio>
+#define MFA_DCHECK(c)                                                            \
+    do {                                                                         \
+        if (!(c)) {                                                              \
+            printf("MFA_DCHECK failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);  \
+            __trap();                                                            \
+        }                                                                        \
+    } while (0)
+#else
+#define MFA_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
+
 namespace mfa {
 
 constexpr int kMaxP = MFA_MAX_DEGREE;
@@ -67,6 +84,7 @@ struct Model {
     int uniform[3] = {0, 0, 0};
     float vmin = 0.f, vmax = 0.f;
     float4* Q = nullptr;           // bricked row quads (kQuads) or Bezier blocks (kBezier)
+    int64_t q_f4 = 0;              // size of Q in float4
     int nb[3] = {0, 0, 0};         // bricks per axis
     unsigned int* queue = nullptr; // kQueueSlots work counters
     AxisTables ax[3];

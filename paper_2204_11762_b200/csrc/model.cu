@@ -516,6 +516,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
             cudaStreamSynchronize(st);
             cudaFree(D);
             m->device_bytes += nblk * bfl * (int64_t)sizeof(float);
+            m->q_f4 = nblk * bfl / 4;
             m->layout = kBezier;
         }
     }
@@ -527,6 +528,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
         relayout_bricks_kernel<<<4736, 256, 0, st>>>(Pdev, m->Q, (int)nu, (int)nv, (int)nw, m->nb[0], m->nb[1], EU, EV,
                                                       EW, qn);
         m->device_bytes += qn * (int64_t)sizeof(float4);
+        m->q_f4 = qn;
         m->layout = kQuads;
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(cuda_fail(e, "layout kernels"));

@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 int i0 = __float_as_int(fm) - 0x4b000000;
                 i0 = min(max(i0, 0), args.tf_n - 2);
                 const float wt = f - (float)i0;
+                MFA_DCHECK(i0 >= 0 && i0 + 1 < args.tf_n);
                 const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
                 float cr = fmaf(wt, T1.x - T0.x, T0.x);
                 float cg = fmaf(wt, T1.y - T0.y, T0.y);
@@ -481,6 +482,8 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->Q = m->Q;
     a->g.nbx = m->nb[0];
     a->g.nby = m->nb[1];
+    a->g.q_f4 = m->q_f4;
+    a->bg.q_f4 = m->q_f4;
     a->bg.S0 = (int)(m->n[0] - m->p);
     a->bg.S1 = (int)(m->n[1] - m->p);
     for (int d = 0; d < 3; ++d) a->ax[d] = make_axis_args(m->ax[d]);
