@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--views", type=int, default=None, help="override the number of views (tests only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-eval", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--out-fp16", action="store_true")
     ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier"],
@@ -312,6 +313,28 @@ def run_ours(args):
     except Exception:
         pass
 
+    # ---- secondary: mfa_eval_batch throughput (2^24 random points, rank 0) --
+    ev = None
+    if rank == 0 and not args.no_eval:
+        u, v_, w_ = (torch.from_numpy(x).cuda() for x in WL.query_points(c, 1 << 24))
+        outs = m.eval(u, v_, w_)
+        for _ in range(2):
+            m.eval(u, v_, w_, out=outs)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            m.eval(u, v_, w_, out=outs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / 5
+        pts = (1 << 24) / (ems / 1e3)
+        fe = RL.flops_per_eval_point(p)
+        ev = {"metric": "mfa_eval_batch points/s (value + 3 partials)", "value": pts, "points": 1 << 24,
+              "ms": ems, "flops_per_point": fe, "achieved_tflops": pts * fe / 1e12,
+              "frac_fp32": pts * fe / 1e12 / peak_tf, "hbm_io_bytes_per_point": 28,
+              "hbm_io_gbps": pts * 28 / 1e9}
+        del u, v_, w_, outs
+
     # ---- end to end through the C ABI with host buffers --------------------
     e2e = None
     if not args.no_e2e:
@@ -341,6 +364,7 @@ def run_ours(args):
             "frames_per_s": V * args.steps / (ms_max / 1e3),
             "samples_per_step": samples_all / args.steps,
             "roofline": roof,
+            "eval": ev,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,

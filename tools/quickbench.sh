@@ -1,7 +1,7 @@
 #!/bin/bash
 # quick perf sweep: device-timed render throughput for C3, C4, C5 (no e2e / cpu baseline)
 for c in ${@:-c3 c4 c5}; do
-  timeout 600 python bench.py --workload $c --steps 3 --warmup 2 --no-cpu-baseline --no-e2e $QB_ARGS > gpurun_out/qb_$c.json 2> gpurun_out/qb_$c.err
+  timeout 600 python bench.py --workload $c --steps 3 --warmup 2 --no-cpu-baseline --no-e2e --no-eval $QB_ARGS > gpurun_out/qb_$c.json 2> gpurun_out/qb_$c.err
   python - "$c" <<'PY'
 import json,sys
 c=sys.argv[1]
