@@ -258,164 +258,186 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         bool live = K > 0;
         float nb[CACHE ? P + 1 : 1][P + 1][P + 1];   // cached neighbourhood (CACHE)
         int64_t nb_key = -1;
+
+        // a4: span + local coordinate per axis of the sample at F
+        auto locate = [&](int (&s)[3], float (&t)[3], float (&gs)[3]) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (UNI) {
+                    uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
+                    gs[i] = args.gsc[i];
+                } else {
+                    t[i] = nu_span(args.ax[i], F[i], nu[i]);
+                    s[i] = nu[i].s;
+                    gs[i] = nu[i].invh * args.gsc[i];
+                }
+            }
+        };
+        // a6: make the neighbourhood of span triple s resident (CACHE layouts)
+        auto fetch = [&](const int (&s)[3]) {
+            if constexpr (BEZ && CACHE) {
+                const int64_t e = ((int64_t)s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
+                if (e != nb_key) {       // reload only when the span triple changed
+                    load_bblock<P>(bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]), nb);
+                    nb_key = e;
+                }
+            } else if constexpr (CACHE) {
+                const int64_t e = brick_entry<P>(args.g, s[0], s[1], s[2]);
+                if (e != nb_key) {
+                    load_block<P>(args.Q + e, nb);
+                    nb_key = e;
+                }
+            }
+        };
+        // a5 + a7: value and t-space gradient of the sample (after fetch)
+        auto query = [&](const int (&s)[3], const float (&t)[3], float& val, float& gu, float& gv, float& gw) {
+            gu = gv = gw = 0.f;
+            if constexpr (BEZ && !CACHE) {   // stream the block slab by slab
+                const float4* q = bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]);
+                float r0[P + 1][P + 1];
+                load_bslab<P>(q, r0);
+                if (SHADE) {
+                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                    bernstein<P, false>(t[0], Bu);
+                    bernstein<P, true>(t[1], Bv);
+                    bernstein<P, false>(t[2], Bw);
+                    contract_vg_bez<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
+                } else {
+                    float nbv[P + 1][P + 1][P + 1];
+                    load_bblock<P>(q, nbv);
+                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                    bernstein_value<P>(t[0], Nu);
+                    bernstein_value<P>(t[1], Nv);
+                    bernstein_value<P>(t[2], Nw);
+                    val = contract_v_cached<P>(nbv, Nu, Nv, Nw);
+                }
+            } else if constexpr (BEZ) {
+                if (SHADE) {  // Bernstein basis, the same polynomials on every span
+                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                    bernstein<P, false>(t[0], Bu);
+                    bernstein<P, true>(t[1], Bv);
+                    bernstein<P, false>(t[2], Bw);
+                    contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                } else {
+                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                    bernstein_value<P>(t[0], Nu);
+                    bernstein_value<P>(t[1], Nv);
+                    bernstein_value<P>(t[2], Nw);
+                    val = contract_v_cached<P>(nb, Nu, Nv, Nw);
+                }
+            } else if constexpr (CACHE) {
+                if (SHADE) {
+                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                    axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
+                    axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
+                    axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
+                    contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                } else {
+                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                    axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+                    axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+                    axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+                    val = contract_v_cached<P>(nb, Nu, Nv, Nw);
+                }
+            } else {
+                const float4* q = args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
+                // issue slab 0 before the basis math; slabs stream through a double buffer
+                float r0[P + 1][P + 1];
+                load_slab<P>(q, r0);
+                if (SHADE) {  // a5 + a7 with derivatives (Alg.1 l.6 and l.9)
+                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                    axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
+                    axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
+                    axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
+                    contract_vg<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
+                } else {      // value only (Alg.1 l.8 ShadingOn == false)
+                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                    axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+                    axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+                    axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+                    val = contract_v<P>(q, r0, Nu, Nv, Nw);
+                }
+            }
+        };
+        // a8-a10 for one queried sample, branch-free (so it can interleave
+        // with the next sample's query)
+        auto shade_composite = [&](float val, float gu, float gv, float gw, const float (&gs)[3]) {
+            // a8: transfer function (l.7)
+            float f = (val - args.v_lo) * args.s_scale;
+            f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
+            // i0 = round(f - 1/2) via the 2^23 magic number (no F2I): any
+            // i0 in {floor(f), f - 1 at integers} gives the same lerp
+            const float fm = f + 8388607.5f;
+            int i0 = __float_as_int(fm) - 0x4b000000;
+            i0 = min(max(i0, 0), args.tf_n - 2);
+            const float wt = f - (float)i0;
+            MFA_DCHECK(i0 >= 0 && i0 + 1 < args.tf_n);
+            const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
+            float cr = fmaf(wt, T1.x - T0.x, T0.x);
+            float cg = fmaf(wt, T1.y - T0.y, T0.y);
+            float cb = fmaf(wt, T1.z - T0.z, T0.z);
+            const float a = fmaf(wt, T1.w - T0.w, T0.w);
+            // a9: Phong with a headlight (l.10-11; R-11); zero gradient -> ambient
+            if (SHADE) {
+                const float gx = gu * gs[0], gy = gv * gs[1], gz = gw * gs[2];
+                const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
+                const bool zero = n2 <= args.eps2;
+                const float ndl = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * rsqrtf(fmaxf(n2, 1e-37f));
+                const float dif = fmaxf(ndl, 0.f);
+                const float rv = fmaxf(fmaf(2.f * ndl, ndl, -1.f), 0.f);
+                float spe = exp2f(args.shin * __log2f(rv));          // rv = 0 -> 0 (shin > 0)
+                if (args.shin == 0.f) spe = 1.f;                       // 0^0 = 1, as pow()
+                spe = ndl > 0.f ? spe : 0.f;
+                const float lit = zero ? args.ka : fmaf(args.kd, dif, args.ka);
+                const float add = zero ? 0.f : args.ks * spe;
+                cr = __saturatef(fmaf(cr, lit, add));
+                cg = __saturatef(fmaf(cg, lit, add));
+                cb = __saturatef(fmaf(cb, lit, add));
+            }
+            // a10: front-to-back compositing (l.13)
+            const float wgt = (1.f - A) * a;
+            C0 = fmaf(wgt, cr, C0);
+            C1 = fmaf(wgt, cg, C1);
+            C2 = fmaf(wgt, cb, C2);
+            A += wgt;
+        };
+
+        // two-stage pipeline: iteration k queries sample k+1 while it shades
+        // and composites sample k; the ERT test (l.14-15; R-13) follows.
+        float val = 0.f, gu = 0.f, gv = 0.f, gw = 0.f, gs[3] = {0.f, 0.f, 0.f};
+        if (live) {
+            int s[3];
+            float t[3];
+            locate(s, t, gs);
+            fetch(s);
+            query(s, t, val, gu, gv, gw);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) F[i] += DF[i];
+        }
         while (__any_sync(0xffffffffu, live)) {
             if (live) {
-                // a4: span + local coordinate per axis
-                int s[3];
-                float t[3], gs[3];
+                if (k + 1 < K) {
+                    int s[3];
+                    float t[3], gs1[3];
+                    locate(s, t, gs1);
+                    fetch(s);
+                    float val1, gu1, gv1, gw1;
+                    shade_composite(val, gu, gv, gw, gs);
+                    query(s, t, val1, gu1, gv1, gw1);
+                    val = val1;
+                    gu = gu1;
+                    gv = gv1;
+                    gw = gw1;
 #pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    if (UNI) {
-                        uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
-                        gs[i] = args.gsc[i];
-                    } else {
-                        t[i] = nu_span(args.ax[i], F[i], nu[i]);
-                        s[i] = nu[i].s;
-                        gs[i] = nu[i].invh * args.gsc[i];
-                    }
-                }
-                // a6: neighbourhood of the span triple
-                float val, gu = 0.f, gv = 0.f, gw = 0.f;
-                if constexpr (BEZ && !CACHE) {   // stream the block slab by slab
-                    const float4* q = bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]);
-                    float r0[P + 1][P + 1];
-                    load_bslab<P>(q, r0);
-                    if (SHADE) {
-                        float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
-                        bernstein<P, false>(t[0], Bu);
-                        bernstein<P, true>(t[1], Bv);
-                        bernstein<P, false>(t[2], Bw);
-                        contract_vg_bez<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
-                    } else {
-                        float nbv[P + 1][P + 1][P + 1];
-                        load_bblock<P>(q, nbv);
-                        float Nu[P + 1], Nv[P + 1], Nw[P + 1];
-                        bernstein_value<P>(t[0], Nu);
-                        bernstein_value<P>(t[1], Nv);
-                        bernstein_value<P>(t[2], Nw);
-                        val = contract_v_cached<P>(nbv, Nu, Nv, Nw);
-                    }
-                } else if constexpr (BEZ) {
-                    const int64_t e = ((int64_t)s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
-                    if (e != nb_key) {       // reload only when the span triple changed
-                        load_bblock<P>(bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]), nb);
-                        nb_key = e;
-                    }
-                    if (SHADE) {  // a5: Bernstein basis, the same polynomials on every span
-                        float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
-                        bernstein<P, false>(t[0], Bu);
-                        bernstein<P, true>(t[1], Bv);
-                        bernstein<P, false>(t[2], Bw);
-                        contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
-                    } else {
-                        float Nu[P + 1], Nv[P + 1], Nw[P + 1];
-                        bernstein_value<P>(t[0], Nu);
-                        bernstein_value<P>(t[1], Nv);
-                        bernstein_value<P>(t[2], Nw);
-                        val = contract_v_cached<P>(nb, Nu, Nv, Nw);
-                    }
-                } else if constexpr (CACHE) {
-                    const int64_t e = brick_entry<P>(args.g, s[0], s[1], s[2]);
-                    if (e != nb_key) {       // reload only when the span triple changed
-                        load_block<P>(args.Q + e, nb);
-                        nb_key = e;
-                    }
-                    if (SHADE) {
-                        float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
-                        axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
-                        axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
-                        axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
-                        contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
-                    } else {
-                        float Nu[P + 1], Nv[P + 1], Nw[P + 1];
-                        axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
-                        axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
-                        axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
-                        val = contract_v_cached<P>(nb, Nu, Nv, Nw);
+                    for (int i = 0; i < 3; ++i) {
+                        gs[i] = gs1[i];
+                        F[i] += DF[i];
                     }
                 } else {
-                    const float4* q = args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
-                    // issue slab 0 before the basis math; slabs stream through a double buffer
-                    float r0[P + 1][P + 1];
-                    load_slab<P>(q, r0);
-                    if (SHADE) {  // a5 + a7 with derivatives (Alg.1 l.6 and l.9)
-                        float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
-                        axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
-                        axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
-                        axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
-                        contract_vg<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
-                    } else {      // value only (Alg.1 l.8 ShadingOn == false)
-                        float Nu[P + 1], Nv[P + 1], Nw[P + 1];
-                        axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
-                        axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
-                        axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
-                        val = contract_v<P>(q, r0, Nu, Nv, Nw);
-                    }
+                    shade_composite(val, gu, gv, gw, gs);
                 }
-                // a8: transfer function (l.7)
-                float f = (val - args.v_lo) * args.s_scale;
-                f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
-                // i0 = round(f - 1/2) via the 2^23 magic number (no F2I): any
-                // i0 in {floor(f), f - 1 at integers} gives the same lerp
-                const float fm = f + 8388607.5f;
-                int i0 = __float_as_int(fm) - 0x4b000000;
-                i0 = min(max(i0, 0), args.tf_n - 2);
-                const float wt = f - (float)i0;
-                MFA_DCHECK(i0 >= 0 && i0 + 1 < args.tf_n);
-                const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
-                float cr = fmaf(wt, T1.x - T0.x, T0.x);
-                float cg = fmaf(wt, T1.y - T0.y, T0.y);
-                float cb = fmaf(wt, T1.z - T0.z, T0.z);
-                const float a = fmaf(wt, T1.w - T0.w, T0.w);
-                // a9: Phong with a headlight (l.10-11; R-11)
-                if (SHADE) {
-                    const float gx = gu * gs[0], gy = gv * gs[1], gz = gw * gs[2];
-                    const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
-                    if (n2 <= args.eps2) {
-                        cr *= args.ka;
-                        cg *= args.ka;
-                        cb *= args.ka;
-                    } else {
-                        const float ndl = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * rsqrtf(n2);
-                        const float dif = fmaxf(ndl, 0.f);
-                        const float rv = fmaxf(fmaf(2.f * ndl, ndl, -1.f), 0.f);
-                        float spe = 0.f;
-                        if (ndl > 0.f) spe = rv > 0.f ? exp2f(args.shin * __log2f(rv)) : (args.shin == 0.f ? 1.f : 0.f);
-                        const float lit = fmaf(args.kd, dif, args.ka);
-                        const float add = args.ks * spe;
-                        cr = __saturatef(fmaf(cr, lit, add));
-                        cg = __saturatef(fmaf(cg, lit, add));
-                        cb = __saturatef(fmaf(cb, lit, add));
-                    }
-                }
-                // a10: front-to-back compositing + ERT (l.13-15; R-13)
-                const float wgt = (1.f - A) * a;
-                C0 = fmaf(wgt, cr, C0);
-                C1 = fmaf(wgt, cg, C1);
-                C2 = fmaf(wgt, cb, C2);
-                A += wgt;
                 ++k;
-#pragma unroll
-                for (int i = 0; i < 3; ++i) F[i] += DF[i];
                 live = !(A > args.o_max) && k < K;
-                if constexpr (BEZ && CACHE && MFA_RENDER_PREFETCH > 0) {
-                    // Hint the block MFA_RENDER_PREFETCH samples ahead into
-                    // L2 (MFA_PREFETCH_L1: into L1).  The span guess uses only
-                    // registers (cached bounds): s, or s +- 1 when the look-ahead
-                    // coordinate leaves them -- no dependent loads.
-                    if (live) {
-                        int sn[3];
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) {
-                            const long long Fa = F[i] + (long long)(MFA_RENDER_PREFETCH - 1) * DF[i];
-                            if constexpr (UNI) sn[i] = uni_span_only(Fa, args.ax[i].nsp);
-                            else sn[i] = nu_span_only(nu[i], Fa, args.ax[i].nsp);
-                        }
-                        const int64_t en = ((int64_t)sn[2] * args.bg.S1 + sn[1]) * args.bg.S0 + sn[0];
-                        if (en != nb_key)
-                            prefetch_bblock<P, !MFA_PREFETCH_L1>(bez_block<P>(args.Q, args.bg, sn[0], sn[1], sn[2]));
-                    }
-                }
             }
         }
         // ---- a11: pixel write ---------------------------------------------
