@@ -218,6 +218,65 @@ mfa_status mfa_unpack_tiles(const void* packed, int32_t in_fp16, const int32_t* 
                             int32_t n_views, int32_t width, int32_t height, float* image_out,
                             mfa_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Ground truth and image quality (§4.1.1 and
+ * §4.2.1: "we generate the ground truth volume rendering image by computing
+ * the value and gradient analytically from the synthetic functions for the
+ * samples on rays.  Metrics of image quality include mean squared error
+ * (MSE), peak signal-to-noise ratio (PSNR), and structural similarity index
+ * (SSIM)").
+ * ---------------------------------------------------------------------- */
+#define MFA_FIELD_GAUSSIAN_BEAM 1   /* Eq. 1: prm = {V_min, V_max, mu, sigma, R} */
+#define MFA_FIELD_MARSCHNER_LOBB 2  /* Eq. 2: prm = {f_M, alpha} */
+#define MFA_SRC_MODEL 0
+#define MFA_SRC_ANALYTIC 1
+
+typedef struct {
+    int32_t kind;        /* MFA_FIELD_* ; the function is defined on x, y, z in [-1,1] and
+                            evaluated at x = 2u - 1 of the sample's parameter point u */
+    int32_t value_src;   /* MFA_SRC_MODEL: value from the MFA query; MFA_SRC_ANALYTIC: from the field */
+    int32_t grad_src;    /* the same for the gradient (the paper's gradient-only test takes the
+                            analytic value and the MFA gradient) */
+    double prm[6];
+} mfa_field;
+
+/*
+ * mfa_render_field -- mfa_render with each sample's value and/or gradient
+ * taken from the analytic field (fp64 evaluation) instead of the MFA query.
+ * Rays, sample positions, TF, shading, compositing and ERT are exactly those
+ * of mfa_render, so value_src = grad_src = MFA_SRC_ANALYTIC is the ground-truth
+ * image of the same view, and value_src = ANALYTIC, grad_src = MODEL is the
+ * gradient-accuracy image of P:209.  field == NULL or both sources MODEL is
+ * mfa_render.  Same arguments, layout, ownership and errors as mfa_render;
+ * an unknown field->kind returns MFA_ERR_INVALID_ARG.
+ */
+mfa_status mfa_render_field(mfa_model m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
+                            const mfa_render_params* prm, const mfa_field* field, const mfa_tiles* tiles,
+                            void* rgba_out, unsigned long long* samples_out, mfa_stream stream);
+
+/*
+ * mfa_image_quality -- MSE, PSNR and SSIM of image a against image b.
+ *
+ * img_a, img_b  device fp32 [height][width][4] premultiplied RGBA (mfa_render's
+ *               output); alpha is ignored: the displayed colour is RGB over
+ *               black, quantised to 8-bit levels q = floor(255 clamp(x,0,1) + 1/2).
+ * err_map       optional device fp32 [height][width]: per-pixel Euclidean RGB
+ *               error in 8-bit levels (the Fig. 6 error distribution).
+ * workspace     device scratch of at least mfa_image_quality_workspace(width,
+ *               height) bytes (caller-owned; nothing is allocated here).
+ * out3          device fp64[3]: {MSE over pixels x 3 channels, PSNR = 10
+ *               log10(255^2/MSE) (+inf if MSE == 0), mean SSIM}.  SSIM: luma
+ *               0.299 R + 0.587 G + 0.114 B, 11x11 Gaussian window sigma 1.5,
+ *               C1 = (0.01*255)^2, C2 = (0.03*255)^2, every window position
+ *               inside the image (readings R-22, after SPEC S:469-516).
+ * fp64 throughout; deterministic (fixed reduction order).  Async on stream.
+ * width or height < 11: MFA_ERR_INVALID_ARG (and the workspace size is 0).
+ */
+size_t mfa_image_quality_workspace(int32_t width, int32_t height);
+mfa_status mfa_image_quality(int32_t width, int32_t height, const float* img_a, const float* img_b,
+                             float* err_map, void* workspace, size_t workspace_bytes, double* out3,
+                             mfa_stream stream);
+
 /* Thread-local message for the last non-OK status on this thread ("" if none). */
 const char* mfa_last_error(void);
 

@@ -46,6 +46,11 @@ class OrcTF(C.Structure):
                 ("v_lo", C.c_double), ("v_hi", C.c_double)]
 
 
+class OrcField(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("value_src", C.c_int32), ("grad_src", C.c_int32),
+                ("prm", C.c_double * 6)]
+
+
 class OrcParams(C.Structure):
     _fields_ = [("box_min", C.c_double * 3), ("box_max", C.c_double * 3), ("step", C.c_double),
                 ("o_max", C.c_double), ("shading", C.c_int32), ("ka", C.c_double),
@@ -75,6 +80,17 @@ def lib():
         _lib.orc_ray.argtypes = [C.POINTER(OrcCamera), C.c_int32, C.c_int32, dp, dp]
         _lib.orc_clip.restype = C.c_int
         _lib.orc_clip.argtypes = [dp, dp, dp, dp, dp, dp]
+        _lib.orc_basis_ders2.restype = None
+        _lib.orc_basis_ders2.argtypes = [C.c_int32, dp, C.c_int64, C.c_double, dp, dp, dp]
+        _lib.orc_eval_hessian.restype = C.c_int
+        _lib.orc_eval_hessian.argtypes = [C.POINTER(OrcModel), C.c_double, C.c_double, C.c_double, dp, dp]
+        _lib.orc_field_eval.restype = C.c_int
+        _lib.orc_field_eval.argtypes = [C.POINTER(OrcField), C.c_double, C.c_double, C.c_double, dp]
+        _lib.orc_render_ex.restype = C.c_int
+        _lib.orc_render_ex.argtypes = [C.POINTER(OrcModel), C.POINTER(OrcCamera), C.POINTER(OrcTF),
+                                       C.POINTER(OrcParams), C.POINTER(OrcField), C.c_int64,
+                                       C.POINTER(C.c_int64), dp, C.POINTER(C.c_int64), C.POINTER(C.c_uint8),
+                                       dp, C.POINTER(C.c_int64), C.c_int32]
         _lib.orc_render.restype = C.c_int
         _lib.orc_render.argtypes = [C.POINTER(OrcModel), C.POINTER(OrcCamera), C.POINTER(OrcTF),
                                     C.POINTER(OrcParams), C.c_int64, C.POINTER(C.c_int64), dp,
@@ -111,6 +127,14 @@ def basis_derivs(p: int, knots, span: int, u: float):
     return N, dN
 
 
+def basis_ders2(p: int, knots, span: int, u: float):
+    """H1: (N, N', N'') of the p+1 non-zero basis functions on span."""
+    U = np.ascontiguousarray(knots, dtype=np.float64)
+    N, dN, d2N = np.zeros(p + 1), np.zeros(p + 1), np.zeros(p + 1)
+    lib().orc_basis_ders2(p, _dp(U), span, float(u), _dp(N), _dp(dN), _dp(d2N))
+    return N, dN, d2N
+
+
 class Model:
     """Oracle view of a model: degrees, fp64 knots, fp32 grid [n_w][n_v][n_u]."""
 
@@ -142,6 +166,20 @@ class Model:
         sig = np.zeros(4)
         rc = lib().orc_eval(C.byref(self.s), float(u), float(v), float(w), _dp(out), _dp(sig))
         return out, sig, rc
+
+    def eval_hessian(self, u, v, w):
+        """H2: (out[10], sigma[10], rc): v, v_u, v_v, v_w, v_uu, v_vv, v_ww, v_uv, v_uw, v_vw."""
+        out = np.zeros(10)
+        sig = np.zeros(10)
+        rc = lib().orc_eval_hessian(C.byref(self.s), float(u), float(v), float(w), _dp(out), _dp(sig))
+        return out, sig, rc
+
+    def eval_hessian_batch(self, u, v, w):
+        n = len(u)
+        out, sig = np.zeros((n, 10)), np.zeros((n, 10))
+        for i in range(n):
+            out[i], sig[i], _ = self.eval_hessian(float(u[i]), float(v[i]), float(w[i]))
+        return out, sig
 
     def eval_batch(self, u, v, w, nthreads=None):
         u = np.ascontiguousarray(u, dtype=np.float32)
@@ -188,9 +226,31 @@ def clip(bmin, bmax, o, d):
     return bool(hit), float(ti[0]), float(to[0])
 
 
+def make_field(field) -> OrcField:
+    """field: workloads.AnalyticField (kind, value_src, grad_src, prm)."""
+    f = OrcField()
+    f.kind = int(field.kind)
+    f.value_src = int(field.value_src)
+    f.grad_src = int(field.grad_src)
+    for i, x in enumerate(field.prm):
+        f.prm[i] = float(x)
+    return f
+
+
+def field_eval(field, u, v, w):
+    """G1: analytic value and parameter-space gradient at (u, v, w)."""
+    out = np.zeros(4)
+    f = make_field(field)
+    rc = lib().orc_field_eval(C.byref(f), float(u), float(v), float(w), _dp(out))
+    assert rc == 0
+    return out
+
+
 def render(model: Model, cam, tf, v_lo, v_hi, params, pixels=None, nthreads=None,
-           ert_window=1e-4, exit_window=1e-6, sens_weight=1e-3, sens_grad=None):
-    """Render one view (all pixels, or a flat pixel-index list).
+           ert_window=1e-4, exit_window=1e-6, sens_weight=1e-3, sens_grad=None, field=None):
+    """Render one view (all pixels, or a flat pixel-index list).  field (a
+    workloads.AnalyticField) takes the value and/or gradient of each sample
+    from the analytic function instead of the MFA (ground truth).
 
     Returns dict(rgba (n,4) fp64, count (n,), flags (n,), alt (n,2,4), alt_count (n,2))."""
     tf = np.ascontiguousarray(tf, dtype=np.float32)
@@ -221,7 +281,8 @@ def render(model: Model, cam, tf, v_lo, v_hi, params, pixels=None, nthreads=None
     flags = np.zeros(n, dtype=np.uint8)
     alt = np.zeros((n, 2, 4))
     alt_count = np.zeros((n, 2), dtype=np.int64)
-    lib().orc_render(C.byref(model.s), C.byref(c), C.byref(t), C.byref(p), n, pix_ptr, _dp(rgba),
+    fptr = C.byref(make_field(field)) if field is not None else None
+    lib().orc_render_ex(C.byref(model.s), C.byref(c), C.byref(t), C.byref(p), fptr, n, pix_ptr, _dp(rgba),
                      count.ctypes.data_as(C.POINTER(C.c_int64)),
                      flags.ctypes.data_as(C.POINTER(C.c_uint8)), _dp(alt),
                      alt_count.ctypes.data_as(C.POINTER(C.c_int64)), nthreads or ncores())

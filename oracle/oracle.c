@@ -19,6 +19,17 @@
  *   O6-O13 march         Algorithm 1 lines 3-18
  *   O14 orc_render       rows/pixels split over threads (Alg.1 l.1)
  *   O15 ambiguity flags  DESIGN.md "readings" R-19
+ *   H1 orc_basis_ders2   second derivatives of the basis (Piegl-Tiller eq. 2.9
+ *                        applied twice)              P:78 "Higher-order derivatives,
+ *                        up to the polynomial degree, are also analytically available"
+ *   H2 orc_eval_hessian  value, gradient and the 6 second partials as plain
+ *                        triple sums                 P:78; SURVEY §8(f) NEXT-4
+ *   G1 orc_field_eval    analytic ground truth (Eq. 1 Gaussian beam, Eq. 2
+ *                        Marschner-Lobb) with analytic gradient
+ *   G2 orc_render_ex     Algorithm 1 with value and/or gradient taken from the
+ *                        analytic field ("ground truth volume rendering image by
+ *                        computing the value and gradient analytically ... for the
+ *                        samples on rays"; gradient-only test P:209)
  *
  * Readings where the paper is silent are listed in DESIGN.md §2 (R-1..R-21);
  * the ones used here are cited inline as "R-n".
@@ -68,6 +79,20 @@ typedef struct {
     double sens_weight;        /* R-19 (iii): composited weight above ... */
     double sens_grad;          /*   ... with |g_phys| below this -> shading-sensitive flag */
 } orc_params;
+
+/* G1: analytic field (NEXT-2).  kind 1 = Gaussian beam (Eq. 1),  */
+/* prm = {V_min, V_max, mu, sigma, R}; kind 2 = Marschner-Lobb (Eq. 2,        */
+/* P:169-175), prm = {f_M, alpha}.  value_src / grad_src: 0 = MFA query,      */
+/* 1 = analytic (the paper's value-only, gradient-only and overall tests,     */
+/* P:193).                                                      */
+typedef struct {
+    int32_t kind;
+    int32_t value_src, grad_src;
+    double prm[6];
+} orc_field;
+
+#define ORC_FIELD_GB 1
+#define ORC_FIELD_ML 2
 
 /* ------------------------------------------------------------------------ */
 /* O1: knot span.  i with U[i] <= u < U[i+1]; u == U[n] -> n-1 (SPEC S:45,   */
@@ -126,6 +151,65 @@ void orc_basis_derivs(int32_t p, const double* U, int64_t span, double u, double
 }
 
 /* ------------------------------------------------------------------------ */
+/* H1: N, N' and N'' of the p+1 non-zero basis functions on span `span`.     */
+/* The degree-q functions N_{i,q}(u), q <= p, come from the Cox-de Boor      */
+/* triangle (as in O2); the derivatives from the textbook recursion          */
+/*   N^(k)_{i,q} = q ( N^(k-1)_{i,q-1} / (U_{i+q} - U_i)                     */
+/*                    - N^(k-1)_{i+1,q-1} / (U_{i+q+1} - U_{i+1}) )          */
+/* (Piegl & Tiller eq. 2.9) for k = 1, 2, with 0/0 := 0 at repeated knots.   */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    double ndu[ORC_MAXP + 1][ORC_MAXP + 1];   /* ndu[r][q] = N_{span-q+r, q}(u), r <= q */
+    const double* U;
+    int64_t span;
+} orc_tri;
+
+static double tri_N(const orc_tri* T, int q, int64_t i)
+{
+    if (q < 0) return 0.0;
+    const int64_t r = i - T->span + q;
+    return (r >= 0 && r <= q) ? T->ndu[r][q] : 0.0;
+}
+
+static double tri_div(double a, double den) { return den != 0.0 ? a / den : 0.0; }
+
+static double tri_dN(const orc_tri* T, int k, int q, int64_t i)   /* k-th derivative of N_{i,q} */
+{
+    if (k == 0) return tri_N(T, q, i);
+    if (q == 0) return 0.0;
+    const double* U = T->U;
+    return q * (tri_div(tri_dN(T, k - 1, q - 1, i), U[i + q] - U[i]) -
+                tri_div(tri_dN(T, k - 1, q - 1, i + 1), U[i + q + 1] - U[i + 1]));
+}
+
+void orc_basis_ders2(int32_t p, const double* U, int64_t span, double u, double* N, double* dN, double* d2N)
+{
+    orc_tri T;
+    T.U = U;
+    T.span = span;
+    double left[ORC_MAXP + 1], right[ORC_MAXP + 1], kd[ORC_MAXP + 1][ORC_MAXP + 1];
+    T.ndu[0][0] = 1.0;
+    for (int j = 1; j <= p; ++j) {            /* the triangle of O2, values only */
+        left[j] = u - U[span + 1 - j];
+        right[j] = U[span + j] - u;
+        double saved = 0.0;
+        for (int r = 0; r < j; ++r) {
+            kd[j][r] = right[r + 1] + left[j - r];
+            double temp = T.ndu[r][j - 1] / kd[j][r];
+            T.ndu[r][j] = saved + right[r + 1] * temp;
+            saved = left[j - r] * temp;
+        }
+        T.ndu[j][j] = saved;
+    }
+    for (int r = 0; r <= p; ++r) {
+        const int64_t i = span - p + r;
+        N[r] = tri_N(&T, p, i);
+        dN[r] = tri_dN(&T, 1, p, i);
+        d2N[r] = tri_dN(&T, 2, p, i);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* O3: value and parameter-space gradient as the plain triple sum over the   */
 /* active (p+1)^3 block (SPEC S:72 value, S:81 gradient "substituting        */
 /* basis_derivs along one axis at a time"; P:100 all three derivatives).     */
@@ -168,10 +252,92 @@ int orc_eval(const orc_model* m, double u, double v, double w, double out[4], do
 }
 
 /* ------------------------------------------------------------------------ */
-/* O4: ray through the centre of pixel (px, py), row 0 at the top (P:100     */
-/* "ray cast for each pixel of the viewport according to the relative        */
-/* location of the camera and the viewport"; camera reading R-14).           */
+/* H2: value, gradient and Hessian (parameter space) as plain triple sums:   */
+/* out = {v, v_u, v_v, v_w, v_uu, v_vv, v_ww, v_uv, v_uw, v_vw}; each term   */
+/* is the product of one basis factor per axis with the derivative orders    */
+/* of that component.  sigma[k] = sum |term| (tolerance scale, R-5).         */
 /* ------------------------------------------------------------------------ */
+int orc_eval_hessian(const orc_model* m, double u, double v, double w, double out[10], double sigma[10])
+{
+    static const int ord[10][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {2, 0, 0},
+                                   {0, 2, 0}, {0, 0, 2}, {1, 1, 0}, {1, 0, 1}, {0, 1, 1}};
+    const double q[3] = {u, v, w};
+    double B[3][3][ORC_MAXP + 1];   /* B[axis][order][r] */
+    int64_t span[3];
+    for (int d = 0; d < 3; ++d) {
+        span[d] = orc_find_span(m->degree[d], m->nctrl[d], m->knots[d], q[d]);
+        if (span[d] < 0) {
+            for (int k = 0; k < 10; ++k) { out[k] = NAN; if (sigma) sigma[k] = NAN; }
+            return -1;
+        }
+        orc_basis_ders2(m->degree[d], m->knots[d], span[d], q[d], B[d][0], B[d][1], B[d][2]);
+    }
+    const int64_t nu = m->nctrl[0], nv = m->nctrl[1];
+    const int pu = m->degree[0], pv = m->degree[1], pw = m->degree[2];
+    double s[10] = {0}, a[10] = {0};
+    for (int c = 0; c <= pw; ++c)
+        for (int b = 0; b <= pv; ++b)
+            for (int aa = 0; aa <= pu; ++aa) {
+                const int64_t i = span[0] - pu + aa, j = span[1] - pv + b, k = span[2] - pw + c;
+                const int64_t idx = (k * nv + j) * nu + i;
+                const double P = m->ctrl64 ? m->ctrl64[idx] : (double)m->ctrl[idx];
+                for (int o = 0; o < 10; ++o) {
+                    const double t = B[0][ord[o][0]][aa] * B[1][ord[o][1]][b] * B[2][ord[o][2]][c] * P;
+                    s[o] += t;
+                    a[o] += fabs(t);
+                }
+            }
+    for (int k = 0; k < 10; ++k) { out[k] = s[k]; if (sigma) sigma[k] = a[k]; }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* G1: value and parameter-space gradient of the analytic field at the       */
+/* parameter point (u,v,w) in [0,1]^3.  The functions are defined on         */
+/* x, y, z in [-1, 1] ("The volume range of x, y, and z is [-1, 1]"),  */
+/* so x = 2u - 1 and d/du = 2 d/dx (R-15, R-4).                               */
+/* ------------------------------------------------------------------------ */
+int orc_field_eval(const orc_field* f, double u, double v, double w, double out[4])
+{
+    const double x = 2.0 * u - 1.0, y = 2.0 * v - 1.0, z = 2.0 * w - 1.0;
+    double F, gx, gy, gz;
+    if (f->kind == ORC_FIELD_GB) {
+        /* Eq. 1: F = V_min + (V_max - V_min) G(r / R), G(l) = exp(-(l - mu)^2 / (2 sigma^2)) */
+        const double vmin = f->prm[0], vmax = f->prm[1], mu = f->prm[2], sg = f->prm[3], R = f->prm[4];
+        const double r = sqrt(x * x + y * y + z * z);
+        const double l = r / R;
+        const double G = exp(-(l - mu) * (l - mu) / (2.0 * sg * sg));
+        F = vmin + (vmax - vmin) * G;
+        /* dF/dx_i = (V_max - V_min) G'(l) (1/R) x_i / r, G'(l) = -(l - mu)/sigma^2 G(l); 0 at r = 0 */
+        const double c = r > 0.0 ? (vmax - vmin) * (-(l - mu) / (sg * sg)) * G / (R * r) : 0.0;
+        gx = c * x;
+        gy = c * y;
+        gz = c * z;
+    } else if (f->kind == ORC_FIELD_ML) {
+        /* Eq. 2: F = (1 - sin(pi z / 2) + alpha (1 + rho(r))) / (2 (1 + alpha)),
+           rho(r) = cos(2 pi f_M cos(pi r / 2)), r = sqrt(x^2 + y^2) */
+        const double fm = f->prm[0], al = f->prm[1];
+        const double PI = 3.14159265358979323846;
+        const double r = sqrt(x * x + y * y);
+        const double rho = cos(2.0 * PI * fm * cos(PI * r / 2.0));
+        const double den = 2.0 * (1.0 + al);
+        F = (1.0 - sin(PI * z / 2.0) + al * (1.0 + rho)) / den;
+        /* rho'(r) = sin(2 pi f_M cos(pi r/2)) * 2 pi f_M * sin(pi r/2) * pi/2 */
+        const double drho = sin(2.0 * PI * fm * cos(PI * r / 2.0)) * 2.0 * PI * fm * sin(PI * r / 2.0) * (PI / 2.0);
+        const double c = r > 0.0 ? al * drho / (r * den) : 0.0;
+        gx = c * x;
+        gy = c * y;
+        gz = -(PI / 2.0) * cos(PI * z / 2.0) / den;
+    } else {
+        return -1;
+    }
+    out[0] = F;
+    out[1] = 2.0 * gx;
+    out[2] = 2.0 * gy;
+    out[3] = 2.0 * gz;
+    return 0;
+}
+
 static void v_sub(const double* a, const double* b, double* r) { for (int i = 0; i < 3; ++i) r[i] = a[i] - b[i]; }
 static void v_cross(const double* a, const double* b, double* r)
 {
@@ -182,6 +348,11 @@ static void v_cross(const double* a, const double* b, double* r)
 static double v_dot(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
 static void v_norm(double* a) { double l = sqrt(v_dot(a, a)); for (int i = 0; i < 3; ++i) a[i] /= l; }
 
+/* ------------------------------------------------------------------------ */
+/* O4: ray through the centre of pixel (px, py), row 0 at the top (P:100     */
+/* "ray cast for each pixel of the viewport according to the relative        */
+/* location of the camera and the viewport"; camera reading R-14).           */
+/* ------------------------------------------------------------------------ */
 void orc_ray(const orc_camera* cam, int32_t px, int32_t py, double o[3], double d[3])
 {
     double f[3], r[3], up[3];
@@ -263,6 +434,7 @@ typedef struct {
     const orc_tf* tf;
     const orc_params* prm;
     double L[3];
+    const orc_field* fld;   /* NULL: every value and gradient from the MFA query */
 } orc_ctx;
 
 /* Result of marching one ray. */
@@ -293,7 +465,15 @@ static void march(const orc_ctx* cx, const double o[3], const double d[3], doubl
             q[i] = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u);
         }
         double vg[4];
-        orc_eval(cx->m, q[0], q[1], q[2], vg, NULL);       /* l.6 queryValueMFA (+ l.9 gradient) */
+        const orc_field* fl = cx->fld;
+        if (!(fl && fl->value_src && fl->grad_src))
+            orc_eval(cx->m, q[0], q[1], q[2], vg, NULL);   /* l.6 queryValueMFA (+ l.9 gradient) */
+        if (fl && (fl->value_src || fl->grad_src)) {        /* G2: analytic ground truth */
+            double a[4];
+            orc_field_eval(fl, q[0], q[1], q[2], a);
+            if (fl->value_src) vg[0] = a[0];
+            if (fl->grad_src) { vg[1] = a[1]; vg[2] = a[2]; vg[3] = a[3]; }
+        }
         double col[4];
         apply_tf(cx->tf, vg[0], col);                        /* l.7 applyTFs */
         double c[3] = {col[0], col[1], col[2]};
@@ -408,11 +588,11 @@ static void* render_worker(void* arg)
     return NULL;
 }
 
-int orc_render(const orc_model* m, const orc_camera* cam, const orc_tf* tf, const orc_params* prm,
-               int64_t npix, const int64_t* pix, double* rgba, int64_t* count, uint8_t* flags,
-               double* alt, int64_t* alt_count, int32_t nthreads)
+int orc_render_ex(const orc_model* m, const orc_camera* cam, const orc_tf* tf, const orc_params* prm,
+                  const orc_field* fld, int64_t npix, const int64_t* pix, double* rgba, int64_t* count,
+                  uint8_t* flags, double* alt, int64_t* alt_count, int32_t nthreads)
 {
-    orc_ctx cx = {m, tf, prm, {0, 0, 0}};
+    orc_ctx cx = {m, tf, prm, {0, 0, 0}, fld};
     for (int i = 0; i < 3; ++i) cx.L[i] = prm->box_max[i] - prm->box_min[i];
     if (nthreads < 1) nthreads = 1;
     if (npix < nthreads) nthreads = npix > 0 ? (int32_t)npix : 1;
@@ -437,6 +617,13 @@ int orc_render(const orc_model* m, const orc_camera* cam, const orc_tf* tf, cons
     free(jobs);
     free(th);
     return 0;
+}
+
+int orc_render(const orc_model* m, const orc_camera* cam, const orc_tf* tf, const orc_params* prm,
+               int64_t npix, const int64_t* pix, double* rgba, int64_t* count, uint8_t* flags,
+               double* alt, int64_t* alt_count, int32_t nthreads)
+{
+    return orc_render_ex(m, cam, tf, prm, NULL, npix, pix, rgba, count, flags, alt, alt_count, nthreads);
 }
 
 /* Batched point evaluation (fp32 inputs used exactly).  Domain errors give  */

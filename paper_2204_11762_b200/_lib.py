@@ -23,6 +23,7 @@ LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2}
 # C-ABI symbols declared in include/mfa.h (checked by tests/test_abi.py)
 EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
            "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version",
+           "mfa_render_field", "mfa_image_quality", "mfa_image_quality_workspace",
            "mfa_probe_fp32", "mfa_probe_read_bw")
 
 
@@ -59,6 +60,11 @@ class ModelDesc_t(C.Structure):
                 ("device", C.c_int32), ("layout", C.c_int32)]
 
 
+class Field_t(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("value_src", C.c_int32), ("grad_src", C.c_int32),
+                ("prm", C.c_double * 6)]
+
+
 class ModelOptions_t(C.Structure):
     _fields_ = [("layout", C.c_int32)]
 
@@ -90,6 +96,13 @@ def lib():
         L.mfa_render.restype = C.c_int
         L.mfa_render.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
                                  C.POINTER(Tiles_t), vp, vp, vp]
+        L.mfa_render_field.restype = C.c_int
+        L.mfa_render_field.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
+                                       C.POINTER(Field_t), C.POINTER(Tiles_t), vp, vp, vp]
+        L.mfa_image_quality_workspace.restype = C.c_size_t
+        L.mfa_image_quality_workspace.argtypes = [i32, i32]
+        L.mfa_image_quality.restype = C.c_int
+        L.mfa_image_quality.argtypes = [i32, i32, vp, vp, vp, vp, C.c_size_t, vp, vp]
         L.mfa_render_host.restype = C.c_int
         L.mfa_render_host.argtypes = [vp, i32, C.POINTER(Camera_t), vp, i32, C.c_float, C.c_float,
                                       C.POINTER(RenderParams_t), vp, vp, vp]
@@ -134,6 +147,15 @@ def cameras_t(cams):
         arr[i].width = c.width
         arr[i].height = c.height
     return arr
+
+
+def field_t(f):
+    """f: workloads.AnalyticField (kind, value_src, grad_src, prm) -> mfa_field."""
+    r = Field_t()
+    r.kind, r.value_src, r.grad_src = int(f.kind), int(f.value_src), int(f.grad_src)
+    for i, x in enumerate(f.prm):
+        r.prm[i] = float(x)
+    return r
 
 
 def params_t(p, out_fp16=False):
@@ -224,8 +246,11 @@ class Model:
 
     # -- Algorithm 1 (mfa_render) ---------------------------------------------
     def render(self, cams, tf, v_lo, v_hi, params, tiles=None, out=None, samples=None, out_fp16=False,
-               stream=None):
+               stream=None, field=None):
         """cams: list of Camera; tf: CUDA fp32 tensor (n,4); params: RenderParams.
+        field: optional workloads.AnalyticField -- samples take their value
+        and/or gradient from the analytic function (mfa_render_field; the
+        ground-truth image when both come from it).
         Returns the image [V,H,W,4] (or packed tiles [T,16,16,4] if tiles given)."""
         import torch
         tf = tf.contiguous()
@@ -242,9 +267,10 @@ class Model:
             shape = (len(cams), H, W, 4)
         if out is None:
             out = torch.empty(shape, device=tf.device, dtype=dt)
-        _check(lib().mfa_render(self._h, len(cams), ca, C.byref(tft), C.byref(pr),
-                                C.byref(tl) if tl is not None else None, _ptr(out), _ptr(samples),
-                                _stream_ptr(stream)))
+        _check(lib().mfa_render_field(self._h, len(cams), ca, C.byref(tft), C.byref(pr),
+                                      C.byref(field_t(field)) if field is not None else None,
+                                      C.byref(tl) if tl is not None else None, _ptr(out), _ptr(samples),
+                                      _stream_ptr(stream)))
         return out
 
     def render_host(self, cams, tf_host: np.ndarray, v_lo, v_hi, params, out_host, out_fp16=False,
@@ -268,6 +294,28 @@ def unpack_tiles(packed, tiles, n_views, width, height, out=None, stream=None):
     _check(lib().mfa_unpack_tiles(_ptr(packed), int(packed.dtype == torch.float16), _ptr(tiles), tiles.shape[0],
                                   n_views, width, height, _ptr(out), _stream_ptr(stream)))
     return out
+
+
+def image_quality(a, b, err_map=False, workspace=None, stream=None):
+    """MSE / PSNR / SSIM of image a against b (mfa_image_quality): CUDA fp32
+    tensors [H,W,4] (premultiplied RGBA; alpha ignored).  Returns a dict with
+    "mse", "psnr", "ssim" (and "err_map", an [H,W] tensor, if requested)."""
+    import torch
+    assert a.shape == b.shape and a.dim() == 3 and a.shape[2] == 4
+    a, b = a.contiguous().float(), b.contiguous().float()
+    H, W = a.shape[0], a.shape[1]
+    nbytes = int(lib().mfa_image_quality_workspace(W, H))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=a.device)
+    out = torch.empty(3, dtype=torch.float64, device=a.device)
+    em = torch.empty((H, W), dtype=torch.float32, device=a.device) if err_map else None
+    _check(lib().mfa_image_quality(W, H, _ptr(a), _ptr(b), _ptr(em), _ptr(workspace), nbytes, _ptr(out),
+                                   _stream_ptr(stream)))
+    r = out.cpu().tolist()
+    res = {"mse": r[0], "psnr": r[1], "ssim": r[2]}
+    if err_map:
+        res["err_map"] = em
+    return res
 
 
 def version() -> str:

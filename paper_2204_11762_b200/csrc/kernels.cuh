@@ -597,44 +597,4 @@ __device__ __forceinline__ void contract_vg_bez(const float4* __restrict__ q, fl
     gu = gvu.y;
 }
 
-// Prefetch of one Bezier block -- a hint, no registers (L1 for the next
-// sample, L2 for one several samples ahead).
-template <int P, bool L2>
-__device__ __forceinline__ void prefetch_bblock(const float4* q) {
-    constexpr int BYTES = BezBlock<P>::FLOATS * 4;
-#pragma unroll
-    for (int off = 0; off < BYTES; off += 128) {
-        if constexpr (L2)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(q) + off));
-        else
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(q) + off));
-    }
-}
-
-// Span of the next sample on a uniform axis (prefetch prediction only).
-__device__ __forceinline__ int uni_span_only(long long F, int S) {
-    int s = (int)(F >> kUniFracBits);
-    return min(max(s, 0), S - 1);
-}
-
-// Span a few samples ahead on a non-uniform axis (prefetch prediction only):
-// one step past the cached bounds, else the bucket of the coordinate.
-__device__ __forceinline__ int nu_span_ahead(const AxisArgs& A, const NUAxis& st, long long F) {
-    if (F < st.hi && F >= st.lo) return st.s;
-    F = max(F, 0LL);
-    F = min(F, (1LL << kNonUniFracBits) - 1);
-    int b = (int)(F >> A.mshift);
-    b = min(max(b, 0), A.M - 1);
-    return __ldg(A.bucket + b);
-}
-
-// Span of the next sample on a non-uniform axis: one step past the cached
-// bounds at most (prefetch prediction only).
-__device__ __forceinline__ int nu_span_only(const NUAxis& st, long long F, int nsp) {
-    int s = st.s;
-    if (F >= st.hi) s = min(s + 1, nsp - 1);
-    else if (F < st.lo) s = max(s - 1, 0);
-    return s;
-}
-
 }  // namespace mfa

@@ -104,6 +104,6 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
                        unsigned long long* n_err, cudaStream_t st);
 mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                          const mfa_render_params* prm, const mfa_tiles* tiles, void* out,
-                         unsigned long long* samples, cudaStream_t st);
+                         unsigned long long* samples, cudaStream_t st, const mfa_field* fld = nullptr);
 
 }  // namespace mfa

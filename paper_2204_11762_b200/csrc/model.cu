@@ -626,7 +626,18 @@ static mfa_status validate_render(const Model* m, int32_t n_views, const mfa_cam
 extern "C" mfa_status mfa_render(mfa_model h, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                                  const mfa_render_params* prm, const mfa_tiles* tiles, void* rgba_out,
                                  unsigned long long* samples_out, mfa_stream stream) {
+    return mfa_render_field(h, n_views, cams, tf, prm, nullptr, tiles, rgba_out, samples_out, stream);
+}
+
+extern "C" mfa_status mfa_render_field(mfa_model h, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
+                                       const mfa_render_params* prm, const mfa_field* field, const mfa_tiles* tiles,
+                                       void* rgba_out, unsigned long long* samples_out, mfa_stream stream) {
     if (!h) return fail(MFA_ERR_INVALID_ARG, "model is NULL");
+    if (field && (field->value_src || field->grad_src) &&
+        !(field->kind == MFA_FIELD_GAUSSIAN_BEAM || field->kind == MFA_FIELD_MARSCHNER_LOBB))
+        return fail(MFA_ERR_INVALID_ARG, "field: unknown kind");
+    if (field && field->kind == MFA_FIELD_GAUSSIAN_BEAM && !(field->prm[3] > 0.0 && field->prm[4] > 0.0))
+        return fail(MFA_ERR_INVALID_ARG, "field: Gaussian beam needs sigma > 0 and R > 0");
     const Model* m = reinterpret_cast<const Model*>(h);
     mfa_status s = validate_render(m, n_views, cams, prm);
     if (s != MFA_OK) return s;
@@ -636,7 +647,7 @@ extern "C" mfa_status mfa_render(mfa_model h, int32_t n_views, const mfa_camera*
     if (tiles && (tiles->n_tiles < 0 || (tiles->n_tiles > 0 && !tiles->tiles)))
         return fail(MFA_ERR_INVALID_ARG, "tiles: bad n_tiles / tiles pointer");
     if ((s = check_device(m)) != MFA_OK) return s;
-    return launch_render(m, n_views, cams, tf, prm, tiles, rgba_out, samples_out, (cudaStream_t)stream);
+    return launch_render(m, n_views, cams, tf, prm, tiles, rgba_out, samples_out, (cudaStream_t)stream, field);
 }
 
 extern "C" mfa_status mfa_unpack_tiles(const void* packed, int32_t in_fp16, const int32_t* tiles, int64_t n_tiles,

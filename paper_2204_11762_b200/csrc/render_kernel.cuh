@@ -1,0 +1,576 @@
+// render_kernel: Algorithm 1 fused per ray (shared by render.cu and
+// truth.cu, which instantiate it without / with the analytic field).
+//
+//   work = warp units of 8x4 pixels (8 per 16x16 tile) handed out by a global
+//          atomic counter to persistent warps (grid = SMs x resident CTAs), so
+//          early-terminating rays never leave an SM idle and no warp waits on
+//          its CTA's slowest warp; consecutive units are neighbouring tiles.
+//   ray  = one thread.  a1-a2 ray setup in fp64; sample positions are kept in
+//          64-bit fixed point (the "fixed-point ray cast model"):
+//          uniform axes in span units * 2^40, non-uniform axes in parameter
+//          units * 2^62, advanced by an exact integer add per sample.
+//   loop = a3 position -> a4 span/t -> a5 basis -> a6/a7 gather+contract ->
+//          a8 TF (shared-memory table) -> a9 Phong -> a10 composite; the warp
+//          leaves the loop when no lane is live (__any_sync), i.e. early ray
+//          termination per ray with a warp-vote exit.
+//   out  = premultiplied RGBA (fp32 or fp16) to the image or to a packed tile.
+#pragma once
+#include <cuda_fp16.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace mfa {
+
+// NEXT-2 ground truth: the analytic field (Eq. 1-2) a sample takes
+// its value and/or gradient from (see field_eval below).
+struct FieldArgs {
+    int kind;                     // MFA_FIELD_GAUSSIAN_BEAM / MFA_FIELD_MARSCHNER_LOBB
+    int vsrc, gsrc;               // 1: analytic, 0: MFA query
+    double prm[6];
+    double fx_scale[3];           // fixed-point sample coordinate -> parameter u
+    float invL[3];                // parameter-space gradient -> physical (R-4)
+};
+
+struct RenderArgs {
+    const float4* Q;
+    BrickGrid g;
+    BezGrid bg;
+    AxisArgs ax[3];
+    const float4* tf;
+    int tf_n;
+    float v_lo, s_scale;          // f = (v - v_lo) * s_scale = s * (n - 1)
+    double bmin[3], L[3];
+    double step;
+    float gsc[3];                 // gradient scale to physical units (uniform: S/L; non-uniform: 1/L)
+    float o_max, ka, kd, ks, shin, eps2;
+    int W, H, tiles_x, tiles_y;
+    int st_x, st_y;               // supertiles (8x8 tiles) per view, full-frame order
+    int n_views;
+    const int* tiles;             // NULL: full frames
+    int64_t n_tiles;
+    int64_t n_units;              // warp units = 8 per tile
+    int view_base;                // full frames: output view index of cams[0]
+    unsigned int* queue;          // work counter (zeroed before the launch)
+    void* out;
+    int out_fp16;
+    unsigned long long* samples;
+    FieldArgs fld;                // used by the FLD instantiations only
+    mfa_camera cams[kMaxViewsPerLaunch];
+};
+
+struct ViewFrame {
+    double eye[3], f[3], A[3], B[3];
+    int ortho;
+};
+
+__device__ __forceinline__ void compute_frame(const mfa_camera& c, ViewFrame& fr) {
+    double f[3] = {c.look_at[0] - c.eye[0], c.look_at[1] - c.eye[1], c.look_at[2] - c.eye[2]};
+    double lf = sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+    for (int i = 0; i < 3; ++i) f[i] /= lf;
+    double r[3] = {f[1] * c.up[2] - f[2] * c.up[1], f[2] * c.up[0] - f[0] * c.up[2], f[0] * c.up[1] - f[1] * c.up[0]};
+    double lr = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    for (int i = 0; i < 3; ++i) r[i] /= lr;
+    double u[3] = {r[1] * f[2] - r[2] * f[1], r[2] * f[0] - r[0] * f[2], r[0] * f[1] - r[1] * f[0]};
+    const double aspect = (double)c.width / (double)c.height;
+    double sx, sy;
+    if (c.fov_y_deg > 0.0) {
+        const double th = tan(0.5 * c.fov_y_deg * 3.14159265358979323846 / 180.0);
+        sx = aspect * th;
+        sy = th;
+        fr.ortho = 0;
+    } else {
+        sx = aspect * c.ortho_half_height;
+        sy = c.ortho_half_height;
+        fr.ortho = 1;
+    }
+    for (int i = 0; i < 3; ++i) {
+        fr.eye[i] = c.eye[i];
+        fr.f[i] = f[i];
+        fr.A[i] = sx * r[i];
+        fr.B[i] = sy * u[i];
+    }
+}
+
+// Analytic field value and parameter-space gradient at parameter point u
+// (fp64).  x = 2u - 1 on [-1,1]^3, d/du = 2 d/dx.
+//   Gaussian beam (Eq. 1): F = V_min + (V_max - V_min) G(r/R),
+//     G(l) = exp(-(l - mu)^2 / (2 sigma^2)), r = |x|
+//   Marschner-Lobb (Eq. 2): F = (1 - sin(pi z/2) + alpha (1 + rho(r))) / (2 (1 + alpha)),
+//     rho(r) = cos(2 pi f_M cos(pi r/2)), r = sqrt(x^2 + y^2)
+__device__ __forceinline__ void field_eval(const FieldArgs& f, const double (&u)[3], double (&out)[4]) {
+    const double x = 2.0 * u[0] - 1.0, y = 2.0 * u[1] - 1.0, z = 2.0 * u[2] - 1.0;
+    if (f.kind == MFA_FIELD_GAUSSIAN_BEAM) {
+        const double r = sqrt(x * x + y * y + z * z), l = r / f.prm[4], dl = l - f.prm[2];
+        const double G = exp(-dl * dl / (2.0 * f.prm[3] * f.prm[3]));
+        const double A = f.prm[1] - f.prm[0];
+        out[0] = f.prm[0] + A * G;
+        const double c = r > 0.0 ? 2.0 * A * G * (-dl / (f.prm[3] * f.prm[3])) / (f.prm[4] * r) : 0.0;
+        out[1] = c * x;
+        out[2] = c * y;
+        out[3] = c * z;
+    } else {
+        const double fm = f.prm[0], al = f.prm[1], den = 2.0 * (1.0 + al);
+        const double r = sqrt(x * x + y * y);
+        double sr, cr, sz, cz;
+        sincospi(0.5 * r, &sr, &cr);
+        sincospi(0.5 * z, &sz, &cz);
+        double sa, ca;
+        sincospi(2.0 * fm * cr, &sa, &ca);
+        out[0] = (1.0 - sz + al * (1.0 + ca)) / den;
+        const double drho = sa * 2.0 * M_PI * fm * sr * (0.5 * M_PI);
+        const double c = r > 0.0 ? 2.0 * al * drho / (r * den) : 0.0;
+        out[1] = c * x;
+        out[2] = c * y;
+        out[3] = 2.0 * (-(0.5 * M_PI) * cz / den);
+    }
+}
+
+// Launch shape per instantiation (measured on B200):
+//   p <= 3 (neighbourhood cache, ~160-170 registers): 128-thread CTAs, >= 3 per SM
+//   p >= 4 (streamed slabs): 256-thread CTAs capped at 128 registers (2 per SM)
+#ifndef MFA_RENDER_CACHE
+#define MFA_RENDER_CACHE 1
+#endif
+#ifndef MFA_BEZ_CACHE
+#define MFA_BEZ_CACHE 1
+#endif
+#ifndef MFA_CTA_TILES    // -1: per shape (p >= 4), 0: off, 1: on
+#define MFA_CTA_TILES -1
+#endif
+
+template <int P, int LAYOUT>
+struct RenderShape {
+    static constexpr bool BEZ = LAYOUT == kBezier;
+    static constexpr bool CACHE = BEZ ? (bool)MFA_BEZ_CACHE : (MFA_RENDER_CACHE && P <= 3);
+#ifdef MFA_RENDER_THREADS
+    static constexpr int THREADS = MFA_RENDER_THREADS;
+#else
+    static constexpr int THREADS = P <= 3 ? 128 : 256;
+#endif
+#ifdef MFA_RENDER_MINB
+    static constexpr int MINB = MFA_RENDER_MINB;
+#else
+    static constexpr int MINB = P <= 3 ? (CACHE ? 3 : 4) : 2;
+#endif
+    // p >= 4: a CTA (8 warps) takes a whole 16x16 tile so its sub-tiles share L1
+    static constexpr bool CTA_TILES = MFA_CTA_TILES < 0 ? (P >= 4 && THREADS == 256) : (bool)MFA_CTA_TILES;
+};
+
+template <int P, int LAYOUT, bool UNI, bool SHADE, bool FLD>
+__global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P, LAYOUT>::MINB)
+    render_kernel(const __grid_constant__ RenderArgs args) {
+    constexpr bool BEZ = LAYOUT == kBezier;
+    constexpr bool CACHE = RenderShape<P, LAYOUT>::CACHE;
+    extern __shared__ float4 s_tf[];
+    __shared__ ViewFrame s_frame[kMaxViewsPerLaunch];
+
+    for (int v = threadIdx.x; v < args.n_views; v += blockDim.x) compute_frame(args.cams[v], s_frame[v]);
+    for (int i = threadIdx.x; i < args.tf_n; i += blockDim.x) s_tf[i] = __ldg(args.tf + i);
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int per_view = args.st_x * args.st_y * 64;   // units are ordered by 8x8-tile supertiles
+    unsigned long long my_samples = 0;
+
+    constexpr int kWarps = RenderShape<P, LAYOUT>::THREADS / 32;
+    __shared__ unsigned s_tile;
+    unsigned tile_base = 0;
+    int round_sub = 0;
+    for (;;) {
+        unsigned unit = 0;
+        if constexpr (RenderShape<P, LAYOUT>::CTA_TILES) {
+            // ---- the CTA takes a whole 16x16 tile; its warps share its 8
+            // sub-units, so neighbouring rays reuse blocks in this SM's L1
+            if (round_sub == 0) {
+                __syncthreads();
+                if (threadIdx.x == 0) s_tile = atomicAdd(args.queue, 1u);
+                __syncthreads();
+                tile_base = s_tile * 8u;
+            }
+            unit = tile_base + (unsigned)((threadIdx.x >> 5) + round_sub * kWarps);
+            round_sub = (round_sub + 1) % (8 / kWarps);
+            if (tile_base >= args.n_units) break;
+        } else {
+            // ---- next warp unit (8x4 pixels) from the global queue ---------
+            if (lane == 0) unit = atomicAdd(args.queue, 1u);
+            unit = __shfl_sync(0xffffffffu, unit, 0);
+            if (unit >= args.n_units) break;
+        }
+        const int64_t tile_id = unit >> 3;
+        const int sub = unit & 7;
+        int view, tx, ty;
+        if (args.tiles) {
+            view = __ldg(args.tiles + 3 * tile_id);
+            tx = __ldg(args.tiles + 3 * tile_id + 1);
+            ty = __ldg(args.tiles + 3 * tile_id + 2);
+            if (view < 0) continue;  // padding unit (multi-GPU equal-size buffers)
+        } else {
+            // supertile order: the ~200 tiles in flight form a compact image
+            // region, so neighbouring rays reuse control blocks from L1/L2
+            view = (int)(tile_id / per_view);
+            const int t = (int)(tile_id % per_view);
+            const int st = t >> 6, lt = t & 63;
+            tx = (st % args.st_x) * 8 + (lt & 7);
+            ty = (st / args.st_x) * 8 + (lt >> 3);
+            if (tx >= args.tiles_x || ty >= args.tiles_y) continue;
+        }
+        const ViewFrame& fr = s_frame[view];
+        const int lx = (sub & 1) * 8 + (lane & 7);
+        const int ly = (sub >> 1) * 4 + (lane >> 3);
+        const int px = tx * MFA_TILE + lx, py = ty * MFA_TILE + ly;
+        const bool valid = px < args.W && py < args.H;
+
+        // ---- a1: ray through the pixel centre (fp64) -----------------------
+        double o[3], d[3];
+        {
+            const double X = 2.0 * (px + 0.5) / args.W - 1.0;
+            const double Y = 1.0 - 2.0 * (py + 0.5) / args.H;
+            if (fr.ortho) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    o[i] = fr.eye[i] + X * fr.A[i] + Y * fr.B[i];
+                    d[i] = fr.f[i];
+                }
+            } else {
+                double l2 = 0.0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    o[i] = fr.eye[i];
+                    d[i] = fr.f[i] + X * fr.A[i] + Y * fr.B[i];
+                    l2 += d[i] * d[i];
+                }
+                const double il = 1.0 / sqrt(l2);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) d[i] *= il;
+            }
+        }
+        // ---- a2: slab clip; K samples at t_in + (k+1/2) step (R-7) ---------
+        int K = 0;
+        double t_in = 0.0;
+        {
+            double tn = -1e300, tf = 1e300;
+            bool hit = valid;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const double bmax = args.bmin[i] + args.L[i];
+                if (d[i] == 0.0) {
+                    if (o[i] < args.bmin[i] || o[i] > bmax) hit = false;
+                    continue;
+                }
+                const double t0 = (args.bmin[i] - o[i]) / d[i], t1 = (bmax - o[i]) / d[i];
+                tn = fmax(tn, fmin(t0, t1));
+                tf = fmin(tf, fmax(t0, t1));
+            }
+            t_in = fmax(tn, 0.0);
+            if (hit && tf > t_in) {
+                const double frc = (tf - t_in) / args.step - 0.5;
+                K = frc > 0.0 ? (int)ceil(frc) : 0;
+            }
+        }
+        // ---- a3 setup: fixed-point sample coordinates per axis --------------
+        long long F[3], DF[3];
+        NUAxis nu[UNI ? 1 : 3];
+        {
+            const double t0 = t_in + 0.5 * args.step;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const double u0 = (o[i] + t0 * d[i] - args.bmin[i]) / args.L[i];
+                const double du = args.step * d[i] / args.L[i];
+                if (UNI) {
+                    const double S = (double)args.ax[i].nsp;
+                    F[i] = llrint(ldexp(u0 * S, kUniFracBits));
+                    DF[i] = llrint(ldexp(du * S, kUniFracBits));
+                } else {
+                    F[i] = llrint(ldexp(u0, kNonUniFracBits));
+                    DF[i] = llrint(ldexp(du, kNonUniFracBits));
+                    if constexpr (!UNI) {
+                        if (K > 0) nu_init(args.ax[i], F[i], nu[i]);
+                    }
+                }
+            }
+        }
+        const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
+
+        float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+        int k = 0;
+        bool live = K > 0;
+        float nb[CACHE ? P + 1 : 1][P + 1][P + 1];   // cached neighbourhood (CACHE)
+        int64_t nb_key = -1;
+
+        // a4: span + local coordinate per axis of the sample at F
+        auto locate = [&](int (&s)[3], float (&t)[3], float (&gs)[3]) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (UNI) {
+                    uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
+                    gs[i] = args.gsc[i];
+                } else {
+                    t[i] = nu_span(args.ax[i], F[i], nu[i]);
+                    s[i] = nu[i].s;
+                    gs[i] = nu[i].invh * args.gsc[i];
+                }
+            }
+        };
+        // a6: make the neighbourhood of span triple s resident (CACHE layouts)
+        auto fetch = [&](const int (&s)[3]) {
+            if constexpr (BEZ && CACHE) {
+                const int64_t e = ((int64_t)s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
+                if (e != nb_key) {       // reload only when the span triple changed
+                    load_bblock<P>(bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]), nb);
+                    nb_key = e;
+                }
+            } else if constexpr (CACHE) {
+                const int64_t e = brick_entry<P>(args.g, s[0], s[1], s[2]);
+                if (e != nb_key) {
+                    load_block<P>(args.Q + e, nb);
+                    nb_key = e;
+                }
+            }
+        };
+        // a5 + a7: value and t-space gradient of the sample (after fetch)
+        auto query = [&](const int (&s)[3], const float (&t)[3], float& val, float& gu, float& gv, float& gw) {
+            gu = gv = gw = 0.f;
+            if constexpr (BEZ && !CACHE) {   // stream the block slab by slab
+                const float4* q = bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]);
+                float r0[P + 1][P + 1];
+                load_bslab<P>(q, r0);
+                if (SHADE) {
+                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                    bernstein<P, false>(t[0], Bu);
+                    bernstein<P, true>(t[1], Bv);
+                    bernstein<P, false>(t[2], Bw);
+                    contract_vg_bez<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
+                } else {
+                    float nbv[P + 1][P + 1][P + 1];
+                    load_bblock<P>(q, nbv);
+                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                    bernstein_value<P>(t[0], Nu);
+                    bernstein_value<P>(t[1], Nv);
+                    bernstein_value<P>(t[2], Nw);
+                    val = contract_v_cached<P>(nbv, Nu, Nv, Nw);
+                }
+            } else if constexpr (BEZ) {
+                if (SHADE) {  // Bernstein basis, the same polynomials on every span
+                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                    bernstein<P, false>(t[0], Bu);
+                    bernstein<P, true>(t[1], Bv);
+                    bernstein<P, false>(t[2], Bw);
+                    contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                } else {
+                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                    bernstein_value<P>(t[0], Nu);
+                    bernstein_value<P>(t[1], Nv);
+                    bernstein_value<P>(t[2], Nw);
+                    val = contract_v_cached<P>(nb, Nu, Nv, Nw);
+                }
+            } else if constexpr (CACHE) {
+                if (SHADE) {
+                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                    axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
+                    axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
+                    axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
+                    contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                } else {
+                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                    axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+                    axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+                    axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+                    val = contract_v_cached<P>(nb, Nu, Nv, Nw);
+                }
+            } else {
+                const float4* q = args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
+                // issue slab 0 before the basis math; slabs stream through a double buffer
+                float r0[P + 1][P + 1];
+                load_slab<P>(q, r0);
+                if (SHADE) {  // a5 + a7 with derivatives (Alg.1 l.6 and l.9)
+                    float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                    axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
+                    axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
+                    axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
+                    contract_vg<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
+                } else {      // value only (Alg.1 l.8 ShadingOn == false)
+                    float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                    axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+                    axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+                    axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+                    val = contract_v<P>(q, r0, Nu, Nv, Nw);
+                }
+            }
+        };
+        // a8-a10 for one queried sample, branch-free (so it can interleave
+        // with the next sample's query)
+        auto shade_composite = [&](float val, float gu, float gv, float gw, const float (&gs)[3]) {
+            // a8: transfer function (l.7)
+            float f = (val - args.v_lo) * args.s_scale;
+            f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
+            // i0 = round(f - 1/2) via the 2^23 magic number (no F2I): any
+            // i0 in {floor(f), f - 1 at integers} gives the same lerp
+            const float fm = f + 8388607.5f;
+            int i0 = __float_as_int(fm) - 0x4b000000;
+            i0 = min(max(i0, 0), args.tf_n - 2);
+            const float wt = f - (float)i0;
+            MFA_DCHECK(i0 >= 0 && i0 + 1 < args.tf_n);
+            const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
+            float cr = fmaf(wt, T1.x - T0.x, T0.x);
+            float cg = fmaf(wt, T1.y - T0.y, T0.y);
+            float cb = fmaf(wt, T1.z - T0.z, T0.z);
+            const float a = fmaf(wt, T1.w - T0.w, T0.w);
+            // a9: Phong with a headlight (l.10-11; R-11); zero gradient -> ambient
+            if (SHADE) {
+                const float gx = gu * gs[0], gy = gv * gs[1], gz = gw * gs[2];
+                const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
+                const bool zero = n2 <= args.eps2;
+                const float ndl = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * rsqrtf(fmaxf(n2, 1e-37f));
+                const float dif = fmaxf(ndl, 0.f);
+                const float rv = fmaxf(fmaf(2.f * ndl, ndl, -1.f), 0.f);
+                float spe = exp2f(args.shin * __log2f(rv));          // rv = 0 -> 0 (shin > 0)
+                if (args.shin == 0.f) spe = 1.f;                       // 0^0 = 1, as pow()
+                spe = ndl > 0.f ? spe : 0.f;
+                const float lit = zero ? args.ka : fmaf(args.kd, dif, args.ka);
+                const float add = zero ? 0.f : args.ks * spe;
+                cr = __saturatef(fmaf(cr, lit, add));
+                cg = __saturatef(fmaf(cg, lit, add));
+                cb = __saturatef(fmaf(cb, lit, add));
+            }
+            // a10: front-to-back compositing (l.13)
+            const float wgt = (1.f - A) * a;
+            C0 = fmaf(wgt, cr, C0);
+            C1 = fmaf(wgt, cg, C1);
+            C2 = fmaf(wgt, cb, C2);
+            A += wgt;
+        };
+
+        // NEXT-2 (FLD instantiations): the sample takes its value and/or its
+        // gradient from the analytic field at the same parameter point
+        auto sample_field = [&](const int (&s)[3], const float (&t)[3], float& v, float& g0, float& g1, float& g2,
+                                float (&gsx)[3]) {
+            if (!(args.fld.vsrc && args.fld.gsrc)) {
+                fetch(s);
+                query(s, t, v, g0, g1, g2);
+            }
+            double uu[3], fa[4];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) uu[i] = fmin(fmax((double)F[i] * args.fld.fx_scale[i], 0.0), 1.0);
+            field_eval(args.fld, uu, fa);
+            if (args.fld.vsrc) v = (float)fa[0];
+            if (args.fld.gsrc) {
+                g0 = (float)fa[1];
+                g1 = (float)fa[2];
+                g2 = (float)fa[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) gsx[i] = args.fld.invL[i];
+            }
+        };
+
+        // two-stage pipeline: iteration k queries sample k+1 while it shades
+        // and composites sample k; the ERT test (l.14-15; R-13) follows.
+        float val = 0.f, gu = 0.f, gv = 0.f, gw = 0.f, gs[3] = {0.f, 0.f, 0.f};
+        if (live) {
+            int s[3];
+            float t[3];
+            locate(s, t, gs);
+            if constexpr (FLD) {
+                sample_field(s, t, val, gu, gv, gw, gs);
+            } else {
+                fetch(s);
+                query(s, t, val, gu, gv, gw);
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) F[i] += DF[i];
+        }
+        while (__any_sync(0xffffffffu, live)) {
+            if (live) {
+                if (k + 1 < K) {
+                    int s[3];
+                    float t[3], gs1[3];
+                    locate(s, t, gs1);
+                    float val1 = 0.f, gu1 = 0.f, gv1 = 0.f, gw1 = 0.f;
+                    if constexpr (FLD) {
+                        shade_composite(val, gu, gv, gw, gs);
+                        sample_field(s, t, val1, gu1, gv1, gw1, gs1);
+                    } else {
+                        fetch(s);
+                        shade_composite(val, gu, gv, gw, gs);
+                        query(s, t, val1, gu1, gv1, gw1);
+                    }
+                    val = val1;
+                    gu = gu1;
+                    gv = gv1;
+                    gw = gw1;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        gs[i] = gs1[i];
+                        F[i] += DF[i];
+                    }
+                } else {
+                    shade_composite(val, gu, gv, gw, gs);
+                }
+                ++k;
+                live = !(A > args.o_max) && k < K;
+            }
+        }
+        // ---- a11: pixel write ---------------------------------------------
+        if (valid) {
+            int64_t idx;
+            if (args.tiles)
+                idx = tile_id * (MFA_TILE * MFA_TILE) + ly * MFA_TILE + lx;
+            else
+                idx = ((int64_t)(args.view_base + view) * args.H + py) * args.W + px;
+            if (args.out_fp16) {
+                __half2* o2 = reinterpret_cast<__half2*>(args.out) + 2 * idx;
+                o2[0] = __floats2half2_rn(C0, C1);
+                o2[1] = __floats2half2_rn(C2, A);
+            } else {
+                reinterpret_cast<float4*>(args.out)[idx] = make_float4(C0, C1, C2, A);
+            }
+        }
+        my_samples += (unsigned)k;
+    }
+    if (args.samples) {
+        my_samples = __reduce_add_sync(0xffffffffu, (unsigned)my_samples);
+        if (lane == 0 && my_samples) atomicAdd(args.samples, my_samples);
+    }
+}
+
+template <int P, int LAYOUT, bool UNI, bool SHADE, bool FLD>
+static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
+    const size_t smem = sizeof(float4) * a.tf_n;
+    auto kern = render_kernel<P, LAYOUT, UNI, SHADE, FLD>;
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    constexpr int kThreads = RenderShape<P, LAYOUT>::THREADS;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+    if (occ < 1) occ = 1;
+    int64_t grid = (int64_t)sms * occ;
+    const int64_t need = (a.n_units + kThreads / 32 - 1) / (kThreads / 32);
+    if (grid > need) grid = need > 0 ? need : 1;
+    kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int P, int LAYOUT, bool FLD>
+static cudaError_t dispatch_render_l(const RenderArgs& a, bool uni, bool shade, cudaStream_t st) {
+    if (uni)
+        return shade ? launch_render_t<P, LAYOUT, true, true, FLD>(a, st)
+                     : launch_render_t<P, LAYOUT, true, false, FLD>(a, st);
+    return shade ? launch_render_t<P, LAYOUT, false, true, FLD>(a, st)
+                 : launch_render_t<P, LAYOUT, false, false, FLD>(a, st);
+}
+
+template <int P, bool FLD>
+static cudaError_t dispatch_render(const RenderArgs& a, int layout, bool uni, bool shade, cudaStream_t st) {
+    if constexpr (P <= 3) {
+        if (layout == kBezier) return dispatch_render_l<P, kBezier, FLD>(a, uni, shade, st);
+    }
+    return dispatch_render_l<P, kQuads, FLD>(a, uni, shade, st);
+}
+
+// defined in render.cu (MFA query only) and truth.cu (analytic field)
+cudaError_t dispatch_render_main(const RenderArgs& a, int p, int layout, bool uni, bool shade, cudaStream_t st);
+cudaError_t dispatch_render_field(const RenderArgs& a, int p, int layout, bool uni, bool shade, cudaStream_t st);
+
+}  // namespace mfa

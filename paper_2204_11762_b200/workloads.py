@@ -69,6 +69,31 @@ class RenderParams:
     grad_eps: float = 0.0     # |g_phys| <= grad_eps -> ambient only
 
 
+# Analytic ground-truth fields (NEXT-2; Eq. 1-2) as
+# render inputs: which function, its parameters, and which of value /
+# gradient each sample takes from it (0 = MFA query, 1 = analytic).
+FIELD_GAUSSIAN_BEAM = 1
+FIELD_MARSCHNER_LOBB = 2
+GB_PARAMS = (0.0, 255.0, 0.0, 1.0 / 3.0, math.sqrt(3.0))   # V_min, V_max, mu, sigma, R
+ML_PARAMS = (6.0, 0.25)                                      # f_M, alpha
+
+
+@dataclass
+class AnalyticField:
+    kind: int
+    value_src: int = 1
+    grad_src: int = 1
+    prm: tuple = ()
+
+    @staticmethod
+    def marschner_lobb(value_src=1, grad_src=1):
+        return AnalyticField(FIELD_MARSCHNER_LOBB, value_src, grad_src, ML_PARAMS)
+
+    @staticmethod
+    def gaussian_beam(value_src=1, grad_src=1):
+        return AnalyticField(FIELD_GAUSSIAN_BEAM, value_src, grad_src, GB_PARAMS)
+
+
 @dataclass
 class Workload:
     name: str
@@ -377,3 +402,55 @@ def tile_subset(c: int, width: int, height: int, frac: float, tile=16, views=(0,
             pix.append((ys * width + xs).ravel())
         out[v] = np.concatenate(pix).astype(np.int64)
     return out
+
+
+# ----------------------------------------------------------------------------
+# NEXT-2 quality workloads: the paper's ground-truth protocol
+# ----------------------------------------------------------------------------
+QUALITY_TESTS = ("value", "gradient", "overall")
+
+
+def ramp_red_tf(n_entries=TF_ENTRIES, a_max=0.08) -> np.ndarray:
+    """Value test: "the ramp function is used as the opacity transfer
+    function ... The color transfer function is constant red"."""
+    t = np.zeros((n_entries, 4), np.float32)
+    t[:, 0] = 1.0
+    t[:, 3] = np.linspace(0.0, a_max, n_entries)
+    return t
+
+
+def step_white_tf(n_entries=TF_ENTRIES, s0=0.5) -> np.ndarray:
+    """Gradient / overall tests: "A step function is used as the
+    opacity transfer function in order to construct a surface ... The color
+    transfer function is constant white"."""
+    t = np.ones((n_entries, 4), np.float32)
+    t[:, 3] = (np.arange(n_entries) / (n_entries - 1) >= s0).astype(np.float32)
+    return t
+
+
+def make_quality(kind: str = "ml", n: int = 64, p: int = 3, test: str = "overall", width: int = 512,
+                 height: int = 512, theta: float = 0.6, phi: float = 0.45, step_spans: float = 0.5):
+    """An MFA of the analytic function (control values = F at the Greville
+    abscissae, uniform knots, degree p, n^3 control points) and the pair of
+    renderings the paper compares: returns (workload, field of the MFA image,
+    field of the ground-truth image, shading).  kind: "ml" (Eq. 2) or "gb"
+    (Eq. 1); test: "value" (shading off, both images' values differ), "gradient"
+    (both take the analytic value, the MFA image the MFA gradient), "overall"."""
+    assert test in QUALITY_TESTS
+    knots = [clamped_uniform_knots(n, p) for _ in range(3)]
+    xi = [2.0 * greville(k, p) - 1.0 for k in knots]
+    f = marschner_lobb if kind == "ml" else gaussian_beam
+    ctrl = f(xi[0][None, None, :], xi[1][None, :, None], xi[2][:, None, None]).astype(np.float32)
+    spans = (n - p,) * 3
+    L, bmin, bmax = _box(spans)
+    make_field = AnalyticField.marschner_lobb if kind == "ml" else AnalyticField.gaussian_beam
+    shading = 0 if test == "value" else 1
+    tf = ramp_red_tf() if test == "value" else step_white_tf()
+    cam = orbit_camera(theta, phi, L, width, height)
+    params = RenderParams(box_min=bmin, box_max=bmax, step=step_spans / max(spans), shading=shading,
+                          grad_eps=grad_eps_for(ctrl, knots, p, L))
+    w = Workload(name=f"Q-{kind}{n}-p{p}-{test}-{width}x{height}", config=0, degree=p, nctrl=(n, n, n),
+                 knots=knots, ctrl=np.ascontiguousarray(ctrl), uniform=True, tf=tf, v_lo=float(ctrl.min()),
+                 v_hi=float(ctrl.max()), cameras=[cam], params=params, step_spans=step_spans)
+    mfa_field = {"value": None, "gradient": make_field(1, 0), "overall": None}[test]
+    return w, mfa_field, make_field(1, 1)

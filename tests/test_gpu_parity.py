@@ -251,3 +251,32 @@ def test_both_layouts_eval_and_render(c, layout):
 def test_default_layouts():
     assert gpu_model(3).info()["layout"] == "quads"
     assert gpu_model(5).info()["layout"] == "bezier"
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_nonuniform_multiple_knots(p):
+    """A non-uniform model with a repeated interior knot (multiplicity 2 <= p,
+    so a zero-length span the span search and tracking must step over and a
+    C^(p-2) joint); both layouts against the oracle on eval and a full frame."""
+    rng = np.random.default_rng(7 + p)
+    n = 12
+    inner = np.sort(rng.uniform(0.1, 0.9, n - p - 2))
+    inner = np.concatenate([inner, [inner[3]]])          # one double knot
+    U = np.concatenate([np.zeros(p + 1), np.sort(inner), np.ones(p + 1)])
+    assert len(U) == n + p + 1
+    ctrl = rng.uniform(-1, 1, (n, n, n)).astype(np.float32)
+    w = WL.make_config(1)
+    w.degree, w.knots, w.ctrl, w.nctrl, w.uniform = p, [U, U, U], ctrl, (n, n, n), False
+    w.v_lo, w.v_hi = float(ctrl.min()), float(ctrl.max())
+    om = O.Model.from_workload(w)
+    from paper_2204_11762_b200 import Model
+    for layout in ("quads", "bezier"):
+        m = Model.from_workload(w, layout=layout)
+        u, v, ww = WL.query_points(1, 1 << 14)
+        got = gpu_eval(m, u, v, ww)
+        ref, sig, _ = om.eval_batch(u, v, ww)
+        parity.check_eval(got, ref, sig, f"double knot p={p} {layout}")
+        img = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params)
+        torch.cuda.synchronize()
+        r = O.render(om, w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
+        parity.check_image(img[0].cpu().numpy().reshape(-1, 4), r, f"double knot p={p} {layout} render")
