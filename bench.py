@@ -335,6 +335,11 @@ def run_ours(args):
               "hbm_io_gbps": pts * 28 / 1e9}
         del u, v_, w_, outs
 
+    # ---- secondary: NEXT-4 Hessian eval, NEXT-2 ground truth + metrics -----
+    extra = None
+    if rank == 0 and not args.no_eval:
+        extra = secondary_kernels(w, m, c, p, img if world == 1 else None, tf, stream)
+
     # ---- end to end through the C ABI with host buffers --------------------
     e2e = None
     if not args.no_e2e:
@@ -365,6 +370,7 @@ def run_ours(args):
             "samples_per_step": samples_all / args.steps,
             "roofline": roof,
             "eval": ev,
+            "next": extra,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
@@ -374,6 +380,52 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _time(fn, reps, stream):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def secondary_kernels(w, m, c, p, img, tf, stream):
+    """Throughput of the NEXT rows on the bench model: mfa_eval_hessian on the
+    2^24 query points; mfa_render_field (analytic Gaussian beam value +
+    gradient along the same rays, one view); mfa_image_quality on two frames."""
+    import torch
+
+    from paper_2204_11762_b200 import image_quality, roofline as RL, workloads as WL
+    res = {}
+    u, v_, w_ = (torch.from_numpy(x).cuda() for x in WL.query_points(c, 1 << 24))
+    ms = _time(lambda: m.eval_hessian(u, v_, w_), 3, stream)
+    fh = RL.flops_per_hessian_point(p)
+    res["eval_hessian"] = {"points_per_s": (1 << 24) / (ms / 1e3), "ms": ms, "points": 1 << 24,
+                           "flops_per_point": fh, "achieved_tflops": fh * (1 << 24) / (ms / 1e3) / 1e12,
+                           "hbm_io_bytes_per_point": 12 + 40}
+    del u, v_, w_
+    cam = w.cameras[:1]
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    fld = WL.AnalyticField.gaussian_beam(1, 1)
+    out = torch.empty((1, cam[0].height, cam[0].width, 4), device="cuda")
+    cnt.zero_()
+    ms = _time(lambda: m.render(cam, tf, 0.0, 255.0, w.params, out=out, samples=cnt, field=fld), 2, stream)
+    res["render_field"] = {"samples_per_s": int(cnt.item()) / 3 / (ms / 1e3), "ms_per_view": ms,
+                           "field": "gaussian beam (value + gradient analytic, fp64)"}
+    if img is not None and img.shape[0] >= 2 and img.dtype == torch.float32:
+        a, b = img[0], img[1]
+        ws = torch.empty(int(__import__("paper_2204_11762_b200")._lib.lib().mfa_image_quality_workspace(
+            a.shape[1], a.shape[0])), dtype=torch.uint8, device="cuda")
+        ms = _time(lambda: image_quality(a, b, workspace=ws), 3, stream)
+        px = a.shape[0] * a.shape[1]
+        res["image_quality"] = {"ms": ms, "pixels": px, "gbps_input": 2 * 16 * px / (ms / 1e3) / 1e9}
+    return res
 
 
 def run_e2e(args, w, m, world, rank, local, out_dt):

@@ -137,6 +137,23 @@ mfa_status mfa_eval_batch(mfa_model m, int64_t n, const float* u, const float* v
                           unsigned long long* n_domain_errors, mfa_stream stream);
 
 /* ------------------------------------------------------------------------
+ * mfa_eval_hessian -- value, gradient and the six second partials of the MFA
+ * at n points ("Higher-order derivatives, up to the
+ * polynomial degree, are also analytically available").
+ *
+ * u, v, w     device fp32 arrays (SoA) of n parameter-space points in [0,1]^3.
+ * value       optional device fp32 [n].
+ * grad        optional device fp32 [3][n]: dF/du, dF/dv, dF/dw (parameter space).
+ * hess        device fp32 [6][n] (required): d2F/du2, d2F/dv2, d2F/dw2,
+ *             d2F/dudv, d2F/dudw, d2F/dvdw (parameter space).
+ * n_domain_errors, errors, n == 0: as mfa_eval_batch (NaN outputs for points
+ * outside [0,1]^3).  Async on stream.
+ * ---------------------------------------------------------------------- */
+mfa_status mfa_eval_hessian(mfa_model m, int64_t n, const float* u, const float* v, const float* w,
+                            float* value, float* grad, float* hess,
+                            unsigned long long* n_domain_errors, mfa_stream stream);
+
+/* ------------------------------------------------------------------------
  * mfa_render -- Algorithm 1 for every pixel of n_views views.
  *
  * Per pixel: a ray through the pixel centre (R-14 camera), clipped to

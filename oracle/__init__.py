@@ -84,6 +84,8 @@ def lib():
         _lib.orc_basis_ders2.argtypes = [C.c_int32, dp, C.c_int64, C.c_double, dp, dp, dp]
         _lib.orc_eval_hessian.restype = C.c_int
         _lib.orc_eval_hessian.argtypes = [C.POINTER(OrcModel), C.c_double, C.c_double, C.c_double, dp, dp]
+        _lib.orc_eval_hessian_batch.restype = C.c_int64
+        _lib.orc_eval_hessian_batch.argtypes = [C.POINTER(OrcModel), C.c_int64, fp, fp, fp, dp, dp, C.c_int32]
         _lib.orc_field_eval.restype = C.c_int
         _lib.orc_field_eval.argtypes = [C.POINTER(OrcField), C.c_double, C.c_double, C.c_double, dp]
         _lib.orc_render_ex.restype = C.c_int
@@ -174,12 +176,17 @@ class Model:
         rc = lib().orc_eval_hessian(C.byref(self.s), float(u), float(v), float(w), _dp(out), _dp(sig))
         return out, sig, rc
 
-    def eval_hessian_batch(self, u, v, w):
+    def eval_hessian_batch(self, u, v, w, nthreads=None):
+        """H2 over fp32 point arrays: (out (n,10), sigma (n,10), n_domain_errors)."""
+        u = np.ascontiguousarray(u, dtype=np.float32)
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        w = np.ascontiguousarray(w, dtype=np.float32)
         n = len(u)
         out, sig = np.zeros((n, 10)), np.zeros((n, 10))
-        for i in range(n):
-            out[i], sig[i], _ = self.eval_hessian(float(u[i]), float(v[i]), float(w[i]))
-        return out, sig
+        fp = C.POINTER(C.c_float)
+        errs = lib().orc_eval_hessian_batch(C.byref(self.s), n, u.ctypes.data_as(fp), v.ctypes.data_as(fp),
+                                            w.ctypes.data_as(fp), _dp(out), _dp(sig), nthreads or ncores())
+        return out, sig, int(errs)
 
     def eval_batch(self, u, v, w, nthreads=None):
         u = np.ascontiguousarray(u, dtype=np.float32)

@@ -661,3 +661,38 @@ int64_t orc_eval_batch(const orc_model* m, int64_t n, const float* u, const floa
     free(th);
     return errs;
 }
+
+/* Batched H2 over threads (fp32 inputs used exactly); domain errors -> NaN rows. */
+typedef struct {
+    const orc_model* m;
+    const float *u, *v, *w;
+    double *out, *sig;
+    int64_t begin, end, errors;
+} hess_job;
+
+static void* hess_worker(void* arg)
+{
+    hess_job* j = (hess_job*)arg;
+    for (int64_t i = j->begin; i < j->end; ++i)
+        if (orc_eval_hessian(j->m, j->u[i], j->v[i], j->w[i], j->out + 10 * i, j->sig ? j->sig + 10 * i : NULL) < 0)
+            j->errors++;
+    return NULL;
+}
+
+int64_t orc_eval_hessian_batch(const orc_model* m, int64_t n, const float* u, const float* v, const float* w,
+                               double* out10, double* sigma10, int32_t nthreads)
+{
+    if (nthreads < 1) nthreads = 1;
+    if (n < nthreads) nthreads = n > 0 ? (int32_t)n : 1;
+    hess_job* jobs = (hess_job*)calloc((size_t)nthreads, sizeof(hess_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t] = (hess_job){m, u, v, w, out10, sigma10, n * t / nthreads, n * (t + 1) / nthreads, 0};
+        pthread_create(&th[t], NULL, hess_worker, &jobs[t]);
+    }
+    int64_t errs = 0;
+    for (int t = 0; t < nthreads; ++t) { pthread_join(th[t], NULL); errs += jobs[t].errors; }
+    free(jobs);
+    free(th);
+    return errs;
+}

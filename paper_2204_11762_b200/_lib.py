@@ -23,7 +23,7 @@ LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2}
 # C-ABI symbols declared in include/mfa.h (checked by tests/test_abi.py)
 EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
            "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version",
-           "mfa_render_field", "mfa_image_quality", "mfa_image_quality_workspace",
+           "mfa_render_field", "mfa_image_quality", "mfa_image_quality_workspace", "mfa_eval_hessian",
            "mfa_probe_fp32", "mfa_probe_read_bw")
 
 
@@ -93,6 +93,8 @@ def lib():
         L.mfa_model_destroy.argtypes = [vp]
         L.mfa_eval_batch.restype = C.c_int
         L.mfa_eval_batch.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.mfa_eval_hessian.restype = C.c_int
+        L.mfa_eval_hessian.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
         L.mfa_render.restype = C.c_int
         L.mfa_render.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
                                  C.POINTER(Tiles_t), vp, vp, vp]
@@ -243,6 +245,18 @@ class Model:
         _check(lib().mfa_eval_batch(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(du), _ptr(dv),
                                     _ptr(dw), _ptr(n_domain_errors), _stream_ptr(stream)))
         return out
+
+    def eval_hessian(self, u, v, w, n_domain_errors=None, stream=None):
+        """NEXT-4 (mfa_eval_hessian): returns (value [n], grad [3,n], hess [6,n]),
+        hess rows = d2/du2, d2/dv2, d2/dw2, d2/dudv, d2/dudw, d2/dvdw (parameter space)."""
+        import torch
+        n = u.numel()
+        val = torch.empty(n, device=u.device, dtype=torch.float32)
+        grad = torch.empty((3, n), device=u.device, dtype=torch.float32)
+        hess = torch.empty((6, n), device=u.device, dtype=torch.float32)
+        _check(lib().mfa_eval_hessian(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(grad), _ptr(hess),
+                                      _ptr(n_domain_errors), _stream_ptr(stream)))
+        return val, grad, hess
 
     # -- Algorithm 1 (mfa_render) ---------------------------------------------
     def render(self, cams, tf, v_lo, v_hi, params, tiles=None, out=None, samples=None, out_fp16=False,

@@ -8,7 +8,8 @@ add / mul / div / rsqrt / exp2 / log2 = 1 FLOP:
   a3 position 14, a4 local coordinate 12, a8 TF 16, a9 Phong 36, a10 composite 9
   -> F(p) = 366 / 627 / 1011 for p = 2 / 3 / 4.
 Counted control-point bytes per sample B(p) = 4 q^3 (108 / 256 / 500).
-Per eval point: contraction + basis + 12.
+Per eval point: contraction + basis + 12.  Per Hessian point (NEXT-4):
+2 (3 q^3 + 6 q^2 + 10 q) + 3 q (6 p + 1) + 21.
 
 FP32 peak (CUDA cores): SMs x 128 lanes x 2 FLOP x SM clock.  B200 has 148
 SMs and clocks.max.sm = 1965 MHz (B200_PROFILING.md) -> 74.4 TFLOP/s.
@@ -44,6 +45,14 @@ def flops_per_sample(p: int, shading: bool = True) -> int:
 
 def flops_per_eval_point(p: int) -> int:
     return flops_contraction(p) + flops_basis(p) + 12
+
+
+def flops_per_hessian_point(p: int) -> int:
+    """NEXT-4 per point: x-stage 3 q^3, y-stage 6 q^2, z-stage 10 q FMAs; per
+    axis q three-output Horner evaluations (3p FMA + 1 mul each); locate 12;
+    t -> u scaling 9."""
+    q = p + 1
+    return 2 * (3 * q ** 3 + 6 * q ** 2 + 10 * q) + 3 * q * (6 * p + 1) + 12 + 9
 
 
 def bytes_per_sample(p: int) -> int:

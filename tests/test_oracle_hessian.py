@@ -28,10 +28,9 @@ def test_uniform_cubic_interior_closed_form():
     p, n = 3, 12
     S = n - p
     U = uniform_knots(p, n)
-    for span in range(2 * p - 1 + p, n - p + 1 - 1 + 1):   # interior spans (knot index)
-        if not (2 * p - 1 <= span - p <= S - p):
-            continue
-        u = (span - p + 0.5) / S
+    for sp in range(2 * p - 1, S - p + 1):        # interior spans (local index)
+        span = sp + p
+        u = (sp + 0.5) / S
         N, dN, d2N = O.basis_ders2(p, U, span, u)
         np.testing.assert_allclose(N, np.array([1, 23, 23, 1]) / 48, atol=1e-14)
         np.testing.assert_allclose(d2N, S * S * np.array([0.5, -0.5, -0.5, 0.5]), atol=1e-10)
@@ -115,3 +114,17 @@ def test_hessian_vs_gradient_differences_and_eval(p):
             qm[j] -= h
             fd = (m.eval(*qp)[0][1 + i] - m.eval(*qm)[0][1 + i]) / (2 * h)
             assert abs(fd - out[k]) <= 1e-5 * sig[k] + 1e-9, (p, i, j, fd, out[k], sig[k])
+
+
+def test_hessian_batch_matches_single():
+    r = np.random.default_rng(60)
+    p, n = 3, (9, 8, 7)
+    knots = [rand_knots(r, p, n[d]) for d in range(3)]
+    m = O.Model(p, knots, r.uniform(-1, 1, (n[2], n[1], n[0])).astype(np.float32))
+    u, v, w = (r.random(50, dtype=np.float32) for _ in range(3))
+    u[3] = 1.5
+    out, sig, errs = m.eval_hessian_batch(u, v, w, nthreads=3)
+    assert errs == 1 and np.isnan(out[3]).all()
+    for i in (0, 7, 49):
+        o, s_, _ = m.eval_hessian(u[i], v[i], w[i])
+        np.testing.assert_array_equal(out[i], o)
