@@ -454,3 +454,20 @@ def make_quality(kind: str = "ml", n: int = 64, p: int = 3, test: str = "overall
                  v_hi=float(ctrl.max()), cameras=[cam], params=params, step_spans=step_spans)
     mfa_field = {"value": None, "gradient": make_field(1, 0), "overall": None}[test]
     return w, mfa_field, make_field(1, 1)
+
+
+# ----------------------------------------------------------------------------
+# NEXT-3 encoder inputs: structured grids of the analytic functions
+# ----------------------------------------------------------------------------
+def analytic_grid(kind: str, dims, noise: float = 0.0, seed: int = 0) -> np.ndarray:
+    """Grid (m_w, m_v, m_u) of Eq. 1 ("gb") or Eq. 2 ("ml") sampled at the
+    uniform parameters j/(m-1) mapped to [-1,1], fp64; optional iid
+    N(0, noise) (the discrete datasets of P:155 'generated from those
+    functions')."""
+    mu, mv, mw = dims
+    x = [2.0 * np.arange(m) / (m - 1) - 1.0 for m in (mu, mv, mw)]
+    f = marschner_lobb if kind == "ml" else gaussian_beam
+    g = f(x[0][None, None, :], x[1][None, :, None], x[2][:, None, None])
+    if noise:
+        g = g + np.random.default_rng(seed).normal(0.0, noise, g.shape)
+    return np.ascontiguousarray(g)
