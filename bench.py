@@ -418,6 +418,21 @@ def secondary_kernels(w, m, c, p, img, tf, stream):
     ms = _time(lambda: m.render(cam, tf, 0.0, 255.0, w.params, out=out, samples=cnt, field=fld), 2, stream)
     res["render_field"] = {"samples_per_s": int(cnt.item()) / 3 / (ms / 1e3), "ms_per_view": ms,
                            "field": "gaussian beam (value + gradient analytic, fp64)"}
+    # NEXT-3: least-squares fit of a 256^3 Gaussian-beam grid (the paper's timing
+    # function) to 128^3 control points, p = 3; and the adaptive loop
+    from paper_2204_11762_b200 import encode_grid, fit_grid
+    q = torch.from_numpy(WL.analytic_grid("gb", (256, 256, 256)).astype(np.float32)).cuda()
+    kn = [WL.clamped_uniform_knots(128, 3)] * 3
+    ms = _time(lambda: fit_grid(q, 3, kn), 3, stream)
+    mbytes = 4 * 256 ** 3 + 4 * 128 ** 3 + 2 * 8 * (128 * 256 * 256 + 128 * 128 * 256) + 2 * 8 * 128 ** 3
+    res["fit_grid"] = {"ms": ms, "samples_per_s": 256 ** 3 / (ms / 1e3), "grid": [256, 256, 256],
+                       "nctrl": [128, 128, 128], "degree": 3, "hbm_bytes_min": mbytes,
+                       "gbps_min_traffic": mbytes / (ms / 1e3) / 1e9}
+    t0 = time.perf_counter()
+    _, _, er, log = encode_grid(q, 3, (8, 8, 8), 1e-3, 8, (128, 128, 128))
+    res["encode_grid"] = {"s": time.perf_counter() - t0, "e_max": 1e-3, "result": er,
+                          "rounds_nctrl_maxerr": [[int(r[0]), int(r[1]), int(r[2]), float(r[3])] for r in log]}
+    del q
     if img is not None and img.shape[0] >= 2 and img.dtype == torch.float32:
         a, b = img[0], img[1]
         ws = torch.empty(int(__import__("paper_2204_11762_b200")._lib.lib().mfa_image_quality_workspace(

@@ -294,6 +294,66 @@ mfa_status mfa_image_quality(int32_t width, int32_t height, const float* img_a, 
                              float* err_map, void* workspace, size_t workspace_bytes, double* out3,
                              mfa_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Encoder (PAPER.md P:74-76 and the Fig. 1 caption
+ * "New control points and knots are added adaptively until all
+ * evaluated points in each span of knots are within the allowable maximum
+ * relative error of the original points ... knot spans that fall beyond the
+ * tolerance are subdivided, and MFA is recomputed").
+ *
+ * Input: a structured grid, device fp32 values[m_w][m_v][m_u] (u fastest),
+ * sample (i,j,k) at parameters (i/(m_u-1), j/(m_v-1), k/(m_w-1)) (R-27).
+ * ---------------------------------------------------------------------- */
+
+/*
+ * mfa_fit_grid -- least-squares control values for given knots: the
+ * minimiser of || (N_w (x) N_v (x) N_u) c - q ||_2 (computed separably, exact
+ * for the tensor-product problem), fp64 arithmetic.
+ * dims[3]     m_u, m_v, m_w (each in [2, 2^20]).
+ * degree      1..5; nctrl[d] in [degree+1, dims[d]]; knots[d] host fp64 clamped
+ *             knot vectors, length nctrl[d]+degree+1.
+ * ctrl_out    device fp32 [n_w][n_v][n_u] (required); ctrl_out64 optional
+ *             device fp64 copy.  A knot layout that leaves a basis function
+ *             without samples makes the normal equations singular:
+ *             MFA_ERR_INVALID_ARG naming the axis.  Scratch is allocated
+ *             internally (not a render-path call); returns after the stream
+ *             is synchronised.
+ */
+mfa_status mfa_fit_grid(const int64_t dims[3], const float* values, int32_t degree, const int64_t nctrl[3],
+                        const double* const knots[3], float* ctrl_out, double* ctrl_out64, mfa_stream stream);
+
+typedef struct {
+    int32_t degree;          /* 1..5, all axes */
+    int64_t nctrl_init[3];   /* initial control counts (clamped uniform knots), >= degree+1 */
+    double e_max;            /* allowable maximum relative error |f - q| / (max q - min q) */
+    int32_t max_rounds;      /* refinement rounds after the first fit (0: fit once) */
+    int64_t max_ctrl[3];     /* per-axis control-count caps (also capped at dims[d]) */
+} mfa_encode_config;
+
+typedef struct {
+    int64_t nctrl[3];        /* control counts of the returned model */
+    int32_t rounds;          /* fits performed */
+    int32_t converged;       /* 1 if the max relative error <= e_max */
+    double max_err, rms_err; /* relative errors of the returned fit at the input samples */
+} mfa_encode_result;
+
+/*
+ * mfa_encode_grid -- the adaptive encoder: fit, evaluate at every sample,
+ * per axis and knot span the max relative error over the samples in that
+ * span; split every span above e_max holding >= 2(p+1) samples at its midpoint
+ * (within the caps) and refit, until the max error <= e_max, max_rounds, or
+ * nothing can be split (R-28).
+ * knots_out[d]  host fp64, capacity max_ctrl[d]+degree+1: the final knots.
+ * ctrl_out      device fp32, capacity prod(max_ctrl): the final control values
+ *               [n_w][n_v][n_u] with n = res->nctrl.
+ * round_log     optional host fp64 [(max_rounds+1)][5]: per fit n_u, n_v, n_w,
+ *               max error, rms error.
+ * Deterministic except for the rms summation order.  Synchronous.
+ */
+mfa_status mfa_encode_grid(const int64_t dims[3], const float* values, const mfa_encode_config* cfg,
+                           double* const knots_out[3], float* ctrl_out, mfa_encode_result* res,
+                           double* round_log, mfa_stream stream);
+
 /* Thread-local message for the last non-OK status on this thread ("" if none). */
 const char* mfa_last_error(void);
 

@@ -19,7 +19,9 @@ in DESIGN.md, after SPEC S:124-200):
                     tolerance are subdivided, and MFA is recomputed":
                     per axis, a span's error = max error over the samples whose
                     coordinate on that axis lies in the span; every span above
-                    e_max holding >= 2 samples is split at its midpoint, within
+                    e_max holding >= 2(p+1) samples is split at its midpoint (so every
+                    span keeps >= p+1 samples and the normal equations stay
+                    regular, Schoenberg-Whitney), within
                     the per-axis control-count cap; stop when the max error <= e_max,
                     after max_rounds, or when nothing can be split.
 """
@@ -112,7 +114,7 @@ def adaptive(q, p: int, nctrl, e_max: float, max_rounds: int, max_ctrl):
             n = len(U) - p - 1
             ins = []
             for s in range(len(per)):
-                if per[s] > e_max and cnt[s] >= 2 and n + len(ins) < max_ctrl[d]:
+                if per[s] > e_max and cnt[s] >= 2 * (p + 1) and n + len(ins) < max_ctrl[d]:
                     lo, hi = U[p + s], U[p + s + 1]
                     ins.append(0.5 * (lo + hi))
             if ins:

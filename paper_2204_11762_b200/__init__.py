@@ -10,6 +10,6 @@ of a tensor-product B-spline (MFA) model on sm_100a.
 The C ABI is include/mfa.h; libmfa.so is built in-tree by
 ``python -m paper_2204_11762_b200.build``.  There is no CPU fallback.
 """
-from ._lib import Model, MfaError, image_quality, lib, unpack_tiles, version  # noqa: F401
+from ._lib import Model, MfaError, encode_grid, fit_grid, image_quality, lib, unpack_tiles, version  # noqa: F401
 
-__all__ = ["Model", "MfaError", "image_quality", "lib", "unpack_tiles", "version"]
+__all__ = ["Model", "MfaError", "encode_grid", "fit_grid", "image_quality", "lib", "unpack_tiles", "version"]

@@ -24,6 +24,7 @@ LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2}
 EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
            "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version",
            "mfa_render_field", "mfa_image_quality", "mfa_image_quality_workspace", "mfa_eval_hessian",
+           "mfa_fit_grid", "mfa_encode_grid",
            "mfa_probe_fp32", "mfa_probe_read_bw")
 
 
@@ -65,6 +66,16 @@ class Field_t(C.Structure):
                 ("prm", C.c_double * 6)]
 
 
+class EncodeConfig_t(C.Structure):
+    _fields_ = [("degree", C.c_int32), ("nctrl_init", C.c_int64 * 3), ("e_max", C.c_double),
+                ("max_rounds", C.c_int32), ("max_ctrl", C.c_int64 * 3)]
+
+
+class EncodeResult_t(C.Structure):
+    _fields_ = [("nctrl", C.c_int64 * 3), ("rounds", C.c_int32), ("converged", C.c_int32),
+                ("max_err", C.c_double), ("rms_err", C.c_double)]
+
+
 class ModelOptions_t(C.Structure):
     _fields_ = [("layout", C.c_int32)]
 
@@ -98,6 +109,12 @@ def lib():
         L.mfa_render.restype = C.c_int
         L.mfa_render.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
                                  C.POINTER(Tiles_t), vp, vp, vp]
+        L.mfa_fit_grid.restype = C.c_int
+        L.mfa_fit_grid.argtypes = [C.POINTER(i64), vp, i32, C.POINTER(i64), C.POINTER(C.POINTER(C.c_double)), vp,
+                                   vp, vp]
+        L.mfa_encode_grid.restype = C.c_int
+        L.mfa_encode_grid.argtypes = [C.POINTER(i64), vp, C.POINTER(EncodeConfig_t),
+                                      C.POINTER(C.POINTER(C.c_double)), vp, C.POINTER(EncodeResult_t), vp, vp]
         L.mfa_render_field.restype = C.c_int
         L.mfa_render_field.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
                                        C.POINTER(Field_t), C.POINTER(Tiles_t), vp, vp, vp]
@@ -330,6 +347,53 @@ def image_quality(a, b, err_map=False, workspace=None, stream=None):
     if err_map:
         res["err_map"] = em
     return res
+
+
+def _knots_arg(knots):
+    ks = [np.ascontiguousarray(k, dtype=np.float64) for k in knots]
+    arr = (C.POINTER(C.c_double) * 3)(*[k.ctypes.data_as(C.POINTER(C.c_double)) for k in ks])
+    return ks, arr
+
+
+def fit_grid(values, degree: int, knots, want64=False, stream=None):
+    """NEXT-3 least-squares fit (mfa_fit_grid): values = CUDA fp32 grid
+    [m_w, m_v, m_u]; knots = 3 fp64 clamped knot vectors.  Returns the control
+    values [n_w, n_v, n_u] (fp32, plus the fp64 copy if want64)."""
+    import torch
+    values = values.contiguous()
+    mw, mv, mu = values.shape
+    dims = (C.c_int64 * 3)(mu, mv, mw)
+    n = [len(k) - degree - 1 for k in knots]
+    nct = (C.c_int64 * 3)(*n)
+    ks, karr = _knots_arg(knots)
+    c32 = torch.empty((n[2], n[1], n[0]), dtype=torch.float32, device=values.device)
+    c64 = torch.empty((n[2], n[1], n[0]), dtype=torch.float64, device=values.device) if want64 else None
+    _check(lib().mfa_fit_grid(dims, _ptr(values), int(degree), nct, karr, _ptr(c32), _ptr(c64), _stream_ptr(stream)))
+    return (c32, c64) if want64 else c32
+
+
+def encode_grid(values, degree: int, nctrl_init, e_max: float, max_rounds: int, max_ctrl, stream=None):
+    """NEXT-3 adaptive encoder (mfa_encode_grid).  Returns (knots [3 x np.ndarray],
+    ctrl CUDA fp32 [n_w, n_v, n_u], result dict, per-round log (rounds x 5))."""
+    import torch
+    values = values.contiguous()
+    mw, mv, mu = values.shape
+    dims = (C.c_int64 * 3)(mu, mv, mw)
+    cfg = EncodeConfig_t(int(degree), (C.c_int64 * 3)(*nctrl_init), float(e_max), int(max_rounds),
+                         (C.c_int64 * 3)(*max_ctrl))
+    cap = [min(int(max_ctrl[d]), (mu, mv, mw)[d]) for d in range(3)]
+    kbuf = [np.zeros(cap[d] + degree + 1) for d in range(3)]
+    _, karr = _knots_arg(kbuf)
+    ctrl = torch.empty(cap[0] * cap[1] * cap[2], dtype=torch.float32, device=values.device)
+    res = EncodeResult_t()
+    log = np.zeros((max_rounds + 1, 5))
+    _check(lib().mfa_encode_grid(dims, _ptr(values), C.byref(cfg), karr, _ptr(ctrl), C.byref(res),
+                                 C.c_void_p(log.ctypes.data), _stream_ptr(stream)))
+    n = [int(x) for x in res.nctrl]
+    knots = [kbuf[d][:n[d] + degree + 1].copy() for d in range(3)]
+    out = dict(nctrl=tuple(n), rounds=res.rounds, converged=bool(res.converged), max_err=res.max_err,
+               rms_err=res.rms_err)
+    return knots, ctrl[:n[0] * n[1] * n[2]].view(n[2], n[1], n[0]), out, log[:res.rounds].copy()
 
 
 def version() -> str:

@@ -60,7 +60,9 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
     if failed:
         raise RuntimeError("nvcc failed")
     tmp = LIB + ".tmp"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+    cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-L" + cudalib, "-lcublas",
+                           "-Xlinker", "-rpath=" + cudalib, "-lrt", "-ldl", "-lpthread"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -1,0 +1,540 @@
+// MFA encoder: least-squares fit of the control points
+// of a tensor-product B-spline to a structured grid, and the adaptive loop of
+// Fig. 1 ("New control points and knots are added adaptively until all
+// evaluated points in each span of knots are within the allowable maximum
+// relative error of the original points ... knot spans that fall beyond the
+// tolerance are subdivided, and MFA is recomputed").
+//
+// Fit (R-27): grid samples at uniform parameters t_j = j/(m-1) per axis; the
+// least-squares solution of (N_w (x) N_v (x) N_u) c = q is separable,
+// c = q x_u N_u^+ x_v N_v^+ x_w N_w^+ with N^+ = (N^T N)^{-1} N^T:
+//   host    per axis: sample spans, basis values (power form per span, fp64),
+//           the banded normal matrix A = N^T N (bandwidth p), its banded
+//           Cholesky factor (a span without samples -> singular -> error), and
+//           the dense n x m operator N^+ by banded solves with the sparse
+//           columns of N^T (fp64)
+//   device  the three axis passes are plain dense fp64 GEMMs over all grid
+//           lines (cuBLAS DGEMM: w pass one GEMM, v pass a strided batch over
+//           the w slices, u pass one GEMM with the operator transposed), with
+//           fp32 <-> fp64 conversion kernels at the ends.  A dense operator
+//           costs 2 m n flops per line instead of the banded solve's ~4 m p,
+//           but every line is independent and the GEMMs run at fp64 tensor
+//           rate; the banded solve is a chain of 2n dependent steps per line.
+// Residual (adaptive loop): K_expand applies N along each axis (the spline
+// at every grid sample, separable), K_err forms |v - q| / (max q - min q) and
+// per-axis per-span maxima (atomicMax on the ordered bits of non-negative
+// doubles); the host splits every span above e_max that holds >= 2(p+1) samples at
+// its midpoint (R-28: every span keeps >= p+1 samples, so the normal equations
+// stay regular), within the per-axis caps, and refits.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include <cublas_v2.h>
+
+#include <map>
+#include <mutex>
+
+#include "mfa_internal.cuh"
+
+namespace mfa {
+
+struct AxisFit {
+    int m = 0, n = 0, p = 0;
+    std::vector<int> f;          // [m] index of the first non-zero function at sample j (= local span)
+    std::vector<double> B;       // [m][p+1] basis values N_{f_j + a}(t_j)
+    std::vector<double> L;       // [n][p+1] banded Cholesky factor, L[i][k] = L(i, i-k)
+    std::vector<double> M;       // [n][m] dense N^+ = (N^T N)^{-1} N^T
+};
+
+struct AxisFitDev {
+    int m, n;
+    const int* f;       // [m]
+    const double* B;    // [m][p+1]
+    const double* M;    // [n][m] dense N^+
+};
+
+// host: the knot span of parameter t (right-continuous; t = 1 -> last non-degenerate span)
+static int host_span(const double* U, int p, int n, double t) {
+    if (t >= U[n]) {
+        int i = n - 1;
+        while (i > p && U[i] == U[n]) --i;
+        return i;
+    }
+    int lo = p, hi = n;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) / 2;
+        if (t < U[mid]) hi = mid; else lo = mid;
+    }
+    return lo;
+}
+
+static mfa_status build_axis(int d, int m, int n, int p, const double* U, AxisFit& A) {
+    A.m = m;
+    A.n = n;
+    A.p = p;
+    A.f.assign(m, 0);
+    A.B.assign((size_t)m * (p + 1), 0.0);
+    for (int j = 0; j < m; ++j) {
+        const double t = (double)j / (double)(m - 1);
+        const int span = host_span(U, p, n, t);
+        double P[kMaxP + 1][kMaxP + 1];
+        span_poly(U, p, span, P);
+        const double h = U[span + 1] - U[span];
+        const double x = (t - U[span]) / h;
+        for (int a = 0; a <= p; ++a) {
+            double v = P[a][p];
+            for (int k = p - 1; k >= 0; --k) v = v * x + P[a][k];
+            A.B[(size_t)j * (p + 1) + a] = v;
+        }
+        A.f[j] = span - p;
+    }
+    // banded normal matrix: Ab[i][k] = (N^T N)(i, i-k)
+    std::vector<double> Ab((size_t)n * (p + 1), 0.0);
+    for (int j = 0; j < m; ++j)
+        for (int a = 0; a <= p; ++a)
+            for (int b = 0; b <= a; ++b)
+                Ab[(size_t)(A.f[j] + a) * (p + 1) + (a - b)] += A.B[(size_t)j * (p + 1) + a] * A.B[(size_t)j * (p + 1) + b];
+    // banded Cholesky A = L L^T
+    A.L.assign((size_t)n * (p + 1), 0.0);
+    auto Lat = [&](int r, int c) -> double& { return A.L[(size_t)r * (p + 1) + (r - c)]; };
+    for (int i = 0; i < n; ++i) {
+        for (int c = std::max(0, i - p); c < i; ++c) {
+            double s = Ab[(size_t)i * (p + 1) + (i - c)];
+            for (int l = std::max(0, i - p); l < c; ++l) s -= Lat(i, l) * Lat(c, l);
+            Lat(i, c) = s / Lat(c, c);
+        }
+        double s = Ab[(size_t)i * (p + 1)];
+        for (int l = std::max(0, i - p); l < i; ++l) s -= Lat(i, l) * Lat(i, l);
+        if (!(s > 1e-14 * std::max(1.0, Ab[(size_t)i * (p + 1)])))
+            return fail(MFA_ERR_INVALID_ARG, std::string("fit: normal equations singular on axis ") + "uvw"[d] +
+                                                 " at control point " + std::to_string(i) +
+                                                 " (a basis function without samples: too many control points for the grid)");
+        Lat(i, i) = sqrt(s);
+    }
+    // dense pseudo-inverse N^+ = A^{-1} N^T (n x m, row-major): column j of N^T
+    // has p+1 entries at rows f_j .. f_j + p; forward then backward banded solve
+    A.M.assign((size_t)n * m, 0.0);
+    std::vector<double> y(n);
+    for (int j = 0; j < m; ++j) {
+        std::fill(y.begin(), y.end(), 0.0);
+        const int i0 = A.f[j];
+        for (int i = i0; i < n; ++i) {
+            double r = (i - i0 <= p) ? A.B[(size_t)j * (p + 1) + (i - i0)] : 0.0;
+            for (int l = std::max(i0, i - p); l < i; ++l) r -= Lat(i, l) * y[l];
+            y[i] = r / Lat(i, i);
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            double r = y[i];
+            for (int l = i + 1; l <= std::min(n - 1, i + p); ++l) r -= Lat(l, i) * y[l];
+            y[i] = r / Lat(i, i);
+        }
+        for (int i = 0; i < n; ++i) A.M[(size_t)i * m + j] = y[i];
+    }
+    return MFA_OK;
+}
+
+__global__ void f32_to_f64_kernel(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (double)a[i];
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (float)a[i];
+}
+
+// the spline along one axis at the grid samples: out_j = sum_a N_{f_j+a}(t_j) in_{f_j+a}
+template <int P>
+__global__ void __launch_bounds__(128) expand_axis_kernel(const double* __restrict__ X, double* __restrict__ Y,
+                                                          const AxisFitDev ax, int64_t n_outer, int64_t inner) {
+    const int64_t total = n_outer * ax.m * inner;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t in = idx % inner;
+        const int64_t rest = idx / inner;
+        const int j = (int)(rest % ax.m);
+        const int64_t o = rest / ax.m;
+        const int f = __ldg(ax.f + j);
+        const double* x = X + (o * ax.n + f) * inner + in;
+        double v = 0.0;
+#pragma unroll
+        for (int a = 0; a <= P; ++a) v = fma(__ldg(ax.B + j * (P + 1) + a), x[a * inner], v);
+        Y[idx] = v;
+    }
+}
+
+__device__ __forceinline__ unsigned long long dbits(double x) { return (unsigned long long)__double_as_longlong(x); }
+
+// relative errors at the samples: per-axis per-span maxima, global max, sum of squares
+__global__ void grid_error_kernel(const double* __restrict__ V, const float* __restrict__ Q, int mu, int mv, int mw,
+                                  double inv_range, const int* __restrict__ fu, const int* __restrict__ fv,
+                                  const int* __restrict__ fw, unsigned long long* __restrict__ eu,
+                                  unsigned long long* __restrict__ ev, unsigned long long* __restrict__ ew,
+                                  unsigned long long* __restrict__ emax, double* __restrict__ esq) {
+    const int64_t total = (int64_t)mu * mv * mw;
+    double sq = 0.0, mx = 0.0;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx % mu);
+        const int j = (int)((idx / mu) % mv);
+        const int k = (int)(idx / ((int64_t)mu * mv));
+        const double e = fabs(V[idx] - (double)Q[idx]) * inv_range;
+        sq += e * e;
+        mx = fmax(mx, e);
+        atomicMax(eu + __ldg(fu + i), dbits(e));
+        atomicMax(ev + __ldg(fv + j), dbits(e));
+        atomicMax(ew + __ldg(fw + k), dbits(e));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(esq, sq);
+        atomicMax(emax, dbits(mx));
+    }
+}
+
+__global__ void range_kernel(const float* __restrict__ Q, int64_t n, double* __restrict__ out /*min,max*/) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        lo = fmin(lo, (double)Q[i]);
+        hi = fmax(hi, (double)Q[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {   // ordered-bits trick: negate for the minimum of possibly negative values
+        const unsigned long long blo = dbits(lo), bhi = dbits(hi);
+        atomicMin(reinterpret_cast<unsigned long long*>(out) + 0,
+                  (blo & 0x8000000000000000ULL) ? ~blo : (blo | 0x8000000000000000ULL));
+        atomicMax(reinterpret_cast<unsigned long long*>(out) + 1,
+                  (bhi & 0x8000000000000000ULL) ? ~bhi : (bhi | 0x8000000000000000ULL));
+    }
+}
+
+static double ord_to_double(unsigned long long u) {
+    const unsigned long long b = (u & 0x8000000000000000ULL) ? (u & 0x7fffffffffffffffULL) : ~u;
+    double d;
+    memcpy(&d, &b, 8);
+    return d;
+}
+
+// device copy of one axis' tables (one allocation)
+struct AxisDevMem {     // stream-ordered allocations (the pool makes repeated fits cheap)
+    void* mem = nullptr;
+    AxisFitDev d{};
+    void release(cudaStream_t st) {
+        if (mem) cudaFreeAsync(mem, st);
+        mem = nullptr;
+    }
+};
+
+static cudaError_t upload_axis(const AxisFit& A, AxisDevMem& D, cudaStream_t st) {
+    const size_t nf = sizeof(int) * A.m, nb = sizeof(double) * A.B.size(), nm = sizeof(double) * A.M.size();
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    cudaError_t e = cudaMallocAsync(&D.mem, up(nf) + up(nb) + up(nm), st);
+    if (e != cudaSuccess) return e;
+    char* b = (char*)D.mem;
+    int* f = (int*)b;
+    double* B = (double*)(b + up(nf));
+    double* M = (double*)(b + up(nf) + up(nb));
+    cudaMemcpyAsync(f, A.f.data(), nf, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(B, A.B.data(), nb, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(M, A.M.data(), nm, cudaMemcpyHostToDevice, st);
+    D.d = AxisFitDev{A.m, A.n, f, B, M};
+    return cudaSuccess;
+}
+
+// Keep the device's default stream-ordered pool from returning memory to the
+// driver at every synchronisation, so repeated fits / refinement rounds reuse
+// their scratch instead of re-mapping it (once per device).
+static void keep_pool() {
+    static std::mutex mu;
+    static std::map<int, bool> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = 8ULL << 30;   // keep up to 8 GiB cached
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
+// one cuBLAS handle per (host thread, device)
+static cublasStatus_t blas_handle(cublasHandle_t* h) {
+    static thread_local std::map<int, cublasHandle_t> handles;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto it = handles.find(dev);
+    if (it != handles.end()) {
+        *h = it->second;
+        return CUBLAS_STATUS_SUCCESS;
+    }
+    cublasStatus_t r = cublasCreate(h);
+    if (r == CUBLAS_STATUS_SUCCESS) handles[dev] = *h;
+    return r;
+}
+
+static unsigned grid_for(int64_t work) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 127) / 128, (int64_t)sms * 16));
+}
+
+// the three axis passes as fp64 GEMMs (row-major views; cuBLAS is column-major):
+//   w: T1[nw][mv*mu]  = M_w[nw][mw] . Q64[mw][mv*mu]
+//   v: T2[k][nv][mu]  = M_v[nv][mv] . T1[k][mv][mu]      (batch over k < nw)
+//   u: C64[nw*nv][nu] = T2[nw*nv][mu] . M_u^T
+static mfa_status fit_all(const double* Q64, const AxisFitDev (&ax)[3], double* T1, double* T2, float* C32,
+                          double* C64, cudaStream_t st) {
+    const int mu = ax[0].m, mv = ax[1].m, mw = ax[2].m, nu = ax[0].n, nv = ax[1].n, nw = ax[2].n;
+    cublasHandle_t h;
+    if (blas_handle(&h) != CUBLAS_STATUS_SUCCESS) return fail(MFA_ERR_CUDA, "cublasCreate failed");
+    cublasSetStream(h, st);
+    const double one = 1.0, zero = 0.0;
+    cublasStatus_t r = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, mv * mu, nw, mw, &one, Q64, mv * mu, ax[2].M, mw,
+                                   &zero, T1, mv * mu);
+    if (r == CUBLAS_STATUS_SUCCESS)
+        r = cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, mu, nv, mv, &one, T1, mu, (long long)mv * mu,
+                                      ax[1].M, mv, 0, &zero, T2, mu, (long long)nv * mu, nw);
+    if (r == CUBLAS_STATUS_SUCCESS)
+        r = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, nu, nw * nv, mu, &one, ax[0].M, mu, T2, mu, &zero, C64, nu);
+    if (r != CUBLAS_STATUS_SUCCESS) return fail(MFA_ERR_CUDA, "cublasDgemm failed (" + std::to_string((int)r) + ")");
+    const int64_t nc = (int64_t)nu * nv * nw;
+    f64_to_f32_kernel<<<grid_for(nc), 128, 0, st>>>(C64, C32, nc);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? MFA_OK : cuda_fail(e, "fit conversion");
+}
+
+template <int P>
+static cudaError_t expand_all_t(const double* C64, const AxisFitDev (&ax)[3], double* T1, double* T2, double* V,
+                                cudaStream_t st) {
+    const int mu = ax[0].m, mv = ax[1].m, mw = ax[2].m, nv = ax[1].n, nw = ax[2].n;
+    expand_axis_kernel<P><<<grid_for((int64_t)nw * nv * mu), 128, 0, st>>>(C64, T1, ax[0], (int64_t)nw * nv, 1);
+    expand_axis_kernel<P><<<grid_for((int64_t)nw * mv * mu), 128, 0, st>>>(T1, T2, ax[1], nw, mu);
+    expand_axis_kernel<P><<<grid_for((int64_t)mw * mv * mu), 128, 0, st>>>(T2, V, ax[2], 1, (int64_t)mv * mu);
+    return cudaGetLastError();
+}
+
+static cudaError_t expand_all(int p, const double* C64, const AxisFitDev (&ax)[3], double* T1, double* T2, double* V,
+                              cudaStream_t st) {
+    switch (p) {
+        case 1: return expand_all_t<1>(C64, ax, T1, T2, V, st);
+        case 2: return expand_all_t<2>(C64, ax, T1, T2, V, st);
+        case 3: return expand_all_t<3>(C64, ax, T1, T2, V, st);
+        case 4: return expand_all_t<4>(C64, ax, T1, T2, V, st);
+        default: return expand_all_t<5>(C64, ax, T1, T2, V, st);
+    }
+}
+
+// scratch sized for the largest control counts the loop may reach
+struct FitScratch {
+    double *Q64 = nullptr, *T1 = nullptr, *T2 = nullptr, *C64 = nullptr, *V = nullptr;
+    unsigned long long* err = nullptr;   // [nu + nv + nw spans] + max, then esq, range
+    void release(cudaStream_t st) {
+        for (void* p : {(void*)Q64, (void*)T1, (void*)T2, (void*)C64, (void*)V, (void*)err})
+            if (p) cudaFreeAsync(p, st);
+        Q64 = T1 = T2 = C64 = V = nullptr;
+        err = nullptr;
+    }
+};
+
+static mfa_status check_grid(const int64_t dims[3], const float* values, int p, const int64_t nctrl[3]) {
+    if (!dims || !values || !nctrl) return fail(MFA_ERR_INVALID_ARG, "NULL argument");
+    if (p < 1 || p > MFA_MAX_DEGREE) return fail(MFA_ERR_UNSUPPORTED, "degree outside 1..5");
+    for (int d = 0; d < 3; ++d) {
+        if (dims[d] < 2 || dims[d] > (1 << 20)) return fail(MFA_ERR_INVALID_ARG, "dims[d] must be in [2, 2^20]");
+        if (nctrl[d] < p + 1) return fail(MFA_ERR_INVALID_ARG, "nctrl[d] < degree + 1");
+        if (nctrl[d] > dims[d]) return fail(MFA_ERR_INVALID_ARG, "nctrl[d] > dims[d]: the fit would be singular");
+    }
+    return MFA_OK;
+}
+
+}  // namespace mfa
+
+using namespace mfa;
+
+extern "C" mfa_status mfa_fit_grid(const int64_t dims[3], const float* values, int32_t degree, const int64_t nctrl[3],
+                                   const double* const knots[3], float* ctrl_out, double* ctrl_out64,
+                                   mfa_stream stream) {
+    mfa_status s = check_grid(dims, values, degree, nctrl);
+    if (s != MFA_OK) return s;
+    if (!knots || !ctrl_out) return fail(MFA_ERR_INVALID_ARG, "knots and ctrl_out are required");
+    const int p = degree;
+    AxisFit A[3];
+    for (int d = 0; d < 3; ++d) {
+        int uni = 0;
+        if (!knots[d]) return fail(MFA_ERR_INVALID_ARG, "knots[d] is NULL");
+        if ((s = validate_knots(d, p, nctrl[d], knots[d], &uni)) != MFA_OK) return s;
+        if ((s = build_axis(d, (int)dims[d], (int)nctrl[d], p, knots[d], A[d])) != MFA_OK) return s;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    keep_pool();
+    AxisDevMem D[3];
+    FitScratch W;
+    auto done = [&](mfa_status r) {
+        cudaStreamSynchronize(st);
+        for (auto& x : D) x.release(st);
+        W.release(st);
+        return r;
+    };
+    cudaError_t e;
+    for (int d = 0; d < 3; ++d)
+        if ((e = upload_axis(A[d], D[d], st)) != cudaSuccess) return done(cuda_fail(e, "fit tables"));
+    const int64_t mu = dims[0], mv = dims[1], mw = dims[2], nu = nctrl[0], nv = nctrl[1], nw = nctrl[2];
+    if ((e = cudaMallocAsync(&W.Q64, sizeof(double) * mw * mv * mu, st)) != cudaSuccess) return done(cuda_fail(e, "fit scratch"));
+    f32_to_f64_kernel<<<grid_for(mw * mv * mu), 128, 0, st>>>(values, W.Q64, mw * mv * mu);
+    if ((e = cudaMallocAsync(&W.T1, sizeof(double) * nw * mv * mu, st)) != cudaSuccess) return done(cuda_fail(e, "fit scratch"));
+    if ((e = cudaMallocAsync(&W.T2, sizeof(double) * nw * nv * mu, st)) != cudaSuccess) return done(cuda_fail(e, "fit scratch"));
+    double* c64 = ctrl_out64;
+    if (!c64) {
+        if ((e = cudaMallocAsync(&W.C64, sizeof(double) * nw * nv * nu, st)) != cudaSuccess) return done(cuda_fail(e, "fit scratch"));
+        c64 = W.C64;
+    }
+    const AxisFitDev ax[3] = {D[0].d, D[1].d, D[2].d};
+    return done(fit_all(W.Q64, ax, W.T1, W.T2, ctrl_out, c64, st));
+}
+
+extern "C" mfa_status mfa_encode_grid(const int64_t dims[3], const float* values, const mfa_encode_config* cfg,
+                                      double* const knots_out[3], float* ctrl_out, mfa_encode_result* res,
+                                      double* round_log, mfa_stream stream) {
+    if (!cfg || !knots_out || !ctrl_out || !res) return fail(MFA_ERR_INVALID_ARG, "NULL argument");
+    const int p = cfg->degree;
+    mfa_status s = check_grid(dims, values, p, cfg->nctrl_init);
+    if (s != MFA_OK) return s;
+    for (int d = 0; d < 3; ++d) {
+        if (!knots_out[d]) return fail(MFA_ERR_INVALID_ARG, "knots_out[d] is NULL");
+        if (cfg->max_ctrl[d] < cfg->nctrl_init[d]) return fail(MFA_ERR_INVALID_ARG, "max_ctrl[d] < nctrl_init[d]");
+    }
+    if (!(cfg->e_max >= 0.0) || cfg->max_rounds < 0) return fail(MFA_ERR_INVALID_ARG, "e_max >= 0, max_rounds >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t mu = dims[0], mv = dims[1], mw = dims[2], npts = mu * mv * mw;
+    int64_t cap[3];
+    for (int d = 0; d < 3; ++d) cap[d] = std::min<int64_t>(cfg->max_ctrl[d], dims[d]);
+    // initial knots: clamped uniform with nctrl_init control points (R-28)
+    std::vector<double> U[3];
+    for (int d = 0; d < 3; ++d) {
+        const int64_t n = cfg->nctrl_init[d], S = n - p;
+        U[d].assign(p + 1, 0.0);
+        for (int64_t k = 1; k < S; ++k) U[d].push_back((double)k / (double)S);
+        U[d].insert(U[d].end(), p + 1, 1.0);
+    }
+    keep_pool();
+    FitScratch W;
+    AxisDevMem D[3];
+    double* rng_dev = nullptr;
+    auto done = [&](mfa_status r) {
+        cudaStreamSynchronize(st);
+        for (auto& x : D) x.release(st);
+        W.release(st);
+        if (rng_dev) cudaFreeAsync(rng_dev, st);
+        return r;
+    };
+    cudaError_t e;
+    const int64_t maxT1 = cap[2] * mv * mu, maxT2 = std::max(cap[2] * cap[1] * mu, cap[2] * mv * mu);
+    if ((e = cudaMallocAsync(&W.T1, sizeof(double) * std::max(maxT1, cap[2] * cap[1] * mu), st)) != cudaSuccess)
+        return done(cuda_fail(e, "encode scratch"));
+    if ((e = cudaMallocAsync(&W.T2, sizeof(double) * std::max(maxT2, mw * mv * mu), st)) != cudaSuccess)
+        return done(cuda_fail(e, "encode scratch"));
+    if ((e = cudaMallocAsync(&W.C64, sizeof(double) * cap[0] * cap[1] * cap[2], st)) != cudaSuccess)
+        return done(cuda_fail(e, "encode scratch"));
+    if ((e = cudaMallocAsync(&W.V, sizeof(double) * npts, st)) != cudaSuccess) return done(cuda_fail(e, "encode scratch"));
+    if ((e = cudaMallocAsync(&W.Q64, sizeof(double) * npts, st)) != cudaSuccess) return done(cuda_fail(e, "encode scratch"));
+    f32_to_f64_kernel<<<grid_for(npts), 128, 0, st>>>(values, W.Q64, npts);
+    const int64_t nerr = cap[0] + cap[1] + cap[2] + 2;
+    if ((e = cudaMallocAsync(&W.err, sizeof(unsigned long long) * nerr, st)) != cudaSuccess)
+        return done(cuda_fail(e, "encode scratch"));
+    if ((e = cudaMallocAsync(&rng_dev, 2 * sizeof(double), st)) != cudaSuccess) return done(cuda_fail(e, "encode scratch"));
+    unsigned long long rinit[2] = {~0ULL, 0ULL};
+    cudaMemcpyAsync(rng_dev, rinit, sizeof(rinit), cudaMemcpyHostToDevice, st);
+    range_kernel<<<grid_for(npts), 128, 0, st>>>(values, npts, rng_dev);
+    unsigned long long rb[2];
+    cudaMemcpyAsync(rb, rng_dev, sizeof(rb), cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return done(cuda_fail(e, "encode range"));
+    const double range = ord_to_double(rb[1]) - ord_to_double(rb[0]);
+    const double inv_range = range > 0.0 ? 1.0 / range : 1.0;
+
+    int rounds = 0;
+    bool converged = false;
+    double max_err = 0.0, rms = 0.0;
+    for (;;) {
+        AxisFit A[3];
+        int64_t n[3];
+        for (int d = 0; d < 3; ++d) {
+            n[d] = (int64_t)U[d].size() - p - 1;
+            if ((s = build_axis(d, (int)dims[d], (int)n[d], p, U[d].data(), A[d])) != MFA_OK) return done(s);
+            D[d].release(st);
+            if ((e = upload_axis(A[d], D[d], st)) != cudaSuccess) return done(cuda_fail(e, "encode tables"));
+        }
+        const AxisFitDev ax[3] = {D[0].d, D[1].d, D[2].d};
+        if ((s = fit_all(W.Q64, ax, W.T1, W.T2, ctrl_out, W.C64, st)) != MFA_OK) return done(s);
+        if ((e = expand_all(p, W.C64, ax, W.T1, W.T2, W.V, st)) != cudaSuccess) return done(cuda_fail(e, "expand"));
+        const int64_t S0 = n[0] - p, S1 = n[1] - p, S2 = n[2] - p;
+        cudaMemsetAsync(W.err, 0, sizeof(unsigned long long) * nerr, st);
+        unsigned long long *eu = W.err, *ev = eu + S0, *ew = ev + S1, *emax = ew + S2;
+        double* esq = reinterpret_cast<double*>(emax + 1);
+        grid_error_kernel<<<grid_for(npts), 128, 0, st>>>(W.V, values, (int)mu, (int)mv, (int)mw, inv_range, ax[0].f,
+                                                           ax[1].f, ax[2].f, eu, ev, ew, emax, esq);
+        std::vector<unsigned long long> h(S0 + S1 + S2 + 2);
+        cudaMemcpyAsync(h.data(), W.err, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st);
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return done(cuda_fail(e, "encode residual"));
+        auto dv = [](unsigned long long b) {
+            double x;
+            memcpy(&x, &b, 8);
+            return x;
+        };
+        max_err = dv(h[S0 + S1 + S2]);
+        double sq;
+        memcpy(&sq, &h[S0 + S1 + S2 + 1], 8);
+        rms = sqrt(sq / (double)npts);
+        if (round_log) {
+            double* r = round_log + 5 * rounds;
+            r[0] = (double)n[0];
+            r[1] = (double)n[1];
+            r[2] = (double)n[2];
+            r[3] = max_err;
+            r[4] = rms;
+        }
+        ++rounds;
+        for (int d = 0; d < 3; ++d) res->nctrl[d] = n[d];
+        if (max_err <= cfg->e_max) {
+            converged = true;
+            break;
+        }
+        if (rounds > cfg->max_rounds) break;
+        // split every offending span holding >= 2 samples at its midpoint, within the caps
+        bool split_any = false;
+        const unsigned long long* hs[3] = {h.data(), h.data() + S0, h.data() + S0 + S1};
+        for (int d = 0; d < 3; ++d) {
+            const int64_t Sd = n[d] - p;
+            std::vector<int> cnt(Sd, 0);
+            for (int j = 0; j < A[d].m; ++j) cnt[A[d].f[j]]++;
+            std::vector<double> ins;
+            for (int64_t sp = 0; sp < Sd; ++sp)
+                if (dv(hs[d][sp]) > cfg->e_max && cnt[sp] >= 2 * (p + 1) && n[d] + (int64_t)ins.size() < cap[d])
+                    ins.push_back(0.5 * (U[d][p + sp] + U[d][p + sp + 1]));
+            if (!ins.empty()) {
+                split_any = true;
+                U[d].insert(U[d].end(), ins.begin(), ins.end());
+                std::sort(U[d].begin(), U[d].end());
+            }
+        }
+        if (!split_any) break;
+    }
+    for (int d = 0; d < 3; ++d) std::copy(U[d].begin(), U[d].end(), knots_out[d]);
+    res->rounds = rounds;
+    res->converged = converged ? 1 : 0;
+    res->max_err = max_err;
+    res->rms_err = rms;
+    return done(MFA_OK);
+}

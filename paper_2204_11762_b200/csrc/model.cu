@@ -119,41 +119,6 @@ __global__ void minmax_kernel(const float* __restrict__ P, int64_t n, unsigned i
 //                    + (U_{j+k+1}-u)/(U_{j+k+1}-U_{j+1}) N_{j+1,k-1}
 // applied to polynomials in t (u = U_i + h t), in fp64.
 // ---------------------------------------------------------------------------
-// Power-basis coefficients of the p+1 non-zero basis functions on knot span
-// i (local t = (u - U_i)/h, u = U_i + h t): P[r][m] = coefficient of t^m of
-// N_{i-p+r,p}.  Cox-de Boor recursion on polynomials in t, fp64.
-__device__ void span_poly(const double* __restrict__ U, int p, int i, double (&P)[kMaxP + 1][kMaxP + 1]) {
-    const double Ui = U[i], h = U[i + 1] - U[i];
-    double Nx[kMaxP + 1][kMaxP + 1];
-    for (int r = 0; r <= kMaxP; ++r)
-        for (int m = 0; m <= kMaxP; ++m) P[r][m] = 0.0;
-    P[0][0] = 1.0;  // level 0: N_{i,0} = 1 on the span
-    for (int k = 1; k <= p; ++k) {
-        for (int r = 0; r <= k; ++r) {
-            for (int m = 0; m <= kMaxP; ++m) Nx[r][m] = 0.0;
-            const int j = i - k + r;
-            if (r >= 1) {  // (u - U_j)/(U_{j+k} - U_j) * N_{j,k-1}; N_{j,k-1} is old function r-1
-                const double den = U[j + k] - U[j];
-                const double c0 = (Ui - U[j]) / den, c1 = h / den;
-                for (int m = 0; m < k; ++m) {
-                    Nx[r][m] += c0 * P[r - 1][m];
-                    Nx[r][m + 1] += c1 * P[r - 1][m];
-                }
-            }
-            if (r <= k - 1) {  // (U_{j+k+1} - u)/(U_{j+k+1} - U_{j+1}) * N_{j+1,k-1}; old function r
-                const double den = U[j + k + 1] - U[j + 1];
-                const double c0 = (U[j + k + 1] - Ui) / den, c1 = -h / den;
-                for (int m = 0; m < k; ++m) {
-                    Nx[r][m] += c0 * P[r][m];
-                    Nx[r][m + 1] += c1 * P[r][m];
-                }
-            }
-        }
-        for (int r = 0; r <= k; ++r)
-            for (int m = 0; m <= kMaxP; ++m) P[r][m] = Nx[r][m];
-    }
-}
-
 __global__ void span_tables_kernel(const double* __restrict__ U, int p, int nsp, int rec,
                                    float* __restrict__ coef, float* __restrict__ invh) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -306,7 +271,7 @@ extern "C" const char* mfa_last_error(void) { return g_err.c_str(); }
 
 extern "C" const char* mfa_version(void) { return "mfa-b200 0.1 sm_100a"; }
 
-static mfa_status validate_knots(int d, int p, int64_t n, const double* U, int* uniform) {
+mfa_status mfa::validate_knots(int d, int p, int64_t n, const double* U, int* uniform) {
     const char* ax = d == 0 ? "u" : (d == 1 ? "v" : "w");
     const int64_t len = n + p + 1;
     for (int64_t i = 0; i < len; ++i)
