@@ -403,6 +403,18 @@ def secondary_kernels(w, m, c, p, img, tf, stream):
 
     from paper_2204_11762_b200 import image_quality, roofline as RL, workloads as WL
     res = {}
+    # mfa_eval_batch on BASELINE.json's eval workload: C3 (256^3, p = 3) at 2^24 random points
+    from paper_2204_11762_b200 import Model
+    w3 = WL.make_config(3, width=16, height=16)
+    m3 = Model.from_workload(w3)
+    u, v_, w_ = (torch.from_numpy(x).cuda() for x in WL.query_points(3, 1 << 24))
+    outs = m3.eval(u, v_, w_)
+    ms = _time(lambda: m3.eval(u, v_, w_, out=outs), 5, stream)
+    fe = RL.flops_per_eval_point(3)
+    res["eval_c3"] = {"points_per_s": (1 << 24) / (ms / 1e3), "ms": ms, "points": 1 << 24, "layout": m3.info()["layout"],
+                      "flops_per_point": fe, "achieved_tflops": fe * (1 << 24) / (ms / 1e3) / 1e12,
+                      "hbm_io_bytes_per_point": 28}
+    del m3, outs
     u, v_, w_ = (torch.from_numpy(x).cuda() for x in WL.query_points(c, 1 << 24))
     ms = _time(lambda: m.eval_hessian(u, v_, w_), 3, stream)
     fh = RL.flops_per_hessian_point(p)

@@ -136,6 +136,23 @@ mfa_status mfa_eval_batch(mfa_model m, int64_t n, const float* u, const float* v
                           float* value, float* du, float* dv, float* dw,
                           unsigned long long* n_domain_errors, mfa_stream stream);
 
+/*
+ * mfa_eval_batch_ws -- mfa_eval_batch with a caller-owned device workspace of
+ * at least mfa_eval_workspace_bytes(m, n) bytes (~20 B per point).  For
+ * n >= 2^16 the points are first grouped by a coarse parameter-space bin
+ * (~16^3 knot spans per bin; a counting sort into (u, v, w, index) records)
+ * and evaluated in bin order, results written at their original indices:
+ * neighbouring points then share control-point neighbourhoods in L1/L2
+ * instead of each pulling ~16 separate lines from HBM.  Same outputs as
+ * mfa_eval_batch (each point's arithmetic is unchanged); workspace == NULL is
+ * mfa_eval_batch.
+ */
+size_t mfa_eval_workspace_bytes(mfa_model m, int64_t n);
+mfa_status mfa_eval_batch_ws(mfa_model m, int64_t n, const float* u, const float* v, const float* w,
+                             float* value, float* du, float* dv, float* dw,
+                             unsigned long long* n_domain_errors, void* workspace, size_t workspace_bytes,
+                             mfa_stream stream);
+
 /* ------------------------------------------------------------------------
  * mfa_eval_hessian -- value, gradient and the six second partials of the MFA
  * at n points ("Higher-order derivatives, up to the

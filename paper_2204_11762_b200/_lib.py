@@ -24,7 +24,7 @@ LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2}
 EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
            "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version",
            "mfa_render_field", "mfa_image_quality", "mfa_image_quality_workspace", "mfa_eval_hessian",
-           "mfa_fit_grid", "mfa_encode_grid",
+           "mfa_fit_grid", "mfa_encode_grid", "mfa_eval_batch_ws", "mfa_eval_workspace_bytes",
            "mfa_probe_fp32", "mfa_probe_read_bw")
 
 
@@ -104,6 +104,10 @@ def lib():
         L.mfa_model_destroy.argtypes = [vp]
         L.mfa_eval_batch.restype = C.c_int
         L.mfa_eval_batch.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.mfa_eval_workspace_bytes.restype = C.c_size_t
+        L.mfa_eval_workspace_bytes.argtypes = [vp, i64]
+        L.mfa_eval_batch_ws.restype = C.c_int
+        L.mfa_eval_batch_ws.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
         L.mfa_eval_hessian.restype = C.c_int
         L.mfa_eval_hessian.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
         L.mfa_render.restype = C.c_int
@@ -249,9 +253,11 @@ class Model:
             pass
 
     # -- queryValueMFA / queryGradientMFA (mfa_eval_batch) --------------------
-    def eval(self, u, v, w, grad=True, out=None, n_domain_errors=None, stream=None):
+    def eval(self, u, v, w, grad=True, out=None, n_domain_errors=None, stream=None, binned=True):
         """u, v, w: CUDA fp32 tensors (n,).  Returns (value, du, dv, dw)
-        (parameter-space partials), or (value,) if grad is False."""
+        (parameter-space partials), or (value,) if grad is False.  binned:
+        large batches go through mfa_eval_batch_ws (spatial binning, a
+        workspace from torch's allocator)."""
         import torch
         n = u.numel()
         dev = u.device
@@ -259,8 +265,14 @@ class Model:
             out = tuple(torch.empty(n, device=dev, dtype=torch.float32) for _ in range(4 if grad else 1))
         val = out[0]
         du, dv, dw = (out[1], out[2], out[3]) if grad else (None, None, None)
-        _check(lib().mfa_eval_batch(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(du), _ptr(dv),
-                                    _ptr(dw), _ptr(n_domain_errors), _stream_ptr(stream)))
+        if binned and n >= (1 << 16):
+            nb = int(lib().mfa_eval_workspace_bytes(self._h, n))
+            ws = torch.empty(nb, dtype=torch.uint8, device=dev)   # stream-ordered by torch's allocator
+            _check(lib().mfa_eval_batch_ws(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(du), _ptr(dv),
+                                           _ptr(dw), _ptr(n_domain_errors), _ptr(ws), nb, _stream_ptr(stream)))
+        else:
+            _check(lib().mfa_eval_batch(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(du), _ptr(dv),
+                                        _ptr(dw), _ptr(n_domain_errors), _stream_ptr(stream)))
         return out
 
     def eval_hessian(self, u, v, w, n_domain_errors=None, stream=None):

@@ -21,23 +21,47 @@ struct EvalArgs {
     float* dw;
     unsigned long long* n_err;
     int64_t n;
+    const float4* rec;     // SORTED: points as (u, v, w, index bits), grouped by spatial bin
+    float4* out4;          // SORTED: (value, du, dv, dw) at the sorted position (in place over rec)
+    const int* pos;        // SORTED: sorted position of point i
 };
 
-template <int P, int LAYOUT, bool UNI, bool GRAD>
+template <int P, int LAYOUT, bool UNI, bool GRAD, bool SORTED>
 __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalArgs args) {
     constexpr bool BEZ = LAYOUT == kBezier;
     unsigned errs = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < args.n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const float q[3] = {__ldg(args.u + i), __ldg(args.v + i), __ldg(args.w + i)};
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < args.n;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = it;
+        float q[3];
+        if constexpr (SORTED) {   // consecutive threads hold spatially close points
+            const float4 r = __ldg(args.rec + it);
+            q[0] = r.x;
+            q[1] = r.y;
+            q[2] = r.z;
+            i = (int64_t)(unsigned)__float_as_int(r.w);
+        } else {
+            q[0] = __ldg(args.u + i);
+            q[1] = __ldg(args.v + i);
+            q[2] = __ldg(args.w + i);
+        }
+        // direct: SoA outputs at i; SORTED: one coalesced float4 at the sorted position
+        auto store = [&](float val, float gu, float gv, float gw) {
+            if constexpr (SORTED) {
+                args.out4[it] = make_float4(val, gu, gv, gw);
+            } else {
+                args.value[i] = val;
+                if (GRAD) {
+                    args.du[i] = gu;
+                    args.dv[i] = gv;
+                    args.dw[i] = gw;
+                }
+            }
+        };
         if (!(q[0] >= 0.f && q[0] <= 1.f && q[1] >= 0.f && q[1] <= 1.f && q[2] >= 0.f && q[2] <= 1.f)) {
             ++errs;
-            args.value[i] = __int_as_float(0x7fc00000);
-            if (GRAD) {
-                args.du[i] = __int_as_float(0x7fc00000);
-                args.dv[i] = __int_as_float(0x7fc00000);
-                args.dw[i] = __int_as_float(0x7fc00000);
-            }
+            const float nan = __int_as_float(0x7fc00000);
+            store(nan, nan, nan, nan);
             continue;
         }
         int s[3];
@@ -62,10 +86,7 @@ __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalA
                 bernstein<P, false>(t[2], Bw);
                 float val, gu, gv, gw;
                 contract_vg_bez<P>(base, r0, Bu, Bv, Bw, val, gu, gv, gw);
-                args.value[i] = val;
-                args.du[i] = gu * sc[0];
-                args.dv[i] = gv * sc[1];
-                args.dw[i] = gw * sc[2];
+                store(val, gu * sc[0], gv * sc[1], gw * sc[2]);
             } else {
                 float nb[P + 1][P + 1][P + 1];
                 load_bblock<P>(base, nb);
@@ -73,7 +94,7 @@ __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalA
                 bernstein_value<P>(t[0], Nu);
                 bernstein_value<P>(t[1], Nv);
                 bernstein_value<P>(t[2], Nw);
-                args.value[i] = contract_v_cached<P>(nb, Nu, Nv, Nw);
+                store(contract_v_cached<P>(nb, Nu, Nv, Nw), 0.f, 0.f, 0.f);
             }
             continue;
         }
@@ -87,16 +108,13 @@ __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalA
             axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
             float val, gu, gv, gw;
             contract_vg<P>(base, r0, Bu, Bv, Bw, val, gu, gv, gw);
-            args.value[i] = val;
-            args.du[i] = gu * sc[0];
-            args.dv[i] = gv * sc[1];
-            args.dw[i] = gw * sc[2];
+            store(val, gu * sc[0], gv * sc[1], gw * sc[2]);
         } else {
             float Nu[P + 1], Nv[P + 1], Nw[P + 1];
             axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
             axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
             axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
-            args.value[i] = contract_v<P>(base, r0, Nu, Nv, Nw);
+            store(contract_v<P>(base, r0, Nu, Nv, Nw), 0.f, 0.f, 0.f);
         }
     }
     if (args.n_err) {
@@ -105,15 +123,21 @@ __global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalA
     }
 }
 
-template <int P, int LAYOUT, bool UNI, bool GRAD>
-static cudaError_t launch_eval_t(const EvalArgs& a, cudaStream_t st) {
+template <int P, int LAYOUT, bool UNI, bool GRAD, bool SORTED>
+static cudaError_t launch_eval_s(const EvalArgs& a, cudaStream_t st) {
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t want = (a.n + 255) / 256;
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * 16);
-    eval_kernel<P, LAYOUT, UNI, GRAD><<<(unsigned)grid, 256, 0, st>>>(a);
+    eval_kernel<P, LAYOUT, UNI, GRAD, SORTED><<<(unsigned)grid, 256, 0, st>>>(a);
     return cudaGetLastError();
+}
+
+template <int P, int LAYOUT, bool UNI, bool GRAD>
+static cudaError_t launch_eval_t(const EvalArgs& a, cudaStream_t st) {
+    if (a.rec) return launch_eval_s<P, LAYOUT, UNI, GRAD, true>(a, st);
+    return launch_eval_s<P, LAYOUT, UNI, GRAD, false>(a, st);
 }
 
 template <int P, int LAYOUT>
@@ -131,9 +155,155 @@ static cudaError_t dispatch_eval(const EvalArgs& a, int layout, bool uni, bool g
     return dispatch_eval_l<P, kQuads>(a, uni, grad, st);
 }
 
+// ---------------------------------------------------------------------------
+// Spatial binning of a large point batch (mfa_eval_batch with a workspace).
+// Random points gather their (p+1)^3 neighbourhoods from random places: each
+// point touches ~16 separate 128-byte lines of a grid far larger than L2, so
+// the kernel is HBM-bound on over-fetched lines (C3: ~1.5 KB of DRAM reads per
+// point).  Grouping the points by a coarse parameter-space bin (about 16^3
+// knot spans per bin; bin = floor(u * NB) per axis) makes the points a CTA
+// processes share neighbourhoods, which then come from L1/L2: a counting sort
+// (per-CTA shared-memory histogram, one scan, an atomic-cursor scatter of
+// (u, v, w, index) records), then the evaluation in bin order writing each
+// result at its original index.  The result of a point does not depend on
+// its position in the order, so outputs stay deterministic.
+// ---------------------------------------------------------------------------
+struct BinGrid {
+    int nb[3];
+    int nbins;   // nb0 * nb1 * nb2; points outside [0,1]^3 (or NaN) go to bin nbins
+};
+
+__device__ __forceinline__ int point_bin(const BinGrid& g, float u, float v, float w) {
+    if (!(u >= 0.f && u <= 1.f && v >= 0.f && v <= 1.f && w >= 0.f && w <= 1.f)) return g.nbins;
+    const int bu = min((int)(u * (float)g.nb[0]), g.nb[0] - 1);
+    const int bv = min((int)(v * (float)g.nb[1]), g.nb[1] - 1);
+    const int bw = min((int)(w * (float)g.nb[2]), g.nb[2] - 1);
+    return (bw * g.nb[1] + bv) * g.nb[0] + bu;
+}
+
+constexpr int kBinSmem = 12288;   // bins counted in shared memory (48 KB)
+
+__global__ void __launch_bounds__(256) bin_count_kernel(const float* __restrict__ u, const float* __restrict__ v,
+                                                        const float* __restrict__ w, int64_t n, const BinGrid g,
+                                                        int* __restrict__ bins, unsigned* __restrict__ counts) {
+    extern __shared__ unsigned sh[];
+    const bool local = g.nbins + 1 <= kBinSmem;
+    if (local)
+        for (int b = threadIdx.x; b <= g.nbins; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int b = point_bin(g, __ldg(u + i), __ldg(v + i), __ldg(w + i));
+        bins[i] = b;
+        if (local) atomicAdd(sh + b, 1u);
+        else atomicAdd(counts + b, 1u);
+    }
+    __syncthreads();
+    if (local)
+        for (int b = threadIdx.x; b <= g.nbins; b += blockDim.x)
+            if (sh[b]) atomicAdd(counts + b, sh[b]);
+}
+
+// exclusive scan of nbins+1 counts into cursors (one CTA of 1024 threads)
+__global__ void __launch_bounds__(1024) bin_scan_kernel(const unsigned* __restrict__ counts, int nb,
+                                                        unsigned* __restrict__ cursor) {
+    __shared__ unsigned part[1024];
+    const int per = (nb + 1023) / 1024;
+    const int b0 = threadIdx.x * per, b1 = min(b0 + per, nb);
+    unsigned s = 0;
+    for (int b = b0; b < b1; ++b) s += counts[b];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {   // Hillis-Steele inclusive scan
+        const unsigned x = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += x;
+        __syncthreads();
+    }
+    unsigned run = part[threadIdx.x] - s;
+    for (int b = b0; b < b1; ++b) {
+        cursor[b] = run;
+        run += counts[b];
+    }
+}
+
+// bins[i] is replaced by the point's sorted position (for the gather back)
+__global__ void __launch_bounds__(256) bin_scatter_kernel(const float* __restrict__ u, const float* __restrict__ v,
+                                                          const float* __restrict__ w, int64_t n,
+                                                          int* __restrict__ bins, unsigned* __restrict__ cursor,
+                                                          float4* __restrict__ rec) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned pos = atomicAdd(cursor + bins[i], 1u);
+        rec[pos] = make_float4(__ldg(u + i), __ldg(v + i), __ldg(w + i), __int_as_float((int)i));
+        bins[i] = (int)pos;
+    }
+}
+
+// results back to the caller's SoA arrays: coalesced writes at i, one 16-byte
+// gather from the sorted position
+__global__ void __launch_bounds__(256) bin_gather_kernel(const float4* __restrict__ out4, const int* __restrict__ pos,
+                                                         int64_t n, float* __restrict__ value, float* __restrict__ du,
+                                                         float* __restrict__ dv, float* __restrict__ dw) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 r = __ldg(out4 + __ldg(pos + i));
+        value[i] = r.x;
+        if (du) {
+            du[i] = r.y;
+            dv[i] = r.z;
+            dw[i] = r.w;
+        }
+    }
+}
+
+static BinGrid make_bins(const Model* m) {
+    BinGrid g;
+    int64_t total = 1;
+    for (int d = 0; d < 3; ++d) {
+        const int64_t S = m->n[d] - m->p;
+        g.nb[d] = (int)std::max<int64_t>(1, (S + 15) / 16);
+        total *= g.nb[d];
+    }
+    while (total > (1 << 22)) {   // keep the bin table small
+        for (int d = 0; d < 3; ++d) g.nb[d] = std::max(1, g.nb[d] / 2);
+        total = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
+    }
+    g.nbins = (int)total;
+    return g;
+}
+
+size_t eval_workspace_bytes(const Model* m, int64_t n) {
+    const BinGrid g = make_bins(m);
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    return up(sizeof(int) * (size_t)n) + up(sizeof(float4) * (size_t)n) + 2 * up(sizeof(unsigned) * (g.nbins + 1));
+}
+
 mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v, const float* w, float* value,
-                       float* du, float* dv, float* dw, unsigned long long* n_err, cudaStream_t st) {
+                       float* du, float* dv, float* dw, unsigned long long* n_err, cudaStream_t st, void* ws,
+                       size_t ws_bytes) {
     EvalArgs a;
+    a.rec = nullptr;
+    a.out4 = nullptr;
+    a.pos = nullptr;
+    if (ws && n >= (int64_t)1 << 16 && n < ((int64_t)1 << 31) && ws_bytes >= eval_workspace_bytes(m, n)) {
+        const BinGrid g = make_bins(m);
+        auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+        char* b = (char*)ws;
+        int* bins = (int*)b;
+        float4* rec = (float4*)(b + up(sizeof(int) * (size_t)n));
+        unsigned* counts = (unsigned*)(b + up(sizeof(int) * (size_t)n) + up(sizeof(float4) * (size_t)n));
+        unsigned* cursor = (unsigned*)((char*)counts + up(sizeof(unsigned) * (g.nbins + 1)));
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+        cudaMemsetAsync(counts, 0, sizeof(unsigned) * (g.nbins + 1), st);
+        const size_t smem = g.nbins + 1 <= kBinSmem ? sizeof(unsigned) * (g.nbins + 1) : 0;
+        bin_count_kernel<<<grid, 256, smem, st>>>(u, v, w, n, g, bins, counts);
+        bin_scan_kernel<<<1, 1024, 0, st>>>(counts, g.nbins + 1, cursor);
+        bin_scatter_kernel<<<grid, 256, 0, st>>>(u, v, w, n, bins, cursor, rec);
+        a.rec = rec;
+        a.out4 = rec;
+        a.pos = bins;
+    }
     a.Q = m->Q;
     a.g.nbx = m->nb[0];
     a.g.nby = m->nb[1];
@@ -160,6 +330,14 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
         case 3: e = dispatch_eval<3>(a, m->layout, uni, grad, st); break;
         case 4: e = dispatch_eval<4>(a, m->layout, uni, grad, st); break;
         default: e = dispatch_eval<5>(a, m->layout, uni, grad, st); break;
+    }
+    if (e == cudaSuccess && a.rec) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+        bin_gather_kernel<<<grid, 256, 0, st>>>(a.out4, a.pos, n, value, du, dv, dw);
+        e = cudaGetLastError();
     }
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "eval launch");
 }

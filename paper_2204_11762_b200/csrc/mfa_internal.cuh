@@ -137,7 +137,8 @@ mfa_status validate_knots(int d, int p, int64_t n, const double* U, int* uniform
 // kernel launchers (defined in eval.cu / render.cu)
 mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v, const float* w,
                        float* value, float* du, float* dv, float* dw,
-                       unsigned long long* n_err, cudaStream_t st);
+                       unsigned long long* n_err, cudaStream_t st, void* ws = nullptr, size_t ws_bytes = 0);
+size_t eval_workspace_bytes(const Model* m, int64_t n);
 mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                          const mfa_render_params* prm, const mfa_tiles* tiles, void* out,
                          unsigned long long* samples, cudaStream_t st, const mfa_field* fld = nullptr);

@@ -561,6 +561,30 @@ extern "C" mfa_status mfa_eval_batch(mfa_model h, int64_t n, const float* u, con
     return launch_eval(m, n, u, v, w, value, du, dv, dw, n_domain_errors, (cudaStream_t)stream);
 }
 
+extern "C" size_t mfa_eval_workspace_bytes(mfa_model h, int64_t n) {
+    if (!h || n < 0) return 0;
+    return eval_workspace_bytes(reinterpret_cast<const Model*>(h), n);
+}
+
+extern "C" mfa_status mfa_eval_batch_ws(mfa_model h, int64_t n, const float* u, const float* v, const float* w,
+                                        float* value, float* du, float* dv, float* dw,
+                                        unsigned long long* n_domain_errors, void* workspace,
+                                        size_t workspace_bytes, mfa_stream stream) {
+    if (!h) return fail(MFA_ERR_INVALID_ARG, "model is NULL");
+    if (n < 0) return fail(MFA_ERR_INVALID_ARG, "n < 0");
+    if (n == 0) return MFA_OK;
+    if (!u || !v || !w || !value) return fail(MFA_ERR_INVALID_ARG, "u, v, w and value are required");
+    const int ng = (du != nullptr) + (dv != nullptr) + (dw != nullptr);
+    if (ng != 0 && ng != 3) return fail(MFA_ERR_INVALID_ARG, "du, dv, dw must be all NULL or all non-NULL");
+    const Model* m = reinterpret_cast<const Model*>(h);
+    if (workspace && workspace_bytes < eval_workspace_bytes(m, n))
+        return fail(MFA_ERR_INVALID_ARG, "workspace smaller than mfa_eval_workspace_bytes()");
+    mfa_status s = check_device(m);
+    if (s != MFA_OK) return s;
+    return launch_eval(m, n, u, v, w, value, du, dv, dw, n_domain_errors, (cudaStream_t)stream, workspace,
+                       workspace_bytes);
+}
+
 static mfa_status validate_render(const Model* m, int32_t n_views, const mfa_camera* cams,
                                   const mfa_render_params* prm) {
     if (n_views < 1) return fail(MFA_ERR_INVALID_ARG, "n_views < 1");

@@ -58,6 +58,26 @@ def test_eval_parity(c):
     print(f"C{c}: n={len(u)} worst value {wv:.2e} sigma, worst gradient {wg:.2e} sigma")
 
 
+@pytest.mark.parametrize("c,layout", [(3, "auto"), (5, "auto"), (5, "quads"), (2, "auto")])
+def test_eval_binned_equals_direct(c, layout):
+    """mfa_eval_batch_ws (spatially binned order) returns exactly the outputs
+    of mfa_eval_batch, including NaN rows and the domain-error count for
+    points outside [0,1]^3."""
+    m = gpu_model(c, layout)
+    u, v, w = WL.query_points(c, 1 << 18)
+    u = u.copy()
+    u[[5, 77, 1000]] = [1.5, np.nan, -0.25]
+    cu, cv, cw = cuda(u), cuda(v), cuda(w)
+    outs = []
+    for binned in (True, False):
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        r = m.eval(cu, cv, cw, n_domain_errors=cnt, binned=binned)
+        torch.cuda.synchronize()
+        outs.append((np.stack([t.cpu().numpy() for t in r], axis=1), int(cnt.item())))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1] == 3
+
+
 def test_eval_value_only_matches():
     c = 2
     u, v, w = WL.query_points(c, 1 << 14)
