@@ -170,6 +170,15 @@ mfa_status mfa_eval_hessian(mfa_model m, int64_t n, const float* u, const float*
                             float* value, float* grad, float* hess,
                             unsigned long long* n_domain_errors, mfa_stream stream);
 
+/* mfa_eval_hessian with a caller-owned workspace of at least
+ * mfa_hessian_workspace_bytes(m, n) bytes (~68 B per point): large batches are
+ * spatially binned first (as mfa_eval_batch_ws); identical outputs. */
+size_t mfa_hessian_workspace_bytes(mfa_model m, int64_t n);
+mfa_status mfa_eval_hessian_ws(mfa_model m, int64_t n, const float* u, const float* v, const float* w,
+                               float* value, float* grad, float* hess,
+                               unsigned long long* n_domain_errors, void* workspace, size_t workspace_bytes,
+                               mfa_stream stream);
+
 /* ------------------------------------------------------------------------
  * mfa_render -- Algorithm 1 for every pixel of n_views views.
  *
@@ -287,6 +296,34 @@ typedef struct {
 mfa_status mfa_render_field(mfa_model m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                             const mfa_render_params* prm, const mfa_field* field, const mfa_tiles* tiles,
                             void* rgba_out, unsigned long long* samples_out, mfa_stream stream);
+
+/*
+ * mfa_render_ex -- mfa_render with the extensions, any combination of:
+ *  field        as mfa_render_field (NULL: the MFA query only);
+ *  n_lights     0: the headlight of mfa_render (R-11); 1..MFA_MAX_LIGHTS:
+ *               directional lights ("multiple light sources can
+ *               be added in the future").  light_dir: host fp64
+ *               [n_lights][3] world-space directions TOWARDS each light
+ *               (normalised here); light_intensity: host fp64 [n_lights].
+ *               Phong per light l (R-30): c = clamp(rgb (k_a + k_d sum_l I_l
+ *               max(0, N.L_l)) + k_s sum_l I_l [N.L_l > 0] max(0, R_l.V)^n),
+ *               V = -d, R_l = 2 (N.L_l) N - L_l; zero gradient -> k_a rgb.
+ *               One light L = -d, I = 1 reproduces the headlight.
+ * ext == NULL is mfa_render.  Errors as mfa_render; bad lights ->
+ * MFA_ERR_INVALID_ARG.  The extended kernels are separate instantiations:
+ * mfa_render's hot path carries none of this.
+ */
+#define MFA_MAX_LIGHTS 8
+typedef struct {
+    const mfa_field* field;
+    int32_t n_lights;
+    const double* light_dir;
+    const double* light_intensity;
+} mfa_render_ext;
+
+mfa_status mfa_render_ex(mfa_model m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
+                         const mfa_render_params* prm, const mfa_render_ext* ext, const mfa_tiles* tiles,
+                         void* rgba_out, unsigned long long* samples_out, mfa_stream stream);
 
 /*
  * mfa_image_quality -- MSE, PSNR and SSIM of image a against image b.

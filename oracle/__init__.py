@@ -56,7 +56,8 @@ class OrcParams(C.Structure):
                 ("o_max", C.c_double), ("shading", C.c_int32), ("ka", C.c_double),
                 ("kd", C.c_double), ("ks", C.c_double), ("shininess", C.c_double),
                 ("grad_eps", C.c_double), ("ert_window", C.c_double), ("exit_window", C.c_double),
-                ("sens_weight", C.c_double), ("sens_grad", C.c_double)]
+                ("sens_weight", C.c_double), ("sens_grad", C.c_double), ("n_lights", C.c_int32),
+                ("light_dir", C.POINTER(C.c_double)), ("light_intensity", C.POINTER(C.c_double))]
 
 
 _lib = None
@@ -254,7 +255,7 @@ def field_eval(field, u, v, w):
 
 
 def render(model: Model, cam, tf, v_lo, v_hi, params, pixels=None, nthreads=None,
-           ert_window=1e-4, exit_window=1e-6, sens_weight=1e-3, sens_grad=None, field=None):
+           ert_window=1e-4, exit_window=1e-6, sens_weight=1e-3, sens_grad=None, field=None, lights=None):
     """Render one view (all pixels, or a flat pixel-index list).  field (a
     workloads.AnalyticField) takes the value and/or gradient of each sample
     from the analytic function instead of the MFA (ground truth).
@@ -275,6 +276,12 @@ def render(model: Model, cam, tf, v_lo, v_hi, params, pixels=None, nthreads=None
     p.exit_window = exit_window
     p.sens_weight = sens_weight
     p.sens_grad = (100.0 * params.grad_eps) if sens_grad is None else sens_grad
+    if lights is not None:   # [(direction towards the light (3,), intensity), ...]
+        ld = np.ascontiguousarray([l[0] for l in lights], dtype=np.float64).reshape(-1, 3)
+        li = np.ascontiguousarray([l[1] for l in lights], dtype=np.float64)
+        p.n_lights = len(lights)
+        p.light_dir = _dp(ld)
+        p.light_intensity = _dp(li)
     c = make_camera(cam)
     if pixels is None:
         n = cam.width * cam.height

@@ -24,6 +24,8 @@
  *                        up to the polynomial degree, are also analytically available"
  *   H2 orc_eval_hessian  value, gradient and the 6 second partials as plain
  *                        triple sums                 P:78; SURVEY §8(f) NEXT-4
+ *   L1 (in march)        several directional lights, Phong summed per light
+ *                        P:307 "multiple light sources can be added"; R-30
  *   G1 orc_field_eval    analytic ground truth (Eq. 1 Gaussian beam, Eq. 2
  *                        Marschner-Lobb) with analytic gradient
  *   G2 orc_render_ex     Algorithm 1 with value and/or gradient taken from the
@@ -78,6 +80,9 @@ typedef struct {
     double exit_window;        /* R-19 (ii): L/step - 1/2 this close to an integer -> alternative */
     double sens_weight;        /* R-19 (iii): composited weight above ... */
     double sens_grad;          /*   ... with |g_phys| below this -> shading-sensitive flag */
+    int32_t n_lights;          /* L1: 0 -> the headlight (R-11); else directional lights (R-30) */
+    const double* light_dir;   /*   [n_lights][3] world directions towards each light */
+    const double* light_intensity; /* [n_lights] */
 } orc_params;
 
 /* G1: analytic field (NEXT-2).  kind 1 = Gaussian beam (Eq. 1),  */
@@ -485,6 +490,25 @@ static void march(const orc_ctx* cx, const double o[3], const double d[3], doubl
             gnorm = sqrt(v_dot(g, g));
             if (gnorm <= P->grad_eps) {                      /* zero gradient -> ambient (R-11) */
                 for (int i = 0; i < 3; ++i) c[i] = P->ka * col[i];
+            } else if (P->n_lights > 0) {                   /* L1: directional lights (R-30) */
+                double N[3], V[3], dif = 0.0, spe = 0.0;
+                for (int i = 0; i < 3; ++i) { N[i] = -g[i] / gnorm; V[i] = -d[i]; }
+                for (int l = 0; l < P->n_lights; ++l) {
+                    double L[3];
+                    const double* Ld = P->light_dir + 3 * l;
+                    const double len = sqrt(v_dot(Ld, Ld));
+                    for (int i = 0; i < 3; ++i) L[i] = Ld[i] / len;
+                    const double ndl = v_dot(N, L);
+                    double R[3];                             /* reflection of L about N */
+                    for (int i = 0; i < 3; ++i) R[i] = 2.0 * ndl * N[i] - L[i];
+                    const double rv = v_dot(R, V);
+                    dif += P->light_intensity[l] * (ndl > 0.0 ? ndl : 0.0);
+                    if (ndl > 0.0) spe += P->light_intensity[l] * pow(rv > 0.0 ? rv : 0.0, P->shininess);
+                }
+                for (int i = 0; i < 3; ++i) {
+                    double x = col[i] * (P->ka + P->kd * dif) + P->ks * spe;
+                    c[i] = x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x);
+                }
             } else {
                 /* headlight: light = view = -d; N = -g/|g|  (R-11) */
                 const double ndl = v_dot(g, d) / gnorm;      /* N . (-d) */

@@ -24,7 +24,8 @@ LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2}
 EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
            "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version",
            "mfa_render_field", "mfa_image_quality", "mfa_image_quality_workspace", "mfa_eval_hessian",
-           "mfa_fit_grid", "mfa_encode_grid", "mfa_eval_batch_ws", "mfa_eval_workspace_bytes",
+           "mfa_fit_grid", "mfa_encode_grid", "mfa_eval_batch_ws", "mfa_eval_workspace_bytes", "mfa_render_ex",
+           "mfa_eval_hessian_ws", "mfa_hessian_workspace_bytes",
            "mfa_probe_fp32", "mfa_probe_read_bw")
 
 
@@ -64,6 +65,11 @@ class ModelDesc_t(C.Structure):
 class Field_t(C.Structure):
     _fields_ = [("kind", C.c_int32), ("value_src", C.c_int32), ("grad_src", C.c_int32),
                 ("prm", C.c_double * 6)]
+
+
+class RenderExt_t(C.Structure):
+    _fields_ = [("field", C.POINTER(Field_t)), ("n_lights", C.c_int32), ("light_dir", C.POINTER(C.c_double)),
+                ("light_intensity", C.POINTER(C.c_double))]
 
 
 class EncodeConfig_t(C.Structure):
@@ -108,6 +114,10 @@ def lib():
         L.mfa_eval_workspace_bytes.argtypes = [vp, i64]
         L.mfa_eval_batch_ws.restype = C.c_int
         L.mfa_eval_batch_ws.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+        L.mfa_hessian_workspace_bytes.restype = C.c_size_t
+        L.mfa_hessian_workspace_bytes.argtypes = [vp, i64]
+        L.mfa_eval_hessian_ws.restype = C.c_int
+        L.mfa_eval_hessian_ws.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
         L.mfa_eval_hessian.restype = C.c_int
         L.mfa_eval_hessian.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
         L.mfa_render.restype = C.c_int
@@ -119,6 +129,9 @@ def lib():
         L.mfa_encode_grid.restype = C.c_int
         L.mfa_encode_grid.argtypes = [C.POINTER(i64), vp, C.POINTER(EncodeConfig_t),
                                       C.POINTER(C.POINTER(C.c_double)), vp, C.POINTER(EncodeResult_t), vp, vp]
+        L.mfa_render_ex.restype = C.c_int
+        L.mfa_render_ex.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
+                                    C.POINTER(RenderExt_t), C.POINTER(Tiles_t), vp, vp, vp]
         L.mfa_render_field.restype = C.c_int
         L.mfa_render_field.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
                                        C.POINTER(Field_t), C.POINTER(Tiles_t), vp, vp, vp]
@@ -275,7 +288,7 @@ class Model:
                                         _ptr(dw), _ptr(n_domain_errors), _stream_ptr(stream)))
         return out
 
-    def eval_hessian(self, u, v, w, n_domain_errors=None, stream=None):
+    def eval_hessian(self, u, v, w, n_domain_errors=None, stream=None, binned=True):
         """NEXT-4 (mfa_eval_hessian): returns (value [n], grad [3,n], hess [6,n]),
         hess rows = d2/du2, d2/dv2, d2/dw2, d2/dudv, d2/dudw, d2/dvdw (parameter space)."""
         import torch
@@ -283,17 +296,25 @@ class Model:
         val = torch.empty(n, device=u.device, dtype=torch.float32)
         grad = torch.empty((3, n), device=u.device, dtype=torch.float32)
         hess = torch.empty((6, n), device=u.device, dtype=torch.float32)
-        _check(lib().mfa_eval_hessian(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(grad), _ptr(hess),
-                                      _ptr(n_domain_errors), _stream_ptr(stream)))
+        if binned and n >= (1 << 16):
+            nb = int(lib().mfa_hessian_workspace_bytes(self._h, n))
+            ws = torch.empty(nb, dtype=torch.uint8, device=u.device)
+            _check(lib().mfa_eval_hessian_ws(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(grad),
+                                             _ptr(hess), _ptr(n_domain_errors), _ptr(ws), nb, _stream_ptr(stream)))
+        else:
+            _check(lib().mfa_eval_hessian(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(grad), _ptr(hess),
+                                          _ptr(n_domain_errors), _stream_ptr(stream)))
         return val, grad, hess
 
     # -- Algorithm 1 (mfa_render) ---------------------------------------------
     def render(self, cams, tf, v_lo, v_hi, params, tiles=None, out=None, samples=None, out_fp16=False,
-               stream=None, field=None):
+               stream=None, field=None, lights=None):
         """cams: list of Camera; tf: CUDA fp32 tensor (n,4); params: RenderParams.
         field: optional workloads.AnalyticField -- samples take their value
         and/or gradient from the analytic function (mfa_render_field; the
-        ground-truth image when both come from it).
+        ground-truth image when both come from it).  lights: optional
+        [(direction towards the light, intensity), ...] replacing the
+        headlight (mfa_render_ex).
         Returns the image [V,H,W,4] (or packed tiles [T,16,16,4] if tiles given)."""
         import torch
         tf = tf.contiguous()
@@ -310,10 +331,17 @@ class Model:
             shape = (len(cams), H, W, 4)
         if out is None:
             out = torch.empty(shape, device=tf.device, dtype=dt)
-        _check(lib().mfa_render_field(self._h, len(cams), ca, C.byref(tft), C.byref(pr),
-                                      C.byref(field_t(field)) if field is not None else None,
-                                      C.byref(tl) if tl is not None else None, _ptr(out), _ptr(samples),
-                                      _stream_ptr(stream)))
+        ext = None
+        if field is not None or lights:
+            ft = field_t(field) if field is not None else None
+            ld = np.ascontiguousarray([l[0] for l in lights or []], dtype=np.float64).reshape(-1)
+            li = np.ascontiguousarray([l[1] for l in lights or []], dtype=np.float64)
+            ext = RenderExt_t(C.pointer(ft) if ft is not None else None, len(lights or []),
+                              ld.ctypes.data_as(C.POINTER(C.c_double)), li.ctypes.data_as(C.POINTER(C.c_double)))
+        _check(lib().mfa_render_ex(self._h, len(cams), ca, C.byref(tft), C.byref(pr),
+                                   C.byref(ext) if ext is not None else None,
+                                   C.byref(tl) if tl is not None else None, _ptr(out), _ptr(samples),
+                                   _stream_ptr(stream)))
         return out
 
     def render_host(self, cams, tf_host: np.ndarray, v_lo, v_hi, params, out_host, out_fp16=False,

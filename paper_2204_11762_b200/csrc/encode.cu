@@ -174,7 +174,16 @@ __global__ void grid_error_kernel(const double* __restrict__ V, const float* __r
                                   double inv_range, const int* __restrict__ fu, const int* __restrict__ fv,
                                   const int* __restrict__ fw, unsigned long long* __restrict__ eu,
                                   unsigned long long* __restrict__ ev, unsigned long long* __restrict__ ew,
-                                  unsigned long long* __restrict__ emax, double* __restrict__ esq) {
+                                  unsigned long long* __restrict__ emax, double* __restrict__ esq, int S0, int S1,
+                                  int nspan_total) {
+    // per-CTA span maxima in shared memory (one global atomic per span per CTA)
+    // when the three span tables fit, else straight to global memory
+    extern __shared__ unsigned long long smax[];
+    const bool local = nspan_total > 0;
+    unsigned long long *su = smax, *sv = smax + S0, *sw = smax + S0 + S1;
+    if (local)
+        for (int b = threadIdx.x; b < nspan_total; b += blockDim.x) smax[b] = 0ULL;
+    __syncthreads();
     const int64_t total = (int64_t)mu * mv * mw;
     double sq = 0.0, mx = 0.0;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -185,10 +194,21 @@ __global__ void grid_error_kernel(const double* __restrict__ V, const float* __r
         const double e = fabs(V[idx] - (double)Q[idx]) * inv_range;
         sq += e * e;
         mx = fmax(mx, e);
-        atomicMax(eu + __ldg(fu + i), dbits(e));
-        atomicMax(ev + __ldg(fv + j), dbits(e));
-        atomicMax(ew + __ldg(fw + k), dbits(e));
+        const unsigned long long eb = dbits(e);
+        if (local) {
+            atomicMax(su + __ldg(fu + i), eb);
+            atomicMax(sv + __ldg(fv + j), eb);
+            atomicMax(sw + __ldg(fw + k), eb);
+        } else {
+            atomicMax(eu + __ldg(fu + i), eb);
+            atomicMax(ev + __ldg(fv + j), eb);
+            atomicMax(ew + __ldg(fw + k), eb);
+        }
     }
+    __syncthreads();
+    if (local)
+        for (int b = threadIdx.x; b < nspan_total; b += blockDim.x)
+            if (smax[b]) atomicMax(eu + b, smax[b]);   // eu, ev, ew are contiguous like smax
     for (int o = 16; o > 0; o >>= 1) {
         sq += __shfl_xor_sync(0xffffffffu, sq, o);
         mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -483,8 +503,10 @@ extern "C" mfa_status mfa_encode_grid(const int64_t dims[3], const float* values
         cudaMemsetAsync(W.err, 0, sizeof(unsigned long long) * nerr, st);
         unsigned long long *eu = W.err, *ev = eu + S0, *ew = ev + S1, *emax = ew + S2;
         double* esq = reinterpret_cast<double*>(emax + 1);
-        grid_error_kernel<<<grid_for(npts), 128, 0, st>>>(W.V, values, (int)mu, (int)mv, (int)mw, inv_range, ax[0].f,
-                                                           ax[1].f, ax[2].f, eu, ev, ew, emax, esq);
+        const int nsp = (S0 + S1 + S2 <= 6144) ? (int)(S0 + S1 + S2) : 0;   // shared-memory span maxima
+        grid_error_kernel<<<grid_for(npts), 128, sizeof(unsigned long long) * nsp, st>>>(
+            W.V, values, (int)mu, (int)mv, (int)mw, inv_range, ax[0].f, ax[1].f, ax[2].f, eu, ev, ew, emax, esq,
+            (int)S0, (int)S1, nsp);
         std::vector<unsigned long long> h(S0 + S1 + S2 + 2);
         cudaMemcpyAsync(h.data(), W.err, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st);
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return done(cuda_fail(e, "encode residual"));

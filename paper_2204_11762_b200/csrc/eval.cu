@@ -270,10 +270,33 @@ static BinGrid make_bins(const Model* m) {
     return g;
 }
 
-size_t eval_workspace_bytes(const Model* m, int64_t n) {
+size_t bin_workspace_bytes(const Model* m, int64_t n) {
     const BinGrid g = make_bins(m);
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
     return up(sizeof(int) * (size_t)n) + up(sizeof(float4) * (size_t)n) + 2 * up(sizeof(unsigned) * (g.nbins + 1));
+}
+
+size_t eval_workspace_bytes(const Model* m, int64_t n) { return bin_workspace_bytes(m, n); }
+
+BinnedPoints bin_points(const Model* m, int64_t n, const float* u, const float* v, const float* w, void* ws,
+                        cudaStream_t st) {
+    const BinGrid g = make_bins(m);
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    char* b = (char*)ws;
+    int* bins = (int*)b;
+    float4* rec = (float4*)(b + up(sizeof(int) * (size_t)n));
+    unsigned* counts = (unsigned*)(b + up(sizeof(int) * (size_t)n) + up(sizeof(float4) * (size_t)n));
+    unsigned* cursor = (unsigned*)((char*)counts + up(sizeof(unsigned) * (g.nbins + 1)));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+    cudaMemsetAsync(counts, 0, sizeof(unsigned) * (g.nbins + 1), st);
+    const size_t smem = g.nbins + 1 <= kBinSmem ? sizeof(unsigned) * (g.nbins + 1) : 0;
+    bin_count_kernel<<<grid, 256, smem, st>>>(u, v, w, n, g, bins, counts);
+    bin_scan_kernel<<<1, 1024, 0, st>>>(counts, g.nbins + 1, cursor);
+    bin_scatter_kernel<<<grid, 256, 0, st>>>(u, v, w, n, bins, cursor, rec);
+    return BinnedPoints{rec, bins};
 }
 
 mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v, const float* w, float* value,
@@ -284,25 +307,10 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
     a.out4 = nullptr;
     a.pos = nullptr;
     if (ws && n >= (int64_t)1 << 16 && n < ((int64_t)1 << 31) && ws_bytes >= eval_workspace_bytes(m, n)) {
-        const BinGrid g = make_bins(m);
-        auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
-        char* b = (char*)ws;
-        int* bins = (int*)b;
-        float4* rec = (float4*)(b + up(sizeof(int) * (size_t)n));
-        unsigned* counts = (unsigned*)(b + up(sizeof(int) * (size_t)n) + up(sizeof(float4) * (size_t)n));
-        unsigned* cursor = (unsigned*)((char*)counts + up(sizeof(unsigned) * (g.nbins + 1)));
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
-        cudaMemsetAsync(counts, 0, sizeof(unsigned) * (g.nbins + 1), st);
-        const size_t smem = g.nbins + 1 <= kBinSmem ? sizeof(unsigned) * (g.nbins + 1) : 0;
-        bin_count_kernel<<<grid, 256, smem, st>>>(u, v, w, n, g, bins, counts);
-        bin_scan_kernel<<<1, 1024, 0, st>>>(counts, g.nbins + 1, cursor);
-        bin_scatter_kernel<<<grid, 256, 0, st>>>(u, v, w, n, bins, cursor, rec);
-        a.rec = rec;
-        a.out4 = rec;
-        a.pos = bins;
+        const BinnedPoints bp = bin_points(m, n, u, v, w, ws, st);
+        a.rec = bp.rec;
+        a.out4 = bp.rec;   // results overwrite the record a thread has just read
+        a.pos = bp.pos;
     }
     a.Q = m->Q;
     a.g.nbx = m->nb[0];

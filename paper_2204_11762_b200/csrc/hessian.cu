@@ -16,6 +16,8 @@
 //   z: v = N_w B0, v_u = N_w B1, v_v = N_w B2, v_w = N'_w B0, v_uu = N_w B3,
 //      v_uv = N_w B4, v_vv = N_w B5, v_uw = N'_w B1, v_vw = N'_w B2, v_ww = N''_w B0
 // then t -> u scaling per axis (sc = S or 1/h; squared / mixed for 2nd order).
+// With a workspace (mfa_eval_hessian_ws) large batches are spatially binned
+// first, as in mfa_eval_batch_ws (eval.cu), and gathered back.
 #include "kernels.cuh"
 
 namespace mfa {
@@ -33,6 +35,8 @@ struct HessArgs {
     float* hess;    // [6][n]: uu, vv, ww, uv, uw, vw
     unsigned long long* n_err;
     int64_t n;
+    const float4* rec;   // SORTED: (u, v, w, index bits) in bin order
+    float4* out;         // SORTED: 3 float4 per sorted position (10 outputs + pad)
 };
 
 // Bernstein polynomials in power form: B_j(t) = sum_m c[j][m] t^m,
@@ -105,13 +109,24 @@ __device__ __forceinline__ void basis3(const AxisArgs& A, int s, float t, float 
     }
 }
 
-template <int P, int LAYOUT, bool UNI>
+template <int P, int LAYOUT, bool UNI, bool SORTED>
 __global__ void __launch_bounds__(256) hessian_kernel(const __grid_constant__ HessArgs args) {
     constexpr bool BEZ = LAYOUT == kBezier;
     const int64_t n = args.n;
     unsigned errs = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float q[3] = {__ldg(args.u + i), __ldg(args.v + i), __ldg(args.w + i)};
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < n; it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = it;
+        float q[3];
+        if constexpr (SORTED) {
+            const float4 r = __ldg(args.rec + it);
+            q[0] = r.x;
+            q[1] = r.y;
+            q[2] = r.z;
+        } else {
+            q[0] = __ldg(args.u + i);
+            q[1] = __ldg(args.v + i);
+            q[2] = __ldg(args.w + i);
+        }
         float out[10];
         if (!(q[0] >= 0.f && q[0] <= 1.f && q[1] >= 0.f && q[1] <= 1.f && q[2] >= 0.f && q[2] <= 1.f)) {
             ++errs;
@@ -182,13 +197,19 @@ __global__ void __launch_bounds__(256) hessian_kernel(const __grid_constant__ He
             out[8] *= sc[0] * sc[2];
             out[9] *= sc[1] * sc[2];
         }
-        if (args.value) args.value[i] = out[0];
-        if (args.grad) {
+        if constexpr (SORTED) {   // coalesced at the sorted position; gathered back afterwards
+            args.out[3 * it + 0] = make_float4(out[0], out[1], out[2], out[3]);
+            args.out[3 * it + 1] = make_float4(out[4], out[5], out[6], out[7]);
+            args.out[3 * it + 2] = make_float4(out[8], out[9], 0.f, 0.f);
+        } else {
+            if (args.value) args.value[i] = out[0];
+            if (args.grad) {
 #pragma unroll
-            for (int k = 0; k < 3; ++k) args.grad[k * n + i] = out[1 + k];
+                for (int k = 0; k < 3; ++k) args.grad[k * n + i] = out[1 + k];
+            }
+#pragma unroll
+            for (int k = 0; k < 6; ++k) args.hess[k * n + i] = out[4 + k];
         }
-#pragma unroll
-        for (int k = 0; k < 6; ++k) args.hess[k * n + i] = out[4 + k];
     }
     if (args.n_err) {
         for (int o = 16; o > 0; o >>= 1) errs += __shfl_xor_sync(0xffffffffu, errs, o);
@@ -202,8 +223,37 @@ static cudaError_t launch_hess_t(const HessArgs& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t grid = std::min<int64_t>((a.n + 255) / 256, (int64_t)sms * 16);
-    hessian_kernel<P, LAYOUT, UNI><<<(unsigned)grid, 256, 0, st>>>(a);
+    if (a.rec)
+        hessian_kernel<P, LAYOUT, UNI, true><<<(unsigned)grid, 256, 0, st>>>(a);
+    else
+        hessian_kernel<P, LAYOUT, UNI, false><<<(unsigned)grid, 256, 0, st>>>(a);
     return cudaGetLastError();
+}
+
+// results of the sorted evaluation back to the caller's SoA arrays
+__global__ void __launch_bounds__(256) hess_gather_kernel(const float4* __restrict__ out, const int* __restrict__ pos,
+                                                          int64_t n, float* __restrict__ value,
+                                                          float* __restrict__ grad, float* __restrict__ hess) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = __ldg(pos + i);
+        const float4 a = __ldg(out + 3 * p), b = __ldg(out + 3 * p + 1), c = __ldg(out + 3 * p + 2);
+        if (value) value[i] = a.x;
+        if (grad) {
+            grad[i] = a.y;
+            grad[n + i] = a.z;
+            grad[2 * n + i] = a.w;
+        }
+        hess[i] = b.x;
+        hess[n + i] = b.y;
+        hess[2 * n + i] = b.z;
+        hess[3 * n + i] = b.w;
+        hess[4 * n + i] = c.x;
+        hess[5 * n + i] = c.y;
+    }
+}
+
+size_t hessian_workspace_bytes(const Model* m, int64_t n) {
+    return bin_workspace_bytes(m, n) + ((sizeof(float4) * 3 * (size_t)n + 255) & ~(size_t)255);
 }
 
 template <int P>
@@ -219,9 +269,21 @@ static cudaError_t dispatch_hess(const HessArgs& a, int layout, bool uni, cudaSt
 
 using namespace mfa;
 
+extern "C" size_t mfa_hessian_workspace_bytes(mfa_model h, int64_t n) {
+    if (!h || n < 0) return 0;
+    return hessian_workspace_bytes(reinterpret_cast<const Model*>(h), n);
+}
+
 extern "C" mfa_status mfa_eval_hessian(mfa_model h, int64_t n, const float* u, const float* v, const float* w,
                                        float* value, float* grad, float* hess, unsigned long long* n_domain_errors,
                                        mfa_stream stream) {
+    return mfa_eval_hessian_ws(h, n, u, v, w, value, grad, hess, n_domain_errors, nullptr, 0, stream);
+}
+
+extern "C" mfa_status mfa_eval_hessian_ws(mfa_model h, int64_t n, const float* u, const float* v, const float* w,
+                                          float* value, float* grad, float* hess,
+                                          unsigned long long* n_domain_errors, void* workspace,
+                                          size_t workspace_bytes, mfa_stream stream) {
     if (!h) return fail(MFA_ERR_INVALID_ARG, "model is NULL");
     if (n < 0) return fail(MFA_ERR_INVALID_ARG, "n < 0");
     if (n == 0) return MFA_OK;
@@ -246,8 +308,19 @@ extern "C" mfa_status mfa_eval_hessian(mfa_model h, int64_t n, const float* u, c
     a.hess = hess;
     a.n_err = n_domain_errors;
     a.n = n;
+    a.rec = nullptr;
+    a.out = nullptr;
     const bool uni = m->uniform[0] && m->uniform[1] && m->uniform[2];
     cudaStream_t st = (cudaStream_t)stream;
+    if (workspace && workspace_bytes < hessian_workspace_bytes(m, n))
+        return fail(MFA_ERR_INVALID_ARG, "workspace smaller than mfa_hessian_workspace_bytes()");
+    const int* pos = nullptr;
+    if (workspace && n >= (int64_t)1 << 16 && n < ((int64_t)1 << 31)) {
+        const BinnedPoints bp = bin_points(m, n, u, v, w, workspace, st);
+        a.rec = bp.rec;
+        pos = bp.pos;
+        a.out = reinterpret_cast<float4*>((char*)workspace + bin_workspace_bytes(m, n));
+    }
     cudaError_t e;
     switch (m->p) {
         case 1: e = dispatch_hess<1>(a, m->layout, uni, st); break;
@@ -255,6 +328,14 @@ extern "C" mfa_status mfa_eval_hessian(mfa_model h, int64_t n, const float* u, c
         case 3: e = dispatch_hess<3>(a, m->layout, uni, st); break;
         case 4: e = dispatch_hess<4>(a, m->layout, uni, st); break;
         default: e = dispatch_hess<5>(a, m->layout, uni, st); break;
+    }
+    if (e == cudaSuccess && a.rec) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+        hess_gather_kernel<<<grid, 256, 0, st>>>(a.out, pos, n, value, grad, hess);
+        e = cudaGetLastError();
     }
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "hessian launch");
 }

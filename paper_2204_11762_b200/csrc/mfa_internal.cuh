@@ -139,8 +139,17 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
                        float* value, float* du, float* dv, float* dw,
                        unsigned long long* n_err, cudaStream_t st, void* ws = nullptr, size_t ws_bytes = 0);
 size_t eval_workspace_bytes(const Model* m, int64_t n);
+// spatial binning of a point batch (eval.cu): records (u, v, w, index bits) in
+// bin order, and pos[i] = sorted position of point i; needs bin_workspace_bytes
+struct BinnedPoints {
+    float4* rec;
+    int* pos;
+};
+size_t bin_workspace_bytes(const Model* m, int64_t n);
+BinnedPoints bin_points(const Model* m, int64_t n, const float* u, const float* v, const float* w, void* ws,
+                        cudaStream_t st);
 mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                          const mfa_render_params* prm, const mfa_tiles* tiles, void* out,
-                         unsigned long long* samples, cudaStream_t st, const mfa_field* fld = nullptr);
+                         unsigned long long* samples, cudaStream_t st, const mfa_render_ext* ext = nullptr);
 
 }  // namespace mfa

@@ -615,18 +615,37 @@ static mfa_status validate_render(const Model* m, int32_t n_views, const mfa_cam
 extern "C" mfa_status mfa_render(mfa_model h, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                                  const mfa_render_params* prm, const mfa_tiles* tiles, void* rgba_out,
                                  unsigned long long* samples_out, mfa_stream stream) {
-    return mfa_render_field(h, n_views, cams, tf, prm, nullptr, tiles, rgba_out, samples_out, stream);
+    return mfa_render_ex(h, n_views, cams, tf, prm, nullptr, tiles, rgba_out, samples_out, stream);
 }
 
 extern "C" mfa_status mfa_render_field(mfa_model h, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                                        const mfa_render_params* prm, const mfa_field* field, const mfa_tiles* tiles,
                                        void* rgba_out, unsigned long long* samples_out, mfa_stream stream) {
+    mfa_render_ext ext{field, 0, nullptr, nullptr};
+    return mfa_render_ex(h, n_views, cams, tf, prm, &ext, tiles, rgba_out, samples_out, stream);
+}
+
+extern "C" mfa_status mfa_render_ex(mfa_model h, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
+                                    const mfa_render_params* prm, const mfa_render_ext* ext, const mfa_tiles* tiles,
+                                    void* rgba_out, unsigned long long* samples_out, mfa_stream stream) {
     if (!h) return fail(MFA_ERR_INVALID_ARG, "model is NULL");
+    const mfa_field* field = ext ? ext->field : nullptr;
     if (field && (field->value_src || field->grad_src) &&
         !(field->kind == MFA_FIELD_GAUSSIAN_BEAM || field->kind == MFA_FIELD_MARSCHNER_LOBB))
         return fail(MFA_ERR_INVALID_ARG, "field: unknown kind");
     if (field && field->kind == MFA_FIELD_GAUSSIAN_BEAM && !(field->prm[3] > 0.0 && field->prm[4] > 0.0))
         return fail(MFA_ERR_INVALID_ARG, "field: Gaussian beam needs sigma > 0 and R > 0");
+    if (ext && ext->n_lights) {
+        if (ext->n_lights < 0 || ext->n_lights > MFA_MAX_LIGHTS)
+            return fail(MFA_ERR_INVALID_ARG, "n_lights must be in [0, MFA_MAX_LIGHTS]");
+        if (!ext->light_dir || !ext->light_intensity) return fail(MFA_ERR_INVALID_ARG, "light arrays are NULL");
+        for (int l = 0; l < ext->n_lights; ++l) {
+            const double* L = ext->light_dir + 3 * l;
+            const double n2 = L[0] * L[0] + L[1] * L[1] + L[2] * L[2];
+            if (!(n2 > 0.0) || !isfinite(n2) || !isfinite(ext->light_intensity[l]))
+                return fail(MFA_ERR_INVALID_ARG, "light " + std::to_string(l) + ": zero or non-finite direction/intensity");
+        }
+    }
     const Model* m = reinterpret_cast<const Model*>(h);
     mfa_status s = validate_render(m, n_views, cams, prm);
     if (s != MFA_OK) return s;
@@ -636,7 +655,7 @@ extern "C" mfa_status mfa_render_field(mfa_model h, int32_t n_views, const mfa_c
     if (tiles && (tiles->n_tiles < 0 || (tiles->n_tiles > 0 && !tiles->tiles)))
         return fail(MFA_ERR_INVALID_ARG, "tiles: bad n_tiles / tiles pointer");
     if ((s = check_device(m)) != MFA_OK) return s;
-    return launch_render(m, n_views, cams, tf, prm, tiles, rgba_out, samples_out, (cudaStream_t)stream, field);
+    return launch_render(m, n_views, cams, tf, prm, tiles, rgba_out, samples_out, (cudaStream_t)stream, ext);
 }
 
 extern "C" mfa_status mfa_unpack_tiles(const void* packed, int32_t in_fp16, const int32_t* tiles, int64_t n_tiles,

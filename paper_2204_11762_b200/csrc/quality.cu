@@ -11,7 +11,7 @@
 // exact in fp64), reductions in a fixed order (deterministic):
 //   K_q  per pixel: levels, luma images, squared-difference partial sums, error map
 //   K_s  per valid window: 5 windowed moments from a shared-memory tile, SSIM partials
-//   K_r  one CTA: final sums -> (MSE, PSNR, mean SSIM)
+//   K_r  one CTA: fixed-order tree of the partials -> (MSE, PSNR, mean SSIM)
 #include <math.h>
 
 #include <algorithm>
@@ -115,12 +115,26 @@ __global__ void __launch_bounds__(kSTileX* kSTileY) ssim_kernel(const double* __
     if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = t;
 }
 
-__global__ void quality_final_kernel(const double* __restrict__ pq, int nq, const double* __restrict__ ps, int ns,
-                                     int64_t npix, int64_t nwin, double* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double s = 0.0, t = 0.0;
-    for (int k = 0; k < nq; ++k) s += pq[k];
-    for (int k = 0; k < ns; ++k) t += ps[k];
+// one CTA of 1024 threads: strided partial sums, then a fixed-order tree
+__global__ void __launch_bounds__(1024) quality_final_kernel(const double* __restrict__ pq, int nq,
+                                                             const double* __restrict__ ps, int ns, int64_t npix,
+                                                             int64_t nwin, double* __restrict__ out) {
+    __shared__ double sq[1024], st[1024];
+    double a = 0.0, b = 0.0;
+    for (int k = threadIdx.x; k < nq; k += 1024) a += pq[k];
+    for (int k = threadIdx.x; k < ns; k += 1024) b += ps[k];
+    sq[threadIdx.x] = a;
+    st[threadIdx.x] = b;
+    __syncthreads();
+    for (int o = 512; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            sq[threadIdx.x] += sq[threadIdx.x + o];
+            st[threadIdx.x] += st[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    const double s = sq[0], t = st[0];
     const double mse = s / (3.0 * (double)npix);
     out[0] = mse;
     out[1] = mse == 0.0 ? INFINITY : 10.0 * log10(255.0 * 255.0 / mse);
@@ -175,7 +189,7 @@ extern "C" mfa_status mfa_image_quality(int32_t width, int32_t height, const flo
     static const GaussWin gw = make_window();
     ssim_kernel<<<dim3(p.sx, p.sy), kSTileX * kSTileY, 0, st>>>(ya, yb, width, height, gw, ps);
     const int64_t nwin = (int64_t)(width - kWin + 1) * (height - kWin + 1);
-    quality_final_kernel<<<1, 32, 0, st>>>(pq, p.nq, ps, p.sx * p.sy, n, nwin, out3);
+    quality_final_kernel<<<1, 1024, 0, st>>>(pq, p.nq, ps, p.sx * p.sy, n, nwin, out3);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "image quality kernels");
 }

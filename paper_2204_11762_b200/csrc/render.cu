@@ -1,6 +1,8 @@
 // mfa_render host side: argument marshalling into RenderArgs and the launch
 // (the kernel is in render_kernel.cuh; this TU instantiates it for the MFA
 // query path, truth.cu for the analytic ground-truth field).
+#include <math.h>
+
 #include <algorithm>
 #include <atomic>
 
@@ -22,10 +24,24 @@ cudaError_t dispatch_render_main(const RenderArgs& a, int p, int layout, bool un
 
 mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                          const mfa_render_params* prm, const mfa_tiles* tiles, void* out,
-                         unsigned long long* samples, cudaStream_t st, const mfa_field* fld) {
+                         unsigned long long* samples, cudaStream_t st, const mfa_render_ext* ext) {
     RenderArgs* a = new RenderArgs();  // ~7 KB: keep it off the caller's stack
-    // the analytic-field instantiations run only when a sample takes something from the field
+    // the extended instantiations run only when a sample takes something from
+    // the analytic field or there are explicit lights
+    const mfa_field* fld = ext ? ext->field : nullptr;
     const bool field = fld && (fld->value_src || fld->grad_src);
+    const bool lights = ext && ext->n_lights > 0;
+    a->fld.vsrc = a->fld.gsrc = 0;
+    a->lights.n = 0;
+    if (lights) {
+        a->lights.n = ext->n_lights;
+        for (int l = 0; l < ext->n_lights; ++l) {
+            const double* L = ext->light_dir + 3 * l;
+            const double len = sqrt(L[0] * L[0] + L[1] * L[1] + L[2] * L[2]);
+            for (int k = 0; k < 3; ++k) a->lights.dir[l][k] = (float)(L[k] / len);
+            a->lights.intensity[l] = (float)ext->light_intensity[l];
+        }
+    }
     if (field) {
         a->fld.kind = fld->kind;
         a->fld.vsrc = fld->value_src != 0;
@@ -79,7 +95,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         a->queue = m->queue + (g_slot.fetch_add(1) % kQueueSlots);
         cudaError_t r = cudaMemsetAsync(a->queue, 0, sizeof(unsigned int), st);
         if (r != cudaSuccess) return r;
-        return field ? dispatch_render_field(*a, m->p, m->layout, uni, shade, st)
+        return (field || lights) ? dispatch_render_ext(*a, m->p, m->layout, uni, shade, st)
                      : dispatch_render_main(*a, m->p, m->layout, uni, shade, st);
     };
     if (tiles) {

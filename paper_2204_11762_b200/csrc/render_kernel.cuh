@@ -1,5 +1,6 @@
 // render_kernel: Algorithm 1 fused per ray (shared by render.cu and
-// truth.cu, which instantiate it without / with the analytic field).
+// truth.cu, which instantiate it without / with the extensions: the analytic
+// ground-truth field of NEXT-2 and several directional lights, NEXT-4).
 //
 //   work = warp units of 8x4 pixels (8 per 16x16 tile) handed out by a global
 //          atomic counter to persistent warps (grid = SMs x resident CTAs), so
@@ -34,6 +35,15 @@ struct FieldArgs {
     float invL[3];                // parameter-space gradient -> physical (R-4)
 };
 
+// NEXT-4 ("multiple light sources can be added in the future"):
+// directional lights, unit direction towards the light and intensity.
+constexpr int kMaxLights = MFA_MAX_LIGHTS;
+struct LightArgs {
+    int n;                        // 0: the headlight (R-11)
+    float dir[kMaxLights][3];
+    float intensity[kMaxLights];
+};
+
 struct RenderArgs {
     const float4* Q;
     BrickGrid g;
@@ -57,7 +67,8 @@ struct RenderArgs {
     void* out;
     int out_fp16;
     unsigned long long* samples;
-    FieldArgs fld;                // used by the FLD instantiations only
+    FieldArgs fld;                // used by the EXT instantiations only
+    LightArgs lights;             // used by the EXT instantiations only
     mfa_camera cams[kMaxViewsPerLaunch];
 };
 
@@ -159,7 +170,7 @@ struct RenderShape {
     static constexpr bool CTA_TILES = MFA_CTA_TILES < 0 ? (P >= 4 && THREADS == 256) : (bool)MFA_CTA_TILES;
 };
 
-template <int P, int LAYOUT, bool UNI, bool SHADE, bool FLD>
+template <int P, int LAYOUT, bool UNI, bool SHADE, bool EXT>
 __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P, LAYOUT>::MINB)
     render_kernel(const __grid_constant__ RenderArgs args) {
     constexpr bool BEZ = LAYOUT == kBezier;
@@ -419,7 +430,33 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             float cb = fmaf(wt, T1.z - T0.z, T0.z);
             const float a = fmaf(wt, T1.w - T0.w, T0.w);
             // a9: Phong with a headlight (l.10-11; R-11); zero gradient -> ambient
-            if (SHADE) {
+            bool lit_done = false;
+            if constexpr (SHADE && EXT) {
+                if (args.lights.n > 0) {  // several directional lights (R-30)
+                    const float gx = gu * gs[0], gy = gv * gs[1], gz = gw * gs[2];
+                    const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
+                    const bool zero = n2 <= args.eps2;
+                    const float inv = rsqrtf(fmaxf(n2, 1e-37f));
+                    const float ndv = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * inv;   // N . V, V = -d
+                    float dif = 0.f, spe = 0.f;
+                    for (int l = 0; l < args.lights.n; ++l) {
+                        const float* L = args.lights.dir[l];
+                        const float ndl = -fmaf(gx, L[0], fmaf(gy, L[1], gz * L[2])) * inv;  // N . L
+                        const float ldv = -fmaf(L[0], dx, fmaf(L[1], dy, L[2] * dz));         // L . V
+                        const float rv = fmaxf(fmaf(2.f * ndl, ndv, -ldv), 0.f);              // R . V
+                        float sp = args.shin == 0.f ? 1.f : exp2f(args.shin * __log2f(rv));
+                        dif = fmaf(args.lights.intensity[l], fmaxf(ndl, 0.f), dif);
+                        spe = fmaf(args.lights.intensity[l], ndl > 0.f ? sp : 0.f, spe);
+                    }
+                    const float lit = zero ? args.ka : fmaf(args.kd, dif, args.ka);
+                    const float add = zero ? 0.f : args.ks * spe;
+                    cr = __saturatef(fmaf(cr, lit, add));
+                    cg = __saturatef(fmaf(cg, lit, add));
+                    cb = __saturatef(fmaf(cb, lit, add));
+                    lit_done = true;
+                }
+            }
+            if (SHADE && !lit_done) {
                 const float gx = gu * gs[0], gy = gv * gs[1], gz = gw * gs[2];
                 const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
                 const bool zero = n2 <= args.eps2;
@@ -443,7 +480,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             A += wgt;
         };
 
-        // NEXT-2 (FLD instantiations): the sample takes its value and/or its
+        // NEXT-2 (EXT instantiations): the sample takes its value and/or its
         // gradient from the analytic field at the same parameter point
         auto sample_field = [&](const int (&s)[3], const float (&t)[3], float& v, float& g0, float& g1, float& g2,
                                 float (&gsx)[3]) {
@@ -472,7 +509,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             int s[3];
             float t[3];
             locate(s, t, gs);
-            if constexpr (FLD) {
+            if constexpr (EXT) {
                 sample_field(s, t, val, gu, gv, gw, gs);
             } else {
                 fetch(s);
@@ -488,7 +525,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                     float t[3], gs1[3];
                     locate(s, t, gs1);
                     float val1 = 0.f, gu1 = 0.f, gv1 = 0.f, gw1 = 0.f;
-                    if constexpr (FLD) {
+                    if constexpr (EXT) {
                         shade_composite(val, gu, gv, gw, gs);
                         sample_field(s, t, val1, gu1, gv1, gw1, gs1);
                     } else {
@@ -535,10 +572,10 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
     }
 }
 
-template <int P, int LAYOUT, bool UNI, bool SHADE, bool FLD>
+template <int P, int LAYOUT, bool UNI, bool SHADE, bool EXT>
 static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(float4) * a.tf_n;
-    auto kern = render_kernel<P, LAYOUT, UNI, SHADE, FLD>;
+    auto kern = render_kernel<P, LAYOUT, UNI, SHADE, EXT>;
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -552,25 +589,25 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int P, int LAYOUT, bool FLD>
+template <int P, int LAYOUT, bool EXT>
 static cudaError_t dispatch_render_l(const RenderArgs& a, bool uni, bool shade, cudaStream_t st) {
     if (uni)
-        return shade ? launch_render_t<P, LAYOUT, true, true, FLD>(a, st)
-                     : launch_render_t<P, LAYOUT, true, false, FLD>(a, st);
-    return shade ? launch_render_t<P, LAYOUT, false, true, FLD>(a, st)
-                 : launch_render_t<P, LAYOUT, false, false, FLD>(a, st);
+        return shade ? launch_render_t<P, LAYOUT, true, true, EXT>(a, st)
+                     : launch_render_t<P, LAYOUT, true, false, EXT>(a, st);
+    return shade ? launch_render_t<P, LAYOUT, false, true, EXT>(a, st)
+                 : launch_render_t<P, LAYOUT, false, false, EXT>(a, st);
 }
 
-template <int P, bool FLD>
+template <int P, bool EXT>
 static cudaError_t dispatch_render(const RenderArgs& a, int layout, bool uni, bool shade, cudaStream_t st) {
     if constexpr (P <= 3) {
-        if (layout == kBezier) return dispatch_render_l<P, kBezier, FLD>(a, uni, shade, st);
+        if (layout == kBezier) return dispatch_render_l<P, kBezier, EXT>(a, uni, shade, st);
     }
-    return dispatch_render_l<P, kQuads, FLD>(a, uni, shade, st);
+    return dispatch_render_l<P, kQuads, EXT>(a, uni, shade, st);
 }
 
-// defined in render.cu (MFA query only) and truth.cu (analytic field)
+// defined in render.cu (the hot path) and truth.cu (analytic field, several lights)
 cudaError_t dispatch_render_main(const RenderArgs& a, int p, int layout, bool uni, bool shade, cudaStream_t st);
-cudaError_t dispatch_render_field(const RenderArgs& a, int p, int layout, bool uni, bool shade, cudaStream_t st);
+cudaError_t dispatch_render_ext(const RenderArgs& a, int p, int layout, bool uni, bool shade, cudaStream_t st);
 
 }  // namespace mfa

@@ -116,3 +116,20 @@ def test_hessian_domain_errors_and_empty():
     e = torch.empty(0, device="cuda")
     m.eval_hessian(e, e, e)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("c,layout", [(3, "quads"), (5, "bezier")])
+def test_hessian_binned_equals_direct(c, layout):
+    w, m, _ = models(c, layout)
+    u, v, ww = WL.query_points(c, 1 << 17)
+    u = u.copy()
+    u[[3, 999]] = [np.nan, 2.0]
+    res = []
+    for binned in (True, False):
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        r = m.eval_hessian(cuda(u), cuda(v), cuda(ww), n_domain_errors=cnt, binned=binned)
+        torch.cuda.synchronize()
+        res.append(([t.cpu().numpy() for t in r], int(cnt.item())))
+    for a, b in zip(res[0][0], res[1][0]):
+        np.testing.assert_array_equal(a, b)
+    assert res[0][1] == res[1][1] == 2

@@ -126,3 +126,33 @@ def test_quality_table_on_gpu_images():
         seq = [r for r in rows if r[1] == test]
         assert seq[0][2] > seq[1][2] > seq[2][2], seq
         assert seq[0][4] < seq[2][4], seq
+
+
+@pytest.mark.parametrize("c", [2, 5])
+def test_lights_parity(c):
+    """NEXT-4 lights (mfa_render_ex, R-30) against the oracle: three lights
+    on C2 (uniform) and a reduced C5 (non-uniform Bezier), also combined with
+    the analytic field; one light towards -d on an orthographic view equals
+    the default headlight render."""
+    from paper_2204_11762_b200 import Model
+    w = WL.make_config(c, width=128, height=96, n_views=1) if c == 5 else WL.make_config(c, width=160, height=128)
+    m = Model.from_workload(w)
+    om = O.Model.from_workload(w)
+    lights = [((0.3, -0.5, 0.8), 0.8), ((-0.7, 0.2, 0.1), 0.5), ((0.0, 0.0, -1.0), 0.3)]
+    for fld in (None, WL.AnalyticField.marschner_lobb(0, 1)):
+        img = m.render(w.cameras[:1], cuda(w.tf), w.v_lo, w.v_hi, w.params, lights=lights, field=fld)
+        torch.cuda.synchronize()
+        ref = O.render(om, w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params, lights=lights, field=fld)
+        st = parity.check_image(img[0].cpu().numpy().reshape(-1, 4), ref, f"C{c} lights field={fld}")
+        print(c, fld is not None, st)
+
+
+def test_single_headlight_light_equals_default():
+    from paper_2204_11762_b200 import Model
+    w = WL.make_config(1)
+    m = Model.from_workload(w)
+    o, d = O.ray(w.cameras[0], 0, 0)
+    a = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params)
+    b = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params, lights=[(-d, 1.0)])
+    torch.cuda.synchronize()
+    assert np.abs(a.cpu().numpy() - b.cpu().numpy()).max() <= 1e-6
