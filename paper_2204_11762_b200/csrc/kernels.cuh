@@ -481,6 +481,10 @@ __device__ __forceinline__ float contract_v_cached(const float (&nb)[P + 1][P + 
 // Bernstein polynomials B_j(t) = C(p,j) t^j (1-t)^(p-j), the same on every
 // span, evaluated here in product form (all terms non-negative).
 // ---------------------------------------------------------------------------
+#ifndef MFA_BERN3
+#define MFA_BERN3 1
+#endif
+
 __host__ __device__ constexpr float binomf(int n, int k) {
     float r = 1.f;
     for (int i = 1; i <= k; ++i) r = r * (float)(n - k + i) / (float)i;
@@ -489,6 +493,18 @@ __host__ __device__ constexpr float binomf(int n, int k) {
 
 template <int P, bool SWAP>
 __device__ __forceinline__ void bernstein(float t, float2 (&B)[P + 1]) {
+#if MFA_BERN3
+    if constexpr (P == 3) {   // cubic written out: 10 FP32 ops for values and derivatives
+        const float s = 1.f - t;
+        const float s2 = s * s, t2 = t * t, ts3 = 3.f * (t * s);
+        const float d0 = -3.f * s2, d3 = 3.f * t2;
+        const float v[4] = {s2 * s, ts3 * s, ts3 * t, t2 * t};
+        const float d[4] = {d0, fmaf(ts3, -2.f, -d0), fmaf(ts3, 2.f, -d3), d3};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) B[j] = SWAP ? make_float2(d[j], v[j]) : make_float2(v[j], d[j]);
+        return;
+    }
+#endif
     const float s = 1.f - t;
     float tp[P + 1], sp[P + 1];
     tp[0] = 1.f;

@@ -139,6 +139,24 @@ __device__ __forceinline__ void field_eval(const FieldArgs& f, const double (&u)
     }
 }
 
+#ifndef MFA_FAST_POW
+#define MFA_FAST_POW 1
+#endif
+
+// x^n for the Phong specular term: 2^(n log2 x) with the ftz approximations
+// (no denormal fix-up sequences; x = 0 -> 0 for n > 0; a specular term below
+// 2^-126 is flushed to 0, far under the image tolerance)
+__device__ __forceinline__ float pow_spec(float x, float n) {
+#if MFA_FAST_POW
+    float l, r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(n * l));
+    return r;
+#else
+    return exp2f(n * __log2f(x));
+#endif
+}
+
 // Launch shape per instantiation (measured on B200):
 //   p <= 3 (neighbourhood cache, ~160-170 registers): 128-thread CTAs, >= 3 per SM
 //   p >= 4 (streamed slabs): 256-thread CTAs capped at 128 registers (2 per SM)
@@ -444,7 +462,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                         const float ndl = -fmaf(gx, L[0], fmaf(gy, L[1], gz * L[2])) * inv;  // N . L
                         const float ldv = -fmaf(L[0], dx, fmaf(L[1], dy, L[2] * dz));         // L . V
                         const float rv = fmaxf(fmaf(2.f * ndl, ndv, -ldv), 0.f);              // R . V
-                        float sp = args.shin == 0.f ? 1.f : exp2f(args.shin * __log2f(rv));
+                        float sp = args.shin == 0.f ? 1.f : pow_spec(rv, args.shin);
                         dif = fmaf(args.lights.intensity[l], fmaxf(ndl, 0.f), dif);
                         spe = fmaf(args.lights.intensity[l], ndl > 0.f ? sp : 0.f, spe);
                     }
@@ -463,7 +481,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 const float ndl = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * rsqrtf(fmaxf(n2, 1e-37f));
                 const float dif = fmaxf(ndl, 0.f);
                 const float rv = fmaxf(fmaf(2.f * ndl, ndl, -1.f), 0.f);
-                float spe = exp2f(args.shin * __log2f(rv));          // rv = 0 -> 0 (shin > 0)
+                float spe = pow_spec(rv, args.shin);                  // rv = 0 -> 0 (shin > 0)
                 if (args.shin == 0.f) spe = 1.f;                       // 0^0 = 1, as pow()
                 spe = ndl > 0.f ? spe : 0.f;
                 const float lit = zero ? args.ka : fmaf(args.kd, dif, args.ka);
