@@ -166,6 +166,9 @@ __device__ __forceinline__ float pow_spec(float x, float n) {
 #ifndef MFA_BEZ_CACHE
 #define MFA_BEZ_CACHE 1
 #endif
+#ifndef MFA_SMEM_FRAMES  // 1: per-view frames in shared memory (computed once per CTA)
+#define MFA_SMEM_FRAMES 0
+#endif
 #ifndef MFA_CARVEOUT     // -1: sized for MINB CTAs (default), else a fixed percentage
 #define MFA_CARVEOUT -1
 #endif
@@ -197,9 +200,13 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
     constexpr bool BEZ = LAYOUT == kBezier;
     constexpr bool CACHE = RenderShape<P, LAYOUT>::CACHE;
     extern __shared__ float4 s_tf[];
+#if MFA_SMEM_FRAMES
     __shared__ ViewFrame s_frame[kMaxViewsPerLaunch];
+#endif
 
+#if MFA_SMEM_FRAMES
     for (int v = threadIdx.x; v < args.n_views; v += blockDim.x) compute_frame(args.cams[v], s_frame[v]);
+#endif
     for (int i = threadIdx.x; i < args.tf_n; i += blockDim.x) s_tf[i] = __ldg(args.tf + i);
     __syncthreads();
 
@@ -249,7 +256,15 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             ty = (st / args.st_x) * 8 + (lt >> 3);
             if (tx >= args.tiles_x || ty >= args.tiles_y) continue;
         }
+#if MFA_SMEM_FRAMES
         const ViewFrame& fr = s_frame[view];
+#else
+        // the view's frame from its camera (kernel parameters, uniform across the
+        // warp): ~60 fp64 ops per 32 rays, and no shared memory, so the L1 keeps
+        // more of the unified 256 KB
+        ViewFrame fr;
+        compute_frame(args.cams[view], fr);
+#endif
         const int lx = (sub & 1) * 8 + (lane & 7);
         const int ly = (sub >> 1) * 4 + (lane >> 3);
         const int px = tx * MFA_TILE + lx, py = ty * MFA_TILE + ly;
