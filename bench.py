@@ -129,10 +129,14 @@ def cpu_oracle_sample(w, seconds: float, cfg_idx: int, nthreads=None):
     r = O.render(om, cam, w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
     dt = max(time.perf_counter() - t0, 1e-3)
     frac = min(1.0, frac * max(1.0, seconds / dt))
-    pix = WL.tile_subset(cfg_idx, cam.width, cam.height, frac)[0]
-    t0 = time.perf_counter()
-    r = O.render(om, cam, w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
-    dt = time.perf_counter() - t0
+    for _ in range(3):   # the calibration sample is small; re-size until the run lands near `seconds`
+        pix = WL.tile_subset(cfg_idx, cam.width, cam.height, frac)[0]
+        t0 = time.perf_counter()
+        r = O.render(om, cam, w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if dt >= 0.6 * seconds or frac >= 1.0:
+            break
+        frac = min(1.0, frac * seconds / max(dt, 1e-3))
     ns = int(r["count"].sum())
     desc = (f"{len(pix)} pixels ({frac * 100:.2f}% of the 16x16 tiles, seeded) of view 0 of {w.name}; "
             f"{ns} composited samples in {dt:.2f} s")

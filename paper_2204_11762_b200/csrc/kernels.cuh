@@ -563,9 +563,34 @@ __device__ __forceinline__ const float4* bez_block(const float4* Q, const BezGri
     return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Q) + b * BezBlock<P>::FLOATS);
 }
 
+#ifndef MFA_LDG256
+#define MFA_LDG256 1
+#endif
+
+// 32-byte vector load (sm_100: LDG.E.256): one full sector per lane
+__device__ __forceinline__ void ldg256(const float* p, float (&r)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
+}
+
 // slab c of a Bezier block: rows b = 0..P at consecutive compile-time offsets
+
 template <int P>
 __device__ __forceinline__ void load_bslab(const float4* __restrict__ q, float (&r)[P + 1][P + 1]) {
+#if MFA_LDG256
+    if constexpr (P == 3) {   // 64 bytes = two sector loads
+        const float* f = reinterpret_cast<const float*>(q);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            float x[8];
+            ldg256(f + 8 * k, x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) r[2 * k + (e >> 2)][e & 3] = x[e];
+        }
+        return;
+    }
+#endif
 #pragma unroll
     for (int b = 0; b <= P; ++b) {
         if constexpr (P == 1) {
@@ -586,6 +611,19 @@ __device__ __forceinline__ const float4* bslab_ptr(const float4* q, int c) {
 
 template <int P>
 __device__ __forceinline__ void load_bblock(const float4* __restrict__ q, float (&nb)[P + 1][P + 1][P + 1]) {
+#if MFA_LDG256
+    if constexpr (P == 3) {   // the 256-byte block as 8 sector loads (two rows each)
+        const float* f = reinterpret_cast<const float*>(q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            float r[8];
+            ldg256(f + 8 * k, r);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) nb[k >> 1][2 * (k & 1) + (e >> 2)][e & 3] = r[e];
+        }
+        return;
+    }
+#endif
 #pragma unroll
     for (int c = 0; c <= P; ++c) load_bslab<P>(bslab_ptr<P>(q, c), nb[c]);
 }
