@@ -28,6 +28,7 @@ struct AxisArgs {
     const float* kl;
     const long long* kfx;
     const int* bucket;
+    const longlong4* srec;
     int nsp;
     int M;
     int mshift;      // 62 - log2(M): bucket of a 2^62 fixed-point coordinate
@@ -45,6 +46,7 @@ __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
     a.kl = A.kl;
     a.kfx = A.kfx;
     a.bucket = A.bucket;
+    a.srec = A.srec;
     a.nsp = A.nsp;
     a.M = A.M;
     int lg = 0;
@@ -277,12 +279,28 @@ struct NUAxis {
     int s;
 };
 
+#ifndef MFA_SPAN_REC
+#define MFA_SPAN_REC 1
+#endif
+
 __device__ __forceinline__ void nu_load(const AxisArgs& A, NUAxis& st) {
     MFA_DCHECK(st.s >= 0 && st.s < A.nsp);
+#if MFA_SPAN_REC
+    // one 32-byte record: {lo, hi, bits(1/h), bits(tsc)} (model.cu span_rec_kernel)
+    long long r0, r1, r2, r3;
+    asm volatile("ld.global.nc.v4.s64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(r0), "=l"(r1), "=l"(r2), "=l"(r3)
+                 : "l"(A.srec + st.s));
+    st.lo = r0;
+    st.hi = r1;
+    st.invh = __int_as_float((int)r2);
+    st.tsc = __int_as_float((int)r3);
+#else
     st.lo = __ldg(A.kfx + st.s);
     st.hi = (st.s + 1 < A.nsp) ? __ldg(A.kfx + st.s + 1) : 0x7fffffffffffffffLL;
     st.invh = __ldg(A.invh + st.s);
     st.tsc = st.invh * A.dscale;
+#endif
 }
 
 __device__ __forceinline__ void nu_init(const AxisArgs& A, long long F, NUAxis& st) {

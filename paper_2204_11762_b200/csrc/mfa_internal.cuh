@@ -66,6 +66,7 @@ struct AxisTables {
     const float* kl = nullptr;        // [nsp+1]
     const long long* kfx = nullptr;   // [nsp+1]
     const int* bucket = nullptr;      // [M]
+    const longlong4* srec = nullptr;  // [nsp] render span records {lo, hi (2^62 fixed point), bits(invh), bits(tsc)}
     int nsp = 0;                      // n - p (number of knot spans incl. zero-length)
     int M = 0;                        // bucket count
     int ic_lo = 0, ic_hi = -1;        // uniform: spans [ic_lo, ic_hi] use the interior constants

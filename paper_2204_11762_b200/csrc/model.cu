@@ -138,6 +138,20 @@ __global__ void span_tables_kernel(const double* __restrict__ U, int p, int nsp,
         for (int m = 0; m <= p; ++m) out[a * (p + 1) + m] = (float)P[a][m];
 }
 
+// Render span records (non-uniform axes): one 32-byte record per span with
+// the bounds [lo, hi) in 2^62 fixed point (hi of the last span = INT64_MAX),
+// 1/h and the offset scale 2^(dshift-62)/h, so a span crossing is one sector
+// load (kernels.cuh nu_load).
+__global__ void span_rec_kernel(const long long* __restrict__ kfx, const float* __restrict__ invh, int nsp,
+                                float dscale, longlong4* __restrict__ rec) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nsp) return;
+    const float ih = invh[s];
+    rec[s] = make_longlong4(kfx[s], s + 1 < nsp ? kfx[s + 1] : 0x7fffffffffffffffLL,
+                            (long long)(unsigned)__float_as_int(ih),
+                            (long long)(unsigned)__float_as_int(ih * dscale));
+}
+
 // Bezier extraction operator of span s: N_{s+a}(t) = sum_j D[a][j] B_j(t) with
 // the Bernstein polynomials B_j(t) = C(p,j) t^j (1-t)^(p-j).  From the power
 // form: t^m = sum_{j>=m} C(j,m)/C(p,m) B_j(t).  All D >= 0 (convex weights).
@@ -378,7 +392,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
 
     // axis tables: one allocation
     const int rec = rec_floats(p);
-    size_t off[3][6];
+    size_t off[3][7];
     size_t total = 0;
     int Mb[3];
     auto bump = [&](size_t bytes) {
@@ -397,6 +411,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
         off[d][3] = bump(sizeof(float) * (nsp + 1));        // kl
         off[d][4] = bump(sizeof(long long) * (nsp + 1));    // kfx
         off[d][5] = bump(sizeof(int) * M);                  // bucket
+        off[d][6] = bump(sizeof(longlong4) * nsp);          // span records
     }
     size_t uoff[3];
     size_t utotal = 0;
@@ -434,6 +449,10 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
         const int nt = std::max(nsp + 1, Mb[d]);
         knot_tables_kernel<<<(nt + 255) / 256, 256, 0, st>>>(Ud, p, nsp, (float*)A.kh, (float*)A.kl,
                                                              (long long*)A.kfx, Mb[d], (int*)A.bucket);
+        A.srec = (longlong4*)(base + off[d][6]);
+        span_rec_kernel<<<(nsp + 127) / 128, 128, 0, st>>>((const long long*)A.kfx, (const float*)A.invh, nsp,
+                                                           ldexpf(1.0f, A.dshift - kNonUniFracBits),
+                                                           (longlong4*)A.srec);
         // uniform interior spans [p-1, S-p] share one polynomial set
         A.ic_lo = p - 1;
         A.ic_hi = nsp - p;
