@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) hessian_kernel(const __grid_constant__ He
                 if constexpr (BEZ)
                     load_bslab<P>(bslab_ptr<P>(base, c), r);
                 else
-                    load_slab<P>(base + c * (Brick<P>::EV * Brick<P>::EU), r);
+                    load_slab<P>(base + c * Brick<P>::SLAB, r);
                 float B[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int b = 0; b <= P; ++b) {

@@ -70,6 +70,9 @@ struct Brick {
     static constexpr int EV = B + P;
     static constexpr int EW = B + P;
     static constexpr int SIZE = EU * EV * EW;   // entries per brick
+    static constexpr int F4 = quad_f4(P);       // float4 per entry (row pairs for p <= 3)
+    static constexpr int ROW = EU * F4;         // float4 between rows b and b+1 of a slab
+    static constexpr int SLAB = EV * EU * F4;   // float4 between slabs c and c+1
 };
 
 struct BrickGrid {
@@ -77,7 +80,7 @@ struct BrickGrid {
     int64_t q_f4;          // size of the quad array in float4 (debug bounds checks)
 };
 
-// Entry index of the neighbourhood origin (row quad of spans (su, sv, sw)).
+// float4 offset of the neighbourhood origin (the entry of spans (su, sv, sw)).
 template <int P>
 __device__ __forceinline__ int64_t brick_entry(const BrickGrid& g, int su, int sv, int sw) {
     const int bx = su >> kBrickLog, by = sv >> kBrickLog, bz = sw >> kBrickLog;
@@ -85,8 +88,9 @@ __device__ __forceinline__ int64_t brick_entry(const BrickGrid& g, int su, int s
     const int brick = (bz * g.nby + by) * g.nbx + bx;
     const int64_t e = (int64_t)brick * Brick<P>::SIZE + (lw * Brick<P>::EV + lv) * Brick<P>::EU + lu;
     MFA_DCHECK(su >= 0 && sv >= 0 && sw >= 0 && e >= 0 &&
-               e + P * Brick<P>::EV * Brick<P>::EU + P * Brick<P>::EU + (P == 5 ? 5 : (P == 4 ? 2 : 1)) <= g.q_f4);
-    return e;
+               (e + P * Brick<P>::EV * Brick<P>::EU + P * Brick<P>::EU) * Brick<P>::F4 +
+                       (P == 5 ? 5 : (P == 4 ? 2 : Brick<P>::F4)) <= g.q_f4);
+    return e * Brick<P>::F4;
 }
 
 // ---------------------------------------------------------------------------
@@ -342,8 +346,32 @@ __device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis&
 // ---------------------------------------------------------------------------
 // a6: one slab c of the neighbourhood: rows b = 0..P, each P+1 u-values.
 // ---------------------------------------------------------------------------
+#ifndef MFA_LDG256
+#define MFA_LDG256 1
+#endif
+
+// 32-byte vector load (sm_100: LDG.E.256): one full sector per lane
+__device__ __forceinline__ void ldg256(const float* p, float (&r)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
+}
+
 template <int P>
 __device__ __forceinline__ void load_slab(const float4* __restrict__ q, float (&r)[P + 1][P + 1]) {
+    if constexpr (P <= 3) {   // row pairs: rows (0,1) and (2,3) are one 32-byte load each
+#pragma unroll
+        for (int b = 0; b <= P; b += 2) {
+            float x[8];
+            ldg256(reinterpret_cast<const float*>(q + b * Brick<P>::ROW), x);
+#pragma unroll
+            for (int a = 0; a <= P; ++a) {
+                r[b][a] = x[a];
+                if (b + 1 <= P) r[b + 1][a] = x[4 + a];
+            }
+        }
+        return;
+    }
     constexpr int EU = Brick<P>::EU;
 #pragma unroll
     for (int b = 0; b <= P; ++b) {
@@ -402,7 +430,7 @@ __device__ __forceinline__ void contract_vg(const float4* __restrict__ q, float 
                                             const float2 (&Bu)[P + 1], const float2 (&Bvs)[P + 1],
                                             const float2 (&Bw)[P + 1], float& val, float& gu, float& gv,
                                             float& gw) {
-    constexpr int SW = Brick<P>::EV * Brick<P>::EU;
+    constexpr int SW = Brick<P>::SLAB;
     float2 vw = make_float2(0.f, 0.f), gvu = make_float2(0.f, 0.f);
     float r1[P + 1][P + 1];
 #pragma unroll
@@ -425,7 +453,7 @@ template <int P>
 __device__ __forceinline__ float contract_v(const float4* __restrict__ q, float (&r0)[P + 1][P + 1],
                                             const float (&Nu)[P + 1], const float (&Nv)[P + 1],
                                             const float (&Nw)[P + 1]) {
-    constexpr int SW = Brick<P>::EV * Brick<P>::EU;
+    constexpr int SW = Brick<P>::SLAB;
     float val = 0.f;
     float r1[P + 1][P + 1];
 #pragma unroll
@@ -456,7 +484,7 @@ __device__ __forceinline__ float contract_v(const float4* __restrict__ q, float 
 // ---------------------------------------------------------------------------
 template <int P>
 __device__ __forceinline__ void load_block(const float4* __restrict__ q, float (&nb)[P + 1][P + 1][P + 1]) {
-    constexpr int SW = Brick<P>::EV * Brick<P>::EU;
+    constexpr int SW = Brick<P>::SLAB;
 #pragma unroll
     for (int c = 0; c <= P; ++c) load_slab<P>(q + c * SW, nb[c]);
 }
@@ -579,17 +607,6 @@ __device__ __forceinline__ const float4* bez_block(const float4* Q, const BezGri
     const int64_t b = ((int64_t)sw * g.S1 + sv) * g.S0 + su;
     MFA_DCHECK((b + 1) * (BezBlock<P>::FLOATS / 4) <= g.q_f4);
     return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Q) + b * BezBlock<P>::FLOATS);
-}
-
-#ifndef MFA_LDG256
-#define MFA_LDG256 1
-#endif
-
-// 32-byte vector load (sm_100: LDG.E.256): one full sector per lane
-__device__ __forceinline__ void ldg256(const float* p, float (&r)[8]) {
-    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
-                 : "l"(p));
 }
 
 // slab c of a Bezier block: rows b = 0..P at consecutive compile-time offsets

@@ -1,10 +1,10 @@
 // Internal declarations of libmfa (not part of the C ABI).
 //
 // Device layout of a model:
-//   Q        float4[n_w][n_v][n_u]: Q[k][j][i] = (P[k][j][i], P[k][j][i+1],
-//            P[k][j][i+2], P[k][j][i+3]) with zeros past n_u-1.  One aligned
-//            16-byte load fetches the p+1 <= 4 consecutive u-values of a row of
-//            the (p+1)^3 neighbourhood at any starting index ("row quads").
+//   Q        bricked row quads (kernels.cuh): the entry of (i, j, k) holds the
+//            quad (P[k][j][i], P[k][j][i+1], P[k][j][i+2], P[k][j][i+3]) -- for
+//            p <= 3 together with the quad of row j+1 (a 32-byte row PAIR, one
+//            256-bit load) -- with zeros past the grid; or Bezier blocks.
 //   per axis span tables (span s = knot interval [U[p+s], U[p+s+1]]):
 //     coef   float[nsp][REC]: power-basis coefficients of the p+1 non-zero
 //            basis functions on span s in the local coordinate
@@ -52,6 +52,10 @@ constexpr int kBrickLog = 4;        // bricks of 16x16x16 spans
 constexpr int kBrick = 1 << kBrickLog;
 constexpr int kQueueSlots = 256;    // persistent-kernel work counters (one per in-flight launch)
 __host__ __device__ constexpr int bez_row(int p) { return p == 1 ? 2 : 4; }  // floats per stored block row
+
+// float4 per brick entry: p <= 3 stores row PAIRS (rows j and j+1 of a quad
+// column, 32 bytes: one 256-bit load fetches two rows), p >= 4 single quads
+__host__ __device__ constexpr int quad_f4(int p) { return p <= 3 ? 2 : 1; }
 
 // brick entry extents for degree p (see kernels.cuh)
 __host__ __device__ constexpr int brick_eu(int p) { return kBrick + (p == 4 ? 1 : (p == 5 ? 4 : 0)); }

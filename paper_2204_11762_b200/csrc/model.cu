@@ -52,7 +52,7 @@ mfa_status check_device(const Model* m) {
 // (zeros outside the grid).  One thread per entry.
 // ---------------------------------------------------------------------------
 __global__ void relayout_bricks_kernel(const float* __restrict__ P, float4* __restrict__ Q, int nu, int nv,
-                                       int nw, int nbx, int nby, int EU, int EV, int EW, int64_t total) {
+                                       int nw, int nbx, int nby, int EU, int EV, int EW, int64_t total, int pairs) {
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t bsz = (int64_t)EU * EV * EW;
@@ -66,15 +66,23 @@ __global__ void relayout_bricks_kernel(const float* __restrict__ P, float4* __re
         const int by = (int)((brick / nbx) % nby);
         const int bz = (int)(brick / ((int64_t)nbx * nby));
         const int i = bx * kBrick + lu, j = by * kBrick + lv, k = bz * kBrick + lw;
-        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (j < nv && k < nw) {
-            const float* r = P + ((int64_t)k * nv + j) * nu;
-            if (i < nu) q.x = r[i];
-            if (i + 1 < nu) q.y = r[i + 1];
-            if (i + 2 < nu) q.z = r[i + 2];
-            if (i + 3 < nu) q.w = r[i + 3];
+        auto quad = [&](int jj) {
+            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (jj < nv && k < nw) {
+                const float* r = P + ((int64_t)k * nv + jj) * nu;
+                if (i < nu) q.x = r[i];
+                if (i + 1 < nu) q.y = r[i + 1];
+                if (i + 2 < nu) q.z = r[i + 2];
+                if (i + 3 < nu) q.w = r[i + 3];
+            }
+            return q;
+        };
+        if (pairs) {   // p <= 3: rows j and j+1 side by side (one 256-bit load, kernels.cuh load_slab)
+            Q[2 * idx] = quad(j);
+            Q[2 * idx + 1] = quad(j + 1);
+        } else {
+            Q[idx] = quad(j);
         }
-        Q[idx] = q;
     }
 }
 
@@ -507,12 +515,13 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
     if (!bez) {   // bricked row quads
         for (int d = 0; d < 3; ++d) m->nb[d] = (int)((nctrl[d] - p + kBrick - 1) / kBrick);
         const int EU = brick_eu(p), EV = brick_ev(p), EW = brick_ev(p);
-        const int64_t qn = (int64_t)m->nb[0] * m->nb[1] * m->nb[2] * EU * EV * EW;
-        if ((e = cudaMalloc(&m->Q, qn * sizeof(float4))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc Q"));
+        const int64_t qn = (int64_t)m->nb[0] * m->nb[1] * m->nb[2] * EU * EV * EW;   // entries
+        const int f4 = quad_f4(p);
+        if ((e = cudaMalloc(&m->Q, qn * f4 * sizeof(float4))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc Q"));
         relayout_bricks_kernel<<<4736, 256, 0, st>>>(Pdev, m->Q, (int)nu, (int)nv, (int)nw, m->nb[0], m->nb[1], EU, EV,
-                                                      EW, qn);
-        m->device_bytes += qn * (int64_t)sizeof(float4);
-        m->q_f4 = qn;
+                                                      EW, qn, f4 == 2);
+        m->device_bytes += qn * f4 * (int64_t)sizeof(float4);
+        m->q_f4 = qn * f4;
         m->layout = kQuads;
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(cuda_fail(e, "layout kernels"));
