@@ -55,7 +55,9 @@ __host__ __device__ constexpr int bez_row(int p) { return p == 1 ? 2 : 4; }  // 
 
 // float4 per brick entry: p <= 3 stores row PAIRS (rows j and j+1 of a quad
 // column, 32 bytes: one 256-bit load fetches two rows), p >= 4 single quads
+// (32-byte octets of one row measured 18% slower on C4: DESIGN.md §9)
 __host__ __device__ constexpr int quad_f4(int p) { return p <= 3 ? 2 : 1; }
+__host__ __device__ constexpr bool quad_pairs(int p) { return p <= 3; }
 
 // brick entry extents for degree p (see kernels.cuh)
 __host__ __device__ constexpr int brick_eu(int p) { return kBrick + (p == 4 ? 1 : (p == 5 ? 4 : 0)); }

@@ -77,7 +77,7 @@ __global__ void relayout_bricks_kernel(const float* __restrict__ P, float4* __re
             }
             return q;
         };
-        if (pairs) {   // p <= 3: rows j and j+1 side by side (one 256-bit load, kernels.cuh load_slab)
+        if (pairs == 1) {   // p <= 3: rows j and j+1 side by side (one 256-bit load, kernels.cuh load_slab)
             Q[2 * idx] = quad(j);
             Q[2 * idx + 1] = quad(j + 1);
         } else {
@@ -519,7 +519,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
         const int f4 = quad_f4(p);
         if ((e = cudaMalloc(&m->Q, qn * f4 * sizeof(float4))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc Q"));
         relayout_bricks_kernel<<<4736, 256, 0, st>>>(Pdev, m->Q, (int)nu, (int)nv, (int)nw, m->nb[0], m->nb[1], EU, EV,
-                                                      EW, qn, f4 == 2);
+                                                      EW, qn, quad_pairs(p) ? 1 : 0);
         m->device_bytes += qn * f4 * (int64_t)sizeof(float4);
         m->q_f4 = qn * f4;
         m->layout = kQuads;
