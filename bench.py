@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-eval", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--out-fp16", action="store_true")
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: direct NVLink stores into rank 0's image (p2p) or packed tiles + NCCL all-gather")
     ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier"],
                     help="control-point layout (default: the library's choice)")
     return ap.parse_args()
@@ -219,6 +221,18 @@ def run_ours(args):
 
         def step():
             m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, out=img, samples=cnt, out_fp16=args.out_fp16)
+    elif args.gather == "p2p":
+        # every rank's render kernel stores its pixels straight into rank 0's
+        # image over NVLink (CUDA IPC mapping): compute and transfer in one kernel
+        lists = D.assign_units(V, W, H, world)
+        mine = torch.from_numpy(lists[rank]).cuda()
+        img0 = torch.empty((V, H, W, 4), dtype=out_dt, device="cuda") if rank == 0 else None
+        img = D.peer_image(img0, rank)
+        launches_per_step = 1
+
+        def step():
+            m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=mine, out=img, samples=cnt,
+                     out_fp16=args.out_fp16, scatter=True)
     else:
         lists = D.assign_units(V, W, H, world)
         mine = torch.from_numpy(lists[rank]).cuda()
@@ -366,7 +380,9 @@ def run_ours(args):
                        "layout": info["layout"],
                        "shading": int(w.params.shading), "o_max": w.params.o_max,
                        "out": "fp16" if args.out_fp16 else "fp32",
-                       "parallelism": f"screen-tile sharding x{world}, model replicated, NCCL all-gather"
+                       "parallelism": (f"screen-tile sharding x{world}, model replicated, "
+                                       + ("render kernels store into rank 0's image over NVLink (CUDA IPC)"
+                                          if args.gather == "p2p" else "NCCL all-gather + unpack"))
                        if world > 1 else "single GPU",
                        "l2": f"inputs larger than L2: {info['layout']} control-point layout {info['device_bytes'] / 2**20:.0f} MiB, "
                              f"image {V * H * W * (8 if args.out_fp16 else 16) / 2**20:.0f} MiB per step"},

@@ -217,7 +217,13 @@ typedef struct {
 
 typedef struct {
     int64_t n_tiles;
-    const int32_t* tiles;      /* device, n_tiles x {view, tile_x, tile_y}, 16x16-pixel tiles */
+    const int32_t* tiles;      /* device, n_tiles x {view, tile_x, tile_y}, 16x16-pixel tiles;
+                                  view < 0 marks a padding entry (skipped) */
+    int32_t scatter;           /* 0: rgba_out is the packed [n_tiles][16][16][4] buffer;
+                                  1: each pixel is stored at its image position, rgba_out is
+                                  [n_views][H][W][4] -- which may be another GPU's image mapped
+                                  through CUDA IPC / peer access: the multi-GPU direct-store path
+                                  (stores travel over NVLink as the tiles finish; no gather) */
 } mfa_tiles;
 
 /*
@@ -225,8 +231,9 @@ typedef struct {
  * tf, prm     host structs (tf->rgba is a device pointer).
  * tiles       NULL: render every pixel; rgba_out is [n_views][H][W][4].
  *             non-NULL: render only the listed 16x16 tiles; rgba_out is the
- *             packed buffer [n_tiles][16][16][4] (pixels outside the image are
- *             left untouched).  Used for screen-tile sharding across GPUs.
+ *             packed buffer [n_tiles][16][16][4] (scatter = 0; pixels outside
+ *             the image are left untouched) or the full image (scatter = 1).
+ *             Used for screen-tile sharding across GPUs.
  * rgba_out    device buffer, fp32 or fp16 per prm->out_fp16.
  * samples_out optional device counter: += the number of composited samples
  *             (each sample up to and including the ERT sample).
@@ -407,6 +414,15 @@ typedef struct {
 mfa_status mfa_encode_grid(const int64_t dims[3], const float* values, const mfa_encode_config* cfg,
                            double* const knots_out[3], float* ctrl_out, mfa_encode_result* res,
                            double* round_log, mfa_stream stream);
+
+/*
+ * mfa_enable_peer_access -- let kernels on the current device load / store
+ * memory of peer_device (cudaDeviceEnablePeerAccess): the direct-store
+ * multi-GPU path writes rank 0's image (mapped through CUDA IPC) from every
+ * rank's render kernel over NVLink.  Same device or already enabled: MFA_OK;
+ * no P2P path between the devices: MFA_ERR_DEVICE.
+ */
+mfa_status mfa_enable_peer_access(int32_t peer_device);
 
 /* Thread-local message for the last non-OK status on this thread ("" if none). */
 const char* mfa_last_error(void);

@@ -25,7 +25,7 @@ EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_mod
            "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version",
            "mfa_render_field", "mfa_image_quality", "mfa_image_quality_workspace", "mfa_eval_hessian",
            "mfa_fit_grid", "mfa_encode_grid", "mfa_eval_batch_ws", "mfa_eval_workspace_bytes", "mfa_render_ex",
-           "mfa_eval_hessian_ws", "mfa_hessian_workspace_bytes",
+           "mfa_eval_hessian_ws", "mfa_hessian_workspace_bytes", "mfa_enable_peer_access",
            "mfa_probe_fp32", "mfa_probe_read_bw")
 
 
@@ -53,7 +53,7 @@ class RenderParams_t(C.Structure):
 
 
 class Tiles_t(C.Structure):
-    _fields_ = [("n_tiles", C.c_int64), ("tiles", C.c_void_p)]
+    _fields_ = [("n_tiles", C.c_int64), ("tiles", C.c_void_p), ("scatter", C.c_int32)]
 
 
 class ModelDesc_t(C.Structure):
@@ -129,6 +129,8 @@ def lib():
         L.mfa_encode_grid.restype = C.c_int
         L.mfa_encode_grid.argtypes = [C.POINTER(i64), vp, C.POINTER(EncodeConfig_t),
                                       C.POINTER(C.POINTER(C.c_double)), vp, C.POINTER(EncodeResult_t), vp, vp]
+        L.mfa_enable_peer_access.restype = C.c_int
+        L.mfa_enable_peer_access.argtypes = [i32]
         L.mfa_render_ex.restype = C.c_int
         L.mfa_render_ex.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
                                     C.POINTER(RenderExt_t), C.POINTER(Tiles_t), vp, vp, vp]
@@ -308,13 +310,15 @@ class Model:
 
     # -- Algorithm 1 (mfa_render) ---------------------------------------------
     def render(self, cams, tf, v_lo, v_hi, params, tiles=None, out=None, samples=None, out_fp16=False,
-               stream=None, field=None, lights=None):
+               stream=None, field=None, lights=None, scatter=False):
         """cams: list of Camera; tf: CUDA fp32 tensor (n,4); params: RenderParams.
         field: optional workloads.AnalyticField -- samples take their value
         and/or gradient from the analytic function (mfa_render_field; the
         ground-truth image when both come from it).  lights: optional
         [(direction towards the light, intensity), ...] replacing the
-        headlight (mfa_render_ex).
+        headlight (mfa_render_ex).  scatter (with tiles): store each pixel at
+        its image position in out ([V,H,W,4], possibly a peer GPU's image)
+        instead of a packed tile buffer.
         Returns the image [V,H,W,4] (or packed tiles [T,16,16,4] if tiles given)."""
         import torch
         tf = tf.contiguous()
@@ -325,8 +329,8 @@ class Model:
         W, H = cams[0].width, cams[0].height
         tl = None
         if tiles is not None:
-            tl = Tiles_t(tiles.shape[0], C.c_void_p(tiles.data_ptr()))
-            shape = (tiles.shape[0], TILE, TILE, 4)
+            tl = Tiles_t(tiles.shape[0], C.c_void_p(tiles.data_ptr()), int(bool(scatter)))
+            shape = (len(cams), H, W, 4) if scatter else (tiles.shape[0], TILE, TILE, 4)
         else:
             shape = (len(cams), H, W, 4)
         if out is None:
@@ -434,6 +438,12 @@ def encode_grid(values, degree: int, nctrl_init, e_max: float, max_rounds: int, 
     out = dict(nctrl=tuple(n), rounds=res.rounds, converged=bool(res.converged), max_err=res.max_err,
                rms_err=res.rms_err)
     return knots, ctrl[:n[0] * n[1] * n[2]].view(n[2], n[1], n[0]), out, log[:res.rounds].copy()
+
+
+def enable_peer_access(peer_device: int):
+    """Let kernels on the current device access memory of peer_device
+    (mfa_enable_peer_access; no-op if already enabled or the same device)."""
+    _check(lib().mfa_enable_peer_access(int(peer_device)))
 
 
 def version() -> str:

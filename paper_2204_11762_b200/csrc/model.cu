@@ -686,6 +686,21 @@ extern "C" mfa_status mfa_render_ex(mfa_model h, int32_t n_views, const mfa_came
     return launch_render(m, n_views, cams, tf, prm, tiles, rgba_out, samples_out, (cudaStream_t)stream, ext);
 }
 
+extern "C" mfa_status mfa_enable_peer_access(int32_t peer_device) {
+    int cur = -1, can = 0;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (peer_device == cur) return MFA_OK;
+    if ((e = cudaDeviceCanAccessPeer(&can, cur, peer_device)) != cudaSuccess) return cuda_fail(e, "cudaDeviceCanAccessPeer");
+    if (!can) return fail(MFA_ERR_DEVICE, "device " + std::to_string(cur) + " cannot access peer " + std::to_string(peer_device));
+    e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return MFA_OK;
+    }
+    return e == cudaSuccess ? MFA_OK : cuda_fail(e, "cudaDeviceEnablePeerAccess");
+}
+
 extern "C" mfa_status mfa_unpack_tiles(const void* packed, int32_t in_fp16, const int32_t* tiles, int64_t n_tiles,
                                        int32_t n_views, int32_t width, int32_t height, float* image_out,
                                        mfa_stream stream) {

@@ -106,12 +106,14 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         for (int v = 0; v < n_views; ++v) a->cams[v] = cams[v];
         a->n_views = n_views;
         a->tiles = tiles->tiles;
+        a->tile_scatter = tiles->scatter != 0;
         a->n_tiles = tiles->n_tiles;
         a->n_units = tiles->n_tiles * 8;
         a->view_base = 0;
         e = run();
     } else {
         a->tiles = nullptr;
+        a->tile_scatter = 0;
         a->n_tiles = 0;
         for (int v0 = 0; v0 < n_views && e == cudaSuccess; v0 += kMaxViewsPerLaunch) {
             const int nv = std::min(kMaxViewsPerLaunch, n_views - v0);

@@ -60,6 +60,7 @@ struct RenderArgs {
     int st_x, st_y;               // supertiles (8x8 tiles) per view, full-frame order
     int n_views;
     const int* tiles;             // NULL: full frames
+    int tile_scatter;             // tiles: 1 = write pixels at their image position, 0 = packed tiles
     int64_t n_tiles;
     int64_t n_units;              // warp units = 8 per tile
     int view_base;                // full frames: output view index of cams[0]
@@ -588,9 +589,10 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         // ---- a11: pixel write ---------------------------------------------
         if (valid) {
             int64_t idx;
-            if (args.tiles)
+            if (args.tiles && !args.tile_scatter)
                 idx = tile_id * (MFA_TILE * MFA_TILE) + ly * MFA_TILE + lx;
-            else
+            else   // full frame, or a tile list stored straight to its image position
+                   // (possibly a peer GPU's image: the multi-GPU direct-store path)
                 idx = ((int64_t)(args.view_base + view) * args.H + py) * args.W + px;
             if (args.out_fp16) {
                 __half2* o2 = reinterpret_cast<__half2*>(args.out) + 2 * idx;

@@ -8,11 +8,17 @@ parallelized").  The work unit is a (view, 16x16 tile).  Units are
 dealt round-robin to ranks along a diagonal order (each tile-row visited with
 its columns rotated by the row index), so counts differ by at most one and
 empty, cheap and ERT-heavy regions spread evenly.
-Each rank renders its units into a packed tile buffer; one collective
-(all_gather_into_tensor over equal, padded buffers; NCCL over NVLink /
-NVSwitch on GPUs) brings all tiles to every rank and rank 0 scatters them
-into the image with the unpack kernel.  Per-pixel arithmetic does not depend
-on the assignment, so the G-GPU image is bit-identical to the 1-GPU image.
+Two ways to bring the pixels to rank 0:
+  * "p2p" (default): rank 0's image is mapped into every rank through CUDA
+    IPC and the render kernel stores each finished pixel straight to its
+    position there (mfa_tiles.scatter = 1): the transfer is NVLink stores
+    issued by the compute kernel itself, overlapped with the rest of the
+    render -- no gather, no unpack (peer_image / render_direct);
+  * "nccl": each rank renders into a packed tile buffer; one
+    all_gather_into_tensor (NCCL over NVLink / NVSwitch) and rank 0's unpack
+    kernel (render_sharded).
+Per-pixel arithmetic does not depend on the assignment, so the G-GPU image
+is bit-identical to the 1-GPU image.
 """
 from __future__ import annotations
 
@@ -77,3 +83,44 @@ def render_sharded(render_tiles, unpack, n_views, width, height, rank, world, de
         return None, len(lists[rank])
     tiles_all = torch.from_numpy(np.concatenate(lists)).to(packed.device)
     return unpack(gathered, tiles_all), len(lists[rank])
+
+
+def peer_image(img, rank: int, group=None):
+    """CUDA-IPC view of rank 0's image on every rank (rank 0 gets img back).
+
+    Rank 0 exports the tensor with torch's CUDA IPC reductions; the others
+    rebuild it (the memory stays on rank 0's device) and enable peer access
+    from their own device, so their kernels can store into it over NVLink."""
+    import torch
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+    obj = [reduce_tensor(img) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if rank == 0:
+        return img
+    fn, args = obj[0]
+    cur = torch.cuda.current_device()
+    t = fn(*args)
+    torch.cuda.set_device(cur)
+    if t.device.index != cur:
+        from ._lib import enable_peer_access
+        enable_peer_access(t.device.index)
+    return t
+
+
+def render_direct(render_scatter, n_views, width, height, rank, world, peer_img, device=None, group=None):
+    """Direct-store sharding: this rank renders its units straight into rank
+    0's image (peer_img from peer_image).  render_scatter(tiles, out) launches
+    the render with scatter = 1.  After the call every rank's stores are
+    complete and visible to rank 0 (stream synchronisation + barrier)."""
+    import torch
+    import torch.distributed as dist
+    lists = assign_units(n_views, width, height, world)
+    mine = torch.from_numpy(lists[rank])
+    if device is not None:
+        mine = mine.to(device)
+    render_scatter(mine, peer_img)
+    torch.cuda.current_stream().synchronize()
+    if world > 1:
+        dist.barrier(group=group)
+    return peer_img if rank == 0 else None, len(lists[rank])
