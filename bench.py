@@ -514,13 +514,22 @@ def run_e2e(args, w, m, world, rank, local, out_dt):
     packed = torch.empty((len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
     gathered = torch.empty((world * len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
 
+    peer = D.peer_image(img, rank) if args.gather == "p2p" else None
+
     def step():
         tf_dev.copy_(tf_host, non_blocking=True)
-        m.render(w.cameras, tf_dev, w.v_lo, w.v_hi, w.params, tiles=mine, out=packed, samples=cnt,
-                 out_fp16=(out_dt == torch.float16))
-        dist.all_gather_into_tensor(gathered, packed)
+        if peer is not None:   # stores straight into rank 0's image over NVLink
+            m.render(w.cameras, tf_dev, w.v_lo, w.v_hi, w.params, tiles=mine, out=peer, samples=cnt,
+                     scatter=True)
+            torch.cuda.current_stream().synchronize()
+            dist.barrier()
+        else:
+            m.render(w.cameras, tf_dev, w.v_lo, w.v_hi, w.params, tiles=mine, out=packed, samples=cnt,
+                     out_fp16=(out_dt == torch.float16))
+            dist.all_gather_into_tensor(gathered, packed)
+            if rank == 0:
+                unpack_tiles(gathered, tiles_all, V, W, H, out=img)
         if rank == 0:
-            unpack_tiles(gathered, tiles_all, V, W, H, out=img)
             host.copy_(img, non_blocking=True)
     step()
     torch.cuda.synchronize()
@@ -535,7 +544,9 @@ def run_e2e(args, w, m, world, rank, local, out_dt):
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     dist.all_reduce(s, op=dist.ReduceOp.SUM)
     return {"value": int(s.item()) / float(dt.item()), "unit": UNIT, "h2d_bytes_per_step": tf_bytes + cam_bytes,
-            "d2h_bytes_per_step": V * H * W * 16, "api": "Model.render (tiles) + NCCL + unpack, host copies",
+            "d2h_bytes_per_step": V * H * W * 16,
+            "api": "Model.render (tiles) + " + ("NVLink stores into rank 0's image" if args.gather == "p2p"
+                                                 else "NCCL + unpack") + ", host copies",
             "steps": K, "timer": "wall clock, max over ranks"}
 
 
