@@ -26,8 +26,12 @@ struct EvalArgs {
     const int* pos;        // SORTED: sorted position of point i
 };
 
+#ifndef MFA_EVAL_MINB     // resident 256-thread CTAs per SM the register budget is sized for
+#define MFA_EVAL_MINB 1
+#endif
+
 template <int P, int LAYOUT, bool UNI, bool GRAD, bool SORTED>
-__global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalArgs args) {
+__global__ void __launch_bounds__(256, MFA_EVAL_MINB) eval_kernel(const __grid_constant__ EvalArgs args) {
     constexpr bool BEZ = LAYOUT == kBezier;
     unsigned errs = 0;
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < args.n;

@@ -167,6 +167,9 @@ __device__ __forceinline__ float pow_spec(float x, float n) {
 #ifndef MFA_BEZ_CACHE
 #define MFA_BEZ_CACHE 1
 #endif
+#ifndef MFA_LANE_STATS   // diagnostic build only
+#define MFA_LANE_STATS 0
+#endif
 #ifndef MFA_SMEM_FRAMES  // 1: per-view frames in shared memory (computed once per CTA)
 #define MFA_SMEM_FRAMES 0
 #endif
@@ -214,6 +217,9 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
     const int lane = threadIdx.x & 31;
     const int per_view = args.st_x * args.st_y * 64;   // units are ordered by 8x8-tile supertiles
     unsigned long long my_samples = 0;
+#if MFA_LANE_STATS
+    unsigned long long lane_slots = 0, lane_live = 0;
+#endif
 
     constexpr int kWarps = RenderShape<P, LAYOUT>::THREADS / 32;
     __shared__ unsigned s_tile;
@@ -556,6 +562,14 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             for (int i = 0; i < 3; ++i) F[i] += DF[i];
         }
         while (__any_sync(0xffffffffu, live)) {
+#if MFA_LANE_STATS   // diagnostic: warp-iterations x 32 and live lanes (samples[1], samples[2])
+            if (lane == 0) {
+                lane_slots += 32;
+                lane_live += __popc(__ballot_sync(0xffffffffu, live));
+            } else {
+                __ballot_sync(0xffffffffu, live);
+            }
+#endif
             if (live) {
                 if (k + 1 < K) {
                     int s[3];
@@ -607,6 +621,12 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
     if (args.samples) {
         my_samples = __reduce_add_sync(0xffffffffu, (unsigned)my_samples);
         if (lane == 0 && my_samples) atomicAdd(args.samples, my_samples);
+#if MFA_LANE_STATS
+        if (lane == 0) {
+            atomicAdd(args.samples + 1, lane_slots);
+            atomicAdd(args.samples + 2, lane_live);
+        }
+#endif
     }
 }
 
