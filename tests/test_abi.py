@@ -48,3 +48,29 @@ def test_sm100a_cubin():
     lib = build.build()
     out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib]).decode()
     assert "sm_100a" in out
+
+
+def test_synchronous_validation_of_next_entry_points():
+    """Argument validation happens before any device work (include/mfa.h
+    conventions), so these errors surface without a GPU."""
+    import ctypes as C
+    from paper_2204_11762_b200 import _lib
+    L = _lib.lib()
+    assert L.mfa_image_quality_workspace(10, 100) == 0          # below the 11x11 SSIM window
+    assert L.mfa_image_quality_workspace(11, 11) > 0
+    st = L.mfa_image_quality(5, 5, None, None, None, None, 0, None, None)
+    assert st == 1 and b"NULL" in L.mfa_last_error()
+    dims = (C.c_int64 * 3)(1, 8, 8)
+    nct = (C.c_int64 * 3)(4, 4, 4)
+    st = L.mfa_fit_grid(dims, C.c_void_p(1), 3, nct, None, C.c_void_p(1), None, None)
+    assert st == 1 and b"dims" in L.mfa_last_error()
+    dims = (C.c_int64 * 3)(8, 8, 8)
+    st = L.mfa_fit_grid(dims, C.c_void_p(1), 7, nct, None, C.c_void_p(1), None, None)
+    assert st == 3                                               # degree outside 1..5
+    st = L.mfa_encode_grid(dims, C.c_void_p(1), None, None, None, None, None, None)
+    assert st == 1
+    assert L.mfa_eval_workspace_bytes(None, 10) == 0 and L.mfa_hessian_workspace_bytes(None, 10) == 0
+    st = L.mfa_eval_hessian(None, 4, None, None, None, None, None, None, None, None)
+    assert st == 1 and b"model" in L.mfa_last_error()
+    st = L.mfa_render_ex(None, 1, None, None, None, None, None, None, None, None)
+    assert st == 1
