@@ -176,18 +176,30 @@ __device__ __forceinline__ void uniform_horner_value(float t, float (&N)[P + 1])
     }
 }
 
+__device__ __forceinline__ void ldg256(const float* p, float (&r)[8]);
+
 template <int P, bool SWAP>
 __device__ __forceinline__ void table_horner(const float* __restrict__ coef, int s, float t, float2 (&B)[P + 1]) {
     MFA_DCHECK(s >= 0);
     float c[rec_floats(P)];
-    const float4* r = reinterpret_cast<const float4*>(coef + (int64_t)s * rec_floats(P));
+    if constexpr (rec_floats(P) % 8 == 0) {   // p = 3: the 64-byte record as two sector loads
 #pragma unroll
-    for (int q = 0; q < rec_floats(P) / 4; ++q) {
-        const float4 x = __ldg(r + q);
-        c[4 * q + 0] = x.x;
-        c[4 * q + 1] = x.y;
-        c[4 * q + 2] = x.z;
-        c[4 * q + 3] = x.w;
+        for (int q = 0; q < rec_floats(P) / 8; ++q) {
+            float x[8];
+            ldg256(coef + (int64_t)s * rec_floats(P) + 8 * q, x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c[8 * q + e] = x[e];
+        }
+    } else {
+        const float4* r = reinterpret_cast<const float4*>(coef + (int64_t)s * rec_floats(P));
+#pragma unroll
+        for (int q = 0; q < rec_floats(P) / 4; ++q) {
+            const float4 x = __ldg(r + q);
+            c[4 * q + 0] = x.x;
+            c[4 * q + 1] = x.y;
+            c[4 * q + 2] = x.z;
+            c[4 * q + 3] = x.w;
+        }
     }
 #pragma unroll
     for (int a = 0; a <= P; ++a) {
