@@ -679,9 +679,10 @@ extern "C" mfa_status mfa_render_ex(mfa_model h, int32_t n_views, const mfa_came
     if (s != MFA_OK) return s;
     if (!tf || !tf->rgba || tf->n_entries < 2 || tf->n_entries > 1024 || !(tf->v_hi > tf->v_lo))
         return fail(MFA_ERR_INVALID_ARG, "tf: need rgba, 2 <= n_entries <= 1024, v_hi > v_lo");
-    if (!rgba_out) return fail(MFA_ERR_INVALID_ARG, "rgba_out is NULL");
     if (tiles && (tiles->n_tiles < 0 || (tiles->n_tiles > 0 && !tiles->tiles)))
         return fail(MFA_ERR_INVALID_ARG, "tiles: bad n_tiles / tiles pointer");
+    if (tiles && tiles->n_tiles == 0) return MFA_OK;   // an empty tile list is valid (nothing to do)
+    if (!rgba_out) return fail(MFA_ERR_INVALID_ARG, "rgba_out is NULL");
     if ((s = check_device(m)) != MFA_OK) return s;
     return launch_render(m, n_views, cams, tf, prm, tiles, rgba_out, samples_out, (cudaStream_t)stream, ext);
 }

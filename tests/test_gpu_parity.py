@@ -300,3 +300,64 @@ def test_nonuniform_multiple_knots(p):
         torch.cuda.synchronize()
         r = O.render(om, w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
         parity.check_image(img[0].cpu().numpy().reshape(-1, 4), r, f"double knot p={p} {layout} render")
+
+
+@pytest.mark.parametrize("p,n,uniform", [(1, 9, True), (5, 12, True), (5, 12, False), (4, 9, False), (2, 3, True),
+                                         (3, 4, False)])
+def test_render_degrees_and_single_span(p, n, uniform):
+    """Degrees outside the configs (1, 5), non-uniform p = 4 / 5 (quads +
+    span tables), and the single-span model n = p + 1 (every axis one span):
+    full-frame render and eval parity."""
+    from paper_2204_11762_b200 import Model
+    r = np.random.default_rng(100 * p + n)
+    knots = []
+    for d in range(3):
+        S = n - p
+        inner = np.arange(1, S) / S if uniform else np.sort(r.uniform(0.05, 0.95, S - 1))
+        knots.append(np.concatenate([np.zeros(p + 1), inner, np.ones(p + 1)]))
+    ctrl = r.uniform(0, 1, (n, n, n)).astype(np.float32)
+    w = WL.make_config(2, width=72, height=56)
+    w.degree, w.knots, w.ctrl, w.nctrl, w.uniform = p, knots, ctrl, (n, n, n), uniform
+    w.v_lo, w.v_hi = float(ctrl.min()), float(ctrl.max())
+    m = Model.from_workload(w)
+    om = O.Model.from_workload(w)
+    img = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params)
+    torch.cuda.synchronize()
+    ref = O.render(om, w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
+    parity.check_image(img[0].cpu().numpy().reshape(-1, 4), ref, f"p={p} n={n} uniform={uniform}")
+    u, v, ww = WL.query_points(2, 1 << 12)
+    got = gpu_eval(m, u, v, ww)
+    e, sg, _ = om.eval_batch(u, v, ww)
+    parity.check_eval(got, e, sg, f"p={p} n={n}")
+
+
+@pytest.mark.parametrize("o_max", [1.0, 0.5])
+def test_ert_threshold_variants(o_max):
+    """o_max = 1 disables early ray termination (every sample composited);
+    o_max = 0.5 terminates early; both against the oracle, and the sample
+    count with ERT off equals the sum of K over the rays."""
+    import dataclasses
+    c = 2
+    w = workload(c, width=128, height=96)
+    prm = dataclasses.replace(w.params, o_max=o_max)
+    m = gpu_model(c)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    img = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, prm, samples=cnt)
+    torch.cuda.synchronize()
+    ref = O.render(oracle_model(c), w.cameras[0], w.tf, w.v_lo, w.v_hi, prm)
+    parity.check_image(img[0].cpu().numpy().reshape(-1, 4), ref, f"o_max={o_max}")
+    tot = int(ref["count"].sum())
+    assert abs(int(cnt.item()) - tot) <= max(1, parity.count_window(ref))
+
+
+def test_empty_tile_list_and_padding_only():
+    c = 1
+    w = workload(c)
+    m = gpu_model(c)
+    out = torch.full((4, 16, 16, 4), 7.0, device="cuda")
+    empty = torch.zeros((0, 3), dtype=torch.int32, device="cuda")
+    m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params, tiles=empty, out=out[:0])
+    pad = torch.full((4, 3), -1, dtype=torch.int32, device="cuda")
+    m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params, tiles=pad, out=out)
+    torch.cuda.synchronize()
+    assert (out == 7.0).all()     # padding units are skipped: nothing written
