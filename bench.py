@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-eval", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--out-fp16", action="store_true")
+    ap.add_argument("--no-shading", action="store_true",
+                    help="NEXT-1: Algorithm 1 with ShadingOn = false (value-only basis and contraction)")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: direct NVLink stores into rank 0's image (p2p) or packed tiles + NCCL all-gather")
     ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier"],
@@ -205,6 +207,9 @@ def run_ours(args):
     c = int(args.workload[1:])
     kw = {"n_views": args.views} if args.views else {}
     w = WL.make_config(c, **kw)
+    if args.no_shading:
+        import dataclasses
+        w.params = dataclasses.replace(w.params, shading=0)
     V = len(w.cameras)
     W, H = w.cameras[0].width, w.cameras[0].height
     stream = torch.cuda.current_stream()
