@@ -57,7 +57,8 @@ class OrcParams(C.Structure):
                 ("kd", C.c_double), ("ks", C.c_double), ("shininess", C.c_double),
                 ("grad_eps", C.c_double), ("ert_window", C.c_double), ("exit_window", C.c_double),
                 ("sens_weight", C.c_double), ("sens_grad", C.c_double), ("n_lights", C.c_int32),
-                ("light_dir", C.POINTER(C.c_double)), ("light_intensity", C.POINTER(C.c_double))]
+                ("light_dir", C.POINTER(C.c_double)), ("light_intensity", C.POINTER(C.c_double)),
+                ("curv_n", C.c_int32), ("curv_rgba", C.POINTER(C.c_float)), ("curv_range", C.c_double)]
 
 
 _lib = None
@@ -87,6 +88,8 @@ def lib():
         _lib.orc_eval_hessian.argtypes = [C.POINTER(OrcModel), C.c_double, C.c_double, C.c_double, dp, dp]
         _lib.orc_eval_hessian_batch.restype = C.c_int64
         _lib.orc_eval_hessian_batch.argtypes = [C.POINTER(OrcModel), C.c_int64, fp, fp, fp, dp, dp, C.c_int32]
+        _lib.orc_curvatures.restype = None
+        _lib.orc_curvatures.argtypes = [dp, dp, dp]
         _lib.orc_field_eval.restype = C.c_int
         _lib.orc_field_eval.argtypes = [C.POINTER(OrcField), C.c_double, C.c_double, C.c_double, dp]
         _lib.orc_render_ex.restype = C.c_int
@@ -245,6 +248,16 @@ def make_field(field) -> OrcField:
     return f
 
 
+def curvatures(g, h6):
+    """C1: principal curvatures (k1 >= k2) from a gradient (3,) and Hessian
+    {xx, yy, zz, xy, xz, yz}."""
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    h = np.ascontiguousarray(h6, dtype=np.float64)
+    k = np.zeros(2)
+    lib().orc_curvatures(_dp(g), _dp(h), _dp(k))
+    return k
+
+
 def field_eval(field, u, v, w):
     """G1: analytic value and parameter-space gradient at (u, v, w)."""
     out = np.zeros(4)
@@ -255,7 +268,8 @@ def field_eval(field, u, v, w):
 
 
 def render(model: Model, cam, tf, v_lo, v_hi, params, pixels=None, nthreads=None,
-           ert_window=1e-4, exit_window=1e-6, sens_weight=1e-3, sens_grad=None, field=None, lights=None):
+           ert_window=1e-4, exit_window=1e-6, sens_weight=1e-3, sens_grad=None, field=None, lights=None,
+           curvature=None):
     """Render one view (all pixels, or a flat pixel-index list).  field (a
     workloads.AnalyticField) takes the value and/or gradient of each sample
     from the analytic function instead of the MFA (ground truth).
@@ -276,6 +290,11 @@ def render(model: Model, cam, tf, v_lo, v_hi, params, pixels=None, nthreads=None
     p.exit_window = exit_window
     p.sens_weight = sens_weight
     p.sens_grad = (100.0 * params.grad_eps) if sens_grad is None else sens_grad
+    if curvature is not None:   # (table float32 (n, n, 4) [kappa_2][kappa_1], range)
+        ctab = np.ascontiguousarray(curvature[0], dtype=np.float32)
+        p.curv_n = ctab.shape[0]
+        p.curv_rgba = ctab.ctypes.data_as(C.POINTER(C.c_float))
+        p.curv_range = float(curvature[1])
     if lights is not None:   # [(direction towards the light (3,), intensity), ...]
         ld = np.ascontiguousarray([l[0] for l in lights], dtype=np.float64).reshape(-1, 3)
         li = np.ascontiguousarray([l[1] for l in lights], dtype=np.float64)

@@ -26,6 +26,9 @@
  *                        triple sums                 P:78; SURVEY §8(f) NEXT-4
  *   L1 (in march)        several directional lights, Phong summed per light
  *                        P:307 "multiple light sources can be added"; R-30
+ *   C1 orc_curvatures    principal curvatures from gradient and Hessian, and
+ *                        a curvature transfer function in march (P:100
+ *                        "curvature-based transfer function"; R-31)
  *   G1 orc_field_eval    analytic ground truth (Eq. 1 Gaussian beam, Eq. 2
  *                        Marschner-Lobb) with analytic gradient
  *   G2 orc_render_ex     Algorithm 1 with value and/or gradient taken from the
@@ -83,6 +86,9 @@ typedef struct {
     int32_t n_lights;          /* L1: 0 -> the headlight (R-11); else directional lights (R-30) */
     const double* light_dir;   /*   [n_lights][3] world directions towards each light */
     const double* light_intensity; /* [n_lights] */
+    int32_t curv_n;            /* C1: 0 -> no curvature TF; else a curv_n x curv_n RGBA table */
+    const float* curv_rgba;    /*   [curv_n (kappa_2)][curv_n (kappa_1)][4], over [-curv_range, curv_range]^2 */
+    double curv_range;
 } orc_params;
 
 /* G1: analytic field (NEXT-2).  kind 1 = Gaussian beam (Eq. 1),  */
@@ -297,6 +303,66 @@ int orc_eval_hessian(const orc_model* m, double u, double v, double w, double ou
 }
 
 /* ------------------------------------------------------------------------ */
+/* C1: principal curvatures of the isosurface through a point from the      */
+/* physical gradient g and Hessian H (Kindlmann et al. 2003, the curvature-  */
+/* based transfer functions P:100 names): n = -g/|g|, P = I - n n^T,         */
+/* G = -P H P / |g|, T = trace G, F = |G|_F,                                 */
+/* kappa_1,2 = (T +- sqrt(2 F^2 - T^2)) / 2.  |g| = 0 -> (0, 0) (R-31).       */
+/* H is given as {h_xx, h_yy, h_zz, h_xy, h_xz, h_yz}.                        */
+/* ------------------------------------------------------------------------ */
+void orc_curvatures(const double g[3], const double h6[6], double k[2])
+{
+    const double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    if (!(gn > 0.0)) { k[0] = k[1] = 0.0; return; }
+    const double H[3][3] = {{h6[0], h6[3], h6[4]}, {h6[3], h6[1], h6[5]}, {h6[4], h6[5], h6[2]}};
+    double n[3], Pm[3][3], PH[3][3], G[3][3];
+    for (int i = 0; i < 3; ++i) n[i] = -g[i] / gn;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Pm[i][j] = (i == j ? 1.0 : 0.0) - n[i] * n[j];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double acc = 0.0;
+            for (int l = 0; l < 3; ++l) acc += Pm[i][l] * H[l][j];
+            PH[i][j] = acc;
+        }
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double acc = 0.0;
+            for (int l = 0; l < 3; ++l) acc += PH[i][l] * Pm[l][j];
+            G[i][j] = -acc / gn;
+        }
+    double T = G[0][0] + G[1][1] + G[2][2], F2 = 0.0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) F2 += G[i][j] * G[i][j];
+    double disc = 2.0 * F2 - T * T;
+    if (disc < 0.0) disc = 0.0;
+    k[0] = 0.5 * (T + sqrt(disc));
+    k[1] = 0.5 * (T - sqrt(disc));
+}
+
+/* C1: bilinear lookup of the curvature table at (kappa_1, kappa_2), clamped */
+static void curv_lookup(const orc_params* P, const double k[2], double out[4])
+{
+    const int n = P->curv_n;
+    double f[2];
+    int i0[2];
+    for (int d = 0; d < 2; ++d) {
+        double x = (k[d] + P->curv_range) / (2.0 * P->curv_range) * (n - 1);
+        if (x < 0.0) x = 0.0;
+        if (x > n - 1) x = n - 1;
+        i0[d] = (int)floor(x);
+        if (i0[d] > n - 2) i0[d] = n - 2;
+        f[d] = x - i0[d];
+    }
+    for (int c = 0; c < 4; ++c) {
+        const float* T = P->curv_rgba;
+        const double a00 = T[4 * (i0[1] * n + i0[0]) + c], a01 = T[4 * (i0[1] * n + i0[0] + 1) + c];
+        const double a10 = T[4 * ((i0[1] + 1) * n + i0[0]) + c], a11 = T[4 * ((i0[1] + 1) * n + i0[0] + 1) + c];
+        out[c] = (1.0 - f[1]) * ((1.0 - f[0]) * a00 + f[0] * a01) + f[1] * ((1.0 - f[0]) * a10 + f[0] * a11);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* G1: value and parameter-space gradient of the analytic field at the       */
 /* parameter point (u,v,w) in [0,1]^3.  The functions are defined on         */
 /* x, y, z in [-1, 1] ("The volume range of x, y, and z is [-1, 1]"),  */
@@ -481,6 +547,22 @@ static void march(const orc_ctx* cx, const double o[3], const double d[3], doubl
         }
         double col[4];
         apply_tf(cx->tf, vg[0], col);                        /* l.7 applyTFs */
+        if (P->curv_n > 0) {                                 /* C1: curvature TF modulates colour and opacity */
+            double hv[10], g[3], h[6], k[2], ct[4];
+            orc_eval_hessian(cx->m, q[0], q[1], q[2], hv, NULL);
+            for (int i = 0; i < 3; ++i) g[i] = hv[1 + i] / cx->L[i];
+            h[0] = hv[4] / (cx->L[0] * cx->L[0]);
+            h[1] = hv[5] / (cx->L[1] * cx->L[1]);
+            h[2] = hv[6] / (cx->L[2] * cx->L[2]);
+            h[3] = hv[7] / (cx->L[0] * cx->L[1]);
+            h[4] = hv[8] / (cx->L[0] * cx->L[2]);
+            h[5] = hv[9] / (cx->L[1] * cx->L[2]);
+            const double gn = sqrt(v_dot(g, g));
+            if (gn <= P->grad_eps) g[0] = g[1] = g[2] = 0.0;   /* zero gradient: no isosurface (R-31) */
+            orc_curvatures(g, h, k);
+            curv_lookup(P, k, ct);
+            for (int i = 0; i < 4; ++i) col[i] *= ct[i];
+        }
         double c[3] = {col[0], col[1], col[2]};
         const double a = col[3];
         double gnorm = 0.0;
