@@ -326,6 +326,17 @@ typedef struct {
     int32_t n_lights;
     const double* light_dir;
     const double* light_intensity;
+    /* curvature transfer function (Kindlmann et al.'s curvature-based TF, named
+       in P:100 as an application of the higher derivatives of P:78; R-31):
+       curv_rgba: device fp32 [curv_n][curv_n][4], indexed [kappa_2][kappa_1]
+       over [-curv_range, curv_range]^2 (bilinear, clamped); each sample's TF
+       colour and opacity are multiplied by it.  kappa_1 >= kappa_2 are the
+       principal curvatures (physical units) of the MFA's isosurface through
+       the sample, from the MFA gradient and Hessian (n = -g/|g|); a sample with
+       |g| <= grad_eps takes kappa = (0, 0).  curv_n = 0: off; else >= 2. */
+    const float* curv_rgba;
+    int32_t curv_n;
+    double curv_range;
 } mfa_render_ext;
 
 mfa_status mfa_render_ex(mfa_model m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,

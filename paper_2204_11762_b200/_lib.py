@@ -69,7 +69,8 @@ class Field_t(C.Structure):
 
 class RenderExt_t(C.Structure):
     _fields_ = [("field", C.POINTER(Field_t)), ("n_lights", C.c_int32), ("light_dir", C.POINTER(C.c_double)),
-                ("light_intensity", C.POINTER(C.c_double))]
+                ("light_intensity", C.POINTER(C.c_double)), ("curv_rgba", C.c_void_p), ("curv_n", C.c_int32),
+                ("curv_range", C.c_double)]
 
 
 class EncodeConfig_t(C.Structure):
@@ -310,7 +311,7 @@ class Model:
 
     # -- Algorithm 1 (mfa_render) ---------------------------------------------
     def render(self, cams, tf, v_lo, v_hi, params, tiles=None, out=None, samples=None, out_fp16=False,
-               stream=None, field=None, lights=None, scatter=False):
+               stream=None, field=None, lights=None, scatter=False, curvature=None):
         """cams: list of Camera; tf: CUDA fp32 tensor (n,4); params: RenderParams.
         field: optional workloads.AnalyticField -- samples take their value
         and/or gradient from the analytic function (mfa_render_field; the
@@ -318,7 +319,9 @@ class Model:
         [(direction towards the light, intensity), ...] replacing the
         headlight (mfa_render_ex).  scatter (with tiles): store each pixel at
         its image position in out ([V,H,W,4], possibly a peer GPU's image)
-        instead of a packed tile buffer.
+        instead of a packed tile buffer.  curvature: optional (CUDA fp32
+        table [n, n, 4] indexed [kappa_2][kappa_1], range) -- the curvature
+        transfer function of mfa_render_ex.
         Returns the image [V,H,W,4] (or packed tiles [T,16,16,4] if tiles given)."""
         import torch
         tf = tf.contiguous()
@@ -336,12 +339,15 @@ class Model:
         if out is None:
             out = torch.empty(shape, device=tf.device, dtype=dt)
         ext = None
-        if field is not None or lights:
+        if field is not None or lights or curvature is not None:
             ft = field_t(field) if field is not None else None
             ld = np.ascontiguousarray([l[0] for l in lights or []], dtype=np.float64).reshape(-1)
             li = np.ascontiguousarray([l[1] for l in lights or []], dtype=np.float64)
+            ctab, crange = (curvature[0].contiguous(), float(curvature[1])) if curvature is not None else (None, 0.0)
             ext = RenderExt_t(C.pointer(ft) if ft is not None else None, len(lights or []),
-                              ld.ctypes.data_as(C.POINTER(C.c_double)), li.ctypes.data_as(C.POINTER(C.c_double)))
+                              ld.ctypes.data_as(C.POINTER(C.c_double)), li.ctypes.data_as(C.POINTER(C.c_double)),
+                              C.c_void_p(ctab.data_ptr()) if ctab is not None else None,
+                              ctab.shape[0] if ctab is not None else 0, crange)
         _check(lib().mfa_render_ex(self._h, len(cams), ca, C.byref(tft), C.byref(pr),
                                    C.byref(ext) if ext is not None else None,
                                    C.byref(tl) if tl is not None else None, _ptr(out), _ptr(samples),

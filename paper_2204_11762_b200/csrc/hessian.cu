@@ -39,76 +39,6 @@ struct HessArgs {
     float4* out;         // SORTED: 3 float4 per sorted position (10 outputs + pad)
 };
 
-// Bernstein polynomials in power form: B_j(t) = sum_m c[j][m] t^m,
-// c[j][m] = C(P,j) C(P-j, m-j) (-1)^(m-j) for m >= j.
-template <int P>
-struct BernPower {
-    double c[P + 1][P + 1];
-};
-
-template <int P>
-constexpr BernPower<P> make_bern_power() {
-    BernPower<P> b{};
-    for (int j = 0; j <= P; ++j)
-        for (int m = j; m <= P; ++m) {
-            double cb = 1.0, cc = 1.0;
-            for (int i = 1; i <= j; ++i) cb = cb * (P - j + i) / i;            // C(P, j)
-            for (int i = 1; i <= m - j; ++i) cc = cc * (P - m + i) / i;        // C(P-j, m-j)
-            b.c[j][m] = (((m - j) & 1) ? -1.0 : 1.0) * cb * cc;
-        }
-    return b;
-}
-
-// f, f', f'' of sum_m c[m] t^m (synthetic division: f''/2 accumulates in d2)
-template <int P>
-__device__ __forceinline__ void horner3(const float (&c)[P + 1], float t, float& f, float& d1, float& d2) {
-    f = c[P];
-    d1 = 0.f;
-    d2 = 0.f;
-#pragma unroll
-    for (int m = P - 1; m >= 0; --m) {
-        d2 = fmaf(d2, t, d1);
-        d1 = fmaf(d1, t, f);
-        f = fmaf(f, t, c[m]);
-    }
-    d2 *= 2.f;
-}
-
-template <int P, int LAYOUT, bool UNI>
-__device__ __forceinline__ void basis3(const AxisArgs& A, int s, float t, float (&N)[P + 1], float (&D1)[P + 1],
-                                       float (&D2)[P + 1]) {
-    if constexpr (LAYOUT == kBezier) {
-        constexpr BernPower<P> BP = make_bern_power<P>();
-#pragma unroll
-        for (int a = 0; a <= P; ++a) {
-            float c[P + 1];
-#pragma unroll
-            for (int m = 0; m <= P; ++m) c[m] = (float)BP.c[a][m];
-            horner3<P>(c, t, N[a], D1[a], D2[a]);
-        }
-    } else {
-        if (UNI && s >= A.ic_lo && s <= A.ic_hi) {
-            constexpr UniformBasis<P> UB = make_uniform_basis<P>();
-#pragma unroll
-            for (int a = 0; a <= P; ++a) {
-                float c[P + 1];
-#pragma unroll
-                for (int m = 0; m <= P; ++m) c[m] = (float)UB.c[a][m];
-                horner3<P>(c, t, N[a], D1[a], D2[a]);
-            }
-        } else {
-            const float* rec = A.coef + (int64_t)s * rec_floats(P);
-#pragma unroll
-            for (int a = 0; a <= P; ++a) {
-                float c[P + 1];
-#pragma unroll
-                for (int m = 0; m <= P; ++m) c[m] = __ldg(rec + a * (P + 1) + m);
-                horner3<P>(c, t, N[a], D1[a], D2[a]);
-            }
-        }
-    }
-}
-
 template <int P, int LAYOUT, bool UNI, bool SORTED>
 __global__ void __launch_bounds__(256) hessian_kernel(const __grid_constant__ HessArgs args) {
     constexpr bool BEZ = LAYOUT == kBezier;

@@ -356,6 +356,151 @@ __device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis&
 }
 
 // ---------------------------------------------------------------------------
+// Second derivatives (mfa_eval_hessian, and the curvature transfer function of
+// the extended render): per axis (N, N', N'') by a three-output Horner scheme
+// on power-basis coefficients, and the value / gradient / Hessian contraction
+// of one slab.
+// ---------------------------------------------------------------------------
+// Bernstein polynomials in power form: B_j(t) = sum_m c[j][m] t^m,
+// c[j][m] = C(P,j) C(P-j, m-j) (-1)^(m-j) for m >= j.
+template <int P>
+struct BernPower {
+    double c[P + 1][P + 1];
+};
+
+template <int P>
+constexpr BernPower<P> make_bern_power() {
+    BernPower<P> b{};
+    for (int j = 0; j <= P; ++j)
+        for (int m = j; m <= P; ++m) {
+            double cb = 1.0, cc = 1.0;
+            for (int i = 1; i <= j; ++i) cb = cb * (P - j + i) / i;            // C(P, j)
+            for (int i = 1; i <= m - j; ++i) cc = cc * (P - m + i) / i;        // C(P-j, m-j)
+            b.c[j][m] = (((m - j) & 1) ? -1.0 : 1.0) * cb * cc;
+        }
+    return b;
+}
+
+// f, f', f'' of sum_m c[m] t^m (synthetic division: f''/2 accumulates in d2)
+template <int P>
+__device__ __forceinline__ void horner3(const float (&c)[P + 1], float t, float& f, float& d1, float& d2) {
+    f = c[P];
+    d1 = 0.f;
+    d2 = 0.f;
+#pragma unroll
+    for (int m = P - 1; m >= 0; --m) {
+        d2 = fmaf(d2, t, d1);
+        d1 = fmaf(d1, t, f);
+        f = fmaf(f, t, c[m]);
+    }
+    d2 *= 2.f;
+}
+
+template <int P, int LAYOUT, bool UNI>
+__device__ __forceinline__ void basis3(const AxisArgs& A, int s, float t, float (&N)[P + 1], float (&D1)[P + 1],
+                                       float (&D2)[P + 1]) {
+    if constexpr (LAYOUT == kBezier) {
+        constexpr BernPower<P> BP = make_bern_power<P>();
+#pragma unroll
+        for (int a = 0; a <= P; ++a) {
+            float c[P + 1];
+#pragma unroll
+            for (int m = 0; m <= P; ++m) c[m] = (float)BP.c[a][m];
+            horner3<P>(c, t, N[a], D1[a], D2[a]);
+        }
+    } else {
+        if (UNI && s >= A.ic_lo && s <= A.ic_hi) {
+            constexpr UniformBasis<P> UB = make_uniform_basis<P>();
+#pragma unroll
+            for (int a = 0; a <= P; ++a) {
+                float c[P + 1];
+#pragma unroll
+                for (int m = 0; m <= P; ++m) c[m] = (float)UB.c[a][m];
+                horner3<P>(c, t, N[a], D1[a], D2[a]);
+            }
+        } else {
+            const float* rec = A.coef + (int64_t)s * rec_floats(P);
+#pragma unroll
+            for (int a = 0; a <= P; ++a) {
+                float c[P + 1];
+#pragma unroll
+                for (int m = 0; m <= P; ++m) c[m] = __ldg(rec + a * (P + 1) + m);
+                horner3<P>(c, t, N[a], D1[a], D2[a]);
+            }
+        }
+    }
+}
+
+// One slab c of the (value, gradient, Hessian) contraction (hessian.cu
+// documents the 3 / 6 / 10 sum structure); out = {v, v_u, v_v, v_w, v_uu,
+// v_vv, v_ww, v_uv, v_uw, v_vw} in t-space, accumulated.
+template <int P>
+__device__ __forceinline__ void contract_vgh_slab(const float (&r)[P + 1][P + 1], const float (&Nu)[P + 1],
+                                                  const float (&Du)[P + 1], const float (&Eu)[P + 1],
+                                                  const float (&Nv)[P + 1], const float (&Dv)[P + 1],
+                                                  const float (&Ev)[P + 1], float nw, float dw, float ew,
+                                                  float (&out)[10]) {
+    float B[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int b = 0; b <= P; ++b) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
+        for (int a = 0; a <= P; ++a) {
+            a0 = fmaf(Nu[a], r[b][a], a0);
+            a1 = fmaf(Du[a], r[b][a], a1);
+            a2 = fmaf(Eu[a], r[b][a], a2);
+        }
+        B[0] = fmaf(Nv[b], a0, B[0]);
+        B[1] = fmaf(Nv[b], a1, B[1]);
+        B[2] = fmaf(Dv[b], a0, B[2]);
+        B[3] = fmaf(Nv[b], a2, B[3]);
+        B[4] = fmaf(Dv[b], a1, B[4]);
+        B[5] = fmaf(Ev[b], a0, B[5]);
+    }
+    out[0] = fmaf(nw, B[0], out[0]);
+    out[1] = fmaf(nw, B[1], out[1]);
+    out[2] = fmaf(nw, B[2], out[2]);
+    out[3] = fmaf(dw, B[0], out[3]);
+    out[4] = fmaf(nw, B[3], out[4]);
+    out[5] = fmaf(nw, B[5], out[5]);
+    out[6] = fmaf(ew, B[0], out[6]);
+    out[7] = fmaf(nw, B[4], out[7]);
+    out[8] = fmaf(dw, B[1], out[8]);
+    out[9] = fmaf(dw, B[2], out[9]);
+}
+
+// principal curvatures from a physical gradient g and Hessian h = {xx, yy, zz,
+// xy, xz, yz} (Kindlmann et al. 2003; R-31): n = -g/|g|, P = I - n n^T,
+// G = -P H P / |g|, kappa = (T +- sqrt(2|G|_F^2 - T^2)) / 2
+__device__ __forceinline__ void curvatures(const float (&g)[3], const float (&h)[6], float& k1, float& k2) {
+    const float g2 = fmaf(g[0], g[0], fmaf(g[1], g[1], g[2] * g[2]));
+    const float inv = rsqrtf(fmaxf(g2, 1e-37f));
+    const float n[3] = {-g[0] * inv, -g[1] * inv, -g[2] * inv};
+    const float H[3][3] = {{h[0], h[3], h[4]}, {h[3], h[1], h[5]}, {h[4], h[5], h[2]}};
+    float Pm[3][3], PH[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Pm[i][j] = (i == j ? 1.f : 0.f) - n[i] * n[j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) PH[i][j] = fmaf(Pm[i][0], H[0][j], fmaf(Pm[i][1], H[1][j], Pm[i][2] * H[2][j]));
+    float T = 0.f, F2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const float Gij = -fmaf(PH[i][0], Pm[0][j], fmaf(PH[i][1], Pm[1][j], PH[i][2] * Pm[2][j])) * inv;
+            if (i == j) T += Gij;
+            F2 = fmaf(Gij, Gij, F2);
+        }
+    const float sd = sqrtf(fmaxf(fmaf(2.f, F2, -T * T), 0.f));
+    k1 = 0.5f * (T + sd);
+    k2 = 0.5f * (T - sd);
+}
+
+// ---------------------------------------------------------------------------
 // a6: one slab c of the neighbourhood: rows b = 0..P, each P+1 u-values.
 // ---------------------------------------------------------------------------
 #ifndef MFA_LDG256

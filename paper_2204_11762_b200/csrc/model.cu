@@ -649,7 +649,7 @@ extern "C" mfa_status mfa_render(mfa_model h, int32_t n_views, const mfa_camera*
 extern "C" mfa_status mfa_render_field(mfa_model h, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                                        const mfa_render_params* prm, const mfa_field* field, const mfa_tiles* tiles,
                                        void* rgba_out, unsigned long long* samples_out, mfa_stream stream) {
-    mfa_render_ext ext{field, 0, nullptr, nullptr};
+    mfa_render_ext ext{field, 0, nullptr, nullptr, nullptr, 0, 0.0};
     return mfa_render_ex(h, n_views, cams, tf, prm, &ext, tiles, rgba_out, samples_out, stream);
 }
 
@@ -674,6 +674,8 @@ extern "C" mfa_status mfa_render_ex(mfa_model h, int32_t n_views, const mfa_came
                 return fail(MFA_ERR_INVALID_ARG, "light " + std::to_string(l) + ": zero or non-finite direction/intensity");
         }
     }
+    if (ext && ext->curv_n && (ext->curv_n < 2 || !ext->curv_rgba || !(ext->curv_range > 0.0)))
+        return fail(MFA_ERR_INVALID_ARG, "curvature TF: need curv_n >= 2, a table and curv_range > 0");
     const Model* m = reinterpret_cast<const Model*>(h);
     mfa_status s = validate_render(m, n_views, cams, prm);
     if (s != MFA_OK) return s;

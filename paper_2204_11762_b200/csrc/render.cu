@@ -31,8 +31,16 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     const mfa_field* fld = ext ? ext->field : nullptr;
     const bool field = fld && (fld->value_src || fld->grad_src);
     const bool lights = ext && ext->n_lights > 0;
+    const bool curv = ext && ext->curv_n > 0;
     a->fld.vsrc = a->fld.gsrc = 0;
     a->lights.n = 0;
+    a->curv.n = 0;
+    if (curv) {
+        a->curv.tab = reinterpret_cast<const float4*>(ext->curv_rgba);
+        a->curv.n = ext->curv_n;
+        a->curv.range = (float)ext->curv_range;
+        a->curv.scale = (float)((ext->curv_n - 1) / (2.0 * ext->curv_range));
+    }
     if (lights) {
         a->lights.n = ext->n_lights;
         for (int l = 0; l < ext->n_lights; ++l) {
@@ -95,7 +103,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         a->queue = m->queue + (g_slot.fetch_add(1) % kQueueSlots);
         cudaError_t r = cudaMemsetAsync(a->queue, 0, sizeof(unsigned int), st);
         if (r != cudaSuccess) return r;
-        return (field || lights) ? dispatch_render_ext(*a, m->p, m->layout, uni, shade, st)
+        return (field || lights || curv) ? dispatch_render_ext(*a, m->p, m->layout, uni, shade, st)
                      : dispatch_render_main(*a, m->p, m->layout, uni, shade, st);
     };
     if (tiles) {

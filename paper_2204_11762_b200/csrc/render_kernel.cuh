@@ -70,6 +70,11 @@ struct RenderArgs {
     unsigned long long* samples;
     FieldArgs fld;                // used by the EXT instantiations only
     LightArgs lights;             // used by the EXT instantiations only
+    struct {                      // curvature transfer function (EXT only; R-31)
+        const float4* tab;        // [n][n] RGBA, [kappa_2][kappa_1]
+        int n;                    // 0: off
+        float scale, range;       // index = (kappa + range) * scale, scale = (n - 1) / (2 range)
+    } curv;
     mfa_camera cams[kMaxViewsPerLaunch];
 };
 
@@ -456,7 +461,8 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         };
         // a8-a10 for one queried sample, branch-free (so it can interleave
         // with the next sample's query)
-        auto shade_composite = [&](float val, float gu, float gv, float gw, const float (&gs)[3]) {
+        auto shade_composite = [&](float val, float gu, float gv, float gw, const float (&gs)[3], float k1,
+                                   float k2) {
             // a8: transfer function (l.7)
             float f = (val - args.v_lo) * args.s_scale;
             f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
@@ -471,7 +477,25 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             float cr = fmaf(wt, T1.x - T0.x, T0.x);
             float cg = fmaf(wt, T1.y - T0.y, T0.y);
             float cb = fmaf(wt, T1.z - T0.z, T0.z);
-            const float a = fmaf(wt, T1.w - T0.w, T0.w);
+            float a = fmaf(wt, T1.w - T0.w, T0.w);
+            if constexpr (EXT) {   // curvature TF: bilinear in (kappa_1, kappa_2), modulates colour and opacity
+                if (args.curv.n > 0) {
+                    const float x = fminf(fmaxf((k1 + args.curv.range) * args.curv.scale, 0.f), (float)(args.curv.n - 1));
+                    const float y = fminf(fmaxf((k2 + args.curv.range) * args.curv.scale, 0.f), (float)(args.curv.n - 1));
+                    const int ix = min((int)x, args.curv.n - 2), iy = min((int)y, args.curv.n - 2);
+                    const float fx = x - (float)ix, fy = y - (float)iy;
+                    const float4* T = args.curv.tab + (int64_t)iy * args.curv.n + ix;
+                    const float4 a00 = __ldg(T), a01 = __ldg(T + 1), a10 = __ldg(T + args.curv.n),
+                                 a11 = __ldg(T + args.curv.n + 1);
+                    auto bl = [&](float p00, float p01, float p10, float p11) {
+                        return fmaf(fy, fmaf(fx, p11 - p10, p10) - fmaf(fx, p01 - p00, p00), fmaf(fx, p01 - p00, p00));
+                    };
+                    cr *= bl(a00.x, a01.x, a10.x, a11.x);
+                    cg *= bl(a00.y, a01.y, a10.y, a11.y);
+                    cb *= bl(a00.z, a01.z, a10.z, a11.z);
+                    a *= bl(a00.w, a01.w, a10.w, a11.w);
+                }
+            }
             // a9: Phong with a headlight (l.10-11; R-11); zero gradient -> ambient
             bool lit_done = false;
             if constexpr (SHADE && EXT) {
@@ -523,6 +547,42 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             A += wgt;
         };
 
+        // curvature TF (EXT): principal curvatures of the MFA's isosurface at the
+        // sample from its gradient and Hessian (t-space, scaled by the MFA's gs)
+        auto curv_query = [&](const int (&s)[3], const float (&t)[3], const float (&gsm)[3], float& k1, float& k2) {
+            float Nu[P + 1], Du[P + 1], Eu[P + 1], Nv[P + 1], Dv[P + 1], Ev[P + 1], Nw[P + 1], Dw[P + 1], Ew[P + 1];
+            constexpr int BL = BEZ ? kBezier : kQuads;
+            basis3<P, BL, UNI>(args.ax[0], s[0], t[0], Nu, Du, Eu);
+            basis3<P, BL, UNI>(args.ax[1], s[1], t[1], Nv, Dv, Ev);
+            basis3<P, BL, UNI>(args.ax[2], s[2], t[2], Nw, Dw, Ew);
+            float o[10];
+#pragma unroll
+            for (int q = 0; q < 10; ++q) o[q] = 0.f;
+            if constexpr (CACHE) {
+                fetch(s);
+#pragma unroll
+                for (int c = 0; c <= P; ++c) contract_vgh_slab<P>(nb[c], Nu, Du, Eu, Nv, Dv, Ev, Nw[c], Dw[c], Ew[c], o);
+            } else {
+#pragma unroll
+                for (int c = 0; c <= P; ++c) {
+                    float r[P + 1][P + 1];
+                    if constexpr (BEZ)
+                        load_bslab<P>(bslab_ptr<P>(bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]), c), r);
+                    else
+                        load_slab<P>(args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]) + c * Brick<P>::SLAB, r);
+                    contract_vgh_slab<P>(r, Nu, Du, Eu, Nv, Dv, Ev, Nw[c], Dw[c], Ew[c], o);
+                }
+            }
+            const float g[3] = {o[1] * gsm[0], o[2] * gsm[1], o[3] * gsm[2]};
+            const float h[6] = {o[4] * gsm[0] * gsm[0], o[5] * gsm[1] * gsm[1], o[6] * gsm[2] * gsm[2],
+                                o[7] * gsm[0] * gsm[1], o[8] * gsm[0] * gsm[2], o[9] * gsm[1] * gsm[2]};
+            if (fmaf(g[0], g[0], fmaf(g[1], g[1], g[2] * g[2])) <= args.eps2) {   // no isosurface (R-31)
+                k1 = k2 = 0.f;
+            } else {
+                curvatures(g, h, k1, k2);
+            }
+        };
+
         // NEXT-2 (EXT instantiations): the sample takes its value and/or its
         // gradient from the analytic field at the same parameter point
         auto sample_field = [&](const int (&s)[3], const float (&t)[3], float& v, float& g0, float& g1, float& g2,
@@ -548,11 +608,13 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         // two-stage pipeline: iteration k queries sample k+1 while it shades
         // and composites sample k; the ERT test (l.14-15; R-13) follows.
         float val = 0.f, gu = 0.f, gv = 0.f, gw = 0.f, gs[3] = {0.f, 0.f, 0.f};
+        float ck1 = 0.f, ck2 = 0.f;   // curvatures of the sample being shaded (EXT curvature TF)
         if (live) {
             int s[3];
             float t[3];
             locate(s, t, gs);
             if constexpr (EXT) {
+                if (args.curv.n > 0) curv_query(s, t, gs, ck1, ck2);
                 sample_field(s, t, val, gu, gv, gw, gs);
             } else {
                 fetch(s);
@@ -577,11 +639,15 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                     locate(s, t, gs1);
                     float val1 = 0.f, gu1 = 0.f, gv1 = 0.f, gw1 = 0.f;
                     if constexpr (EXT) {
-                        shade_composite(val, gu, gv, gw, gs);
+                        float nk1 = 0.f, nk2 = 0.f;
+                        if (args.curv.n > 0) curv_query(s, t, gs1, nk1, nk2);
+                        shade_composite(val, gu, gv, gw, gs, ck1, ck2);
                         sample_field(s, t, val1, gu1, gv1, gw1, gs1);
+                        ck1 = nk1;
+                        ck2 = nk2;
                     } else {
                         fetch(s);
-                        shade_composite(val, gu, gv, gw, gs);
+                        shade_composite(val, gu, gv, gw, gs, 0.f, 0.f);
                         query(s, t, val1, gu1, gv1, gw1);
                     }
                     val = val1;
@@ -594,7 +660,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                         F[i] += DF[i];
                     }
                 } else {
-                    shade_composite(val, gu, gv, gw, gs);
+                    shade_composite(val, gu, gv, gw, gs, ck1, ck2);
                 }
                 ++k;
                 live = !(A > args.o_max) && k < K;

@@ -156,3 +156,39 @@ def test_single_headlight_light_equals_default():
     b = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params, lights=[(-d, 1.0)])
     torch.cuda.synchronize()
     assert np.abs(a.cpu().numpy() - b.cpu().numpy()).max() <= 1e-6
+
+
+def curvature_table(n=16, seed=3):
+    r = np.random.default_rng(seed)
+    k = np.linspace(0, 1, n)
+    t = np.empty((n, n, 4), np.float32)
+    for c in range(4):   # smooth: low-order polynomial in (kappa_1, kappa_2) plus a tiny seeded term
+        a, b, d = r.uniform(-0.3, 0.3, 3)
+        t[:, :, c] = np.clip(0.6 + a * k[None, :] + b * k[:, None] + d * np.outer(k, k), 0.05, 1.0)
+    return t
+
+
+@pytest.mark.parametrize("c,layout", [(2, "auto"), (5, "auto"), (4, "auto"), (5, "quads")])
+def test_curvature_tf_parity(c, layout):
+    """Curvature transfer function (mfa_render_ex, R-31; oracle C1): the
+    GPU's fp32 gradient / Hessian / principal curvatures / bilinear table
+    against the fp64 oracle, on uniform quads (C2), the Bezier layout (C5),
+    streamed p = 4 slabs (C4) and non-uniform quads (C5)."""
+    from paper_2204_11762_b200 import Model
+    kw = dict(width=96, height=72, n_views=1)
+    if c == 4:
+        kw["nctrl"] = (40, 40, 40)
+    if c == 5:
+        kw["nctrl"] = (96, 32, 32)
+    w = WL.make_config(c, **kw)
+    m = Model.from_workload(w, layout=layout)
+    om = O.Model.from_workload(w)
+    tab = curvature_table()
+    rng = {2: 60.0, 4: 80.0, 5: 120.0}[c]
+    img = m.render(w.cameras[:1], cuda(w.tf), w.v_lo, w.v_hi, w.params, curvature=(cuda(tab), rng))
+    torch.cuda.synchronize()
+    ref = O.render(om, w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params, curvature=(tab, rng))
+    st = parity.check_image(img[0].cpu().numpy().reshape(-1, 4), ref, f"C{c} {layout} curvature TF")
+    plain = O.render(om, w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
+    assert np.abs(plain["rgba"] - ref["rgba"]).max() > 1e-2      # the table really modulates the image
+    print(c, layout, st)
