@@ -238,7 +238,9 @@ typedef struct {
  * samples_out optional device counter: += the number of composited samples
  *             (each sample up to and including the ERT sample).
  * Deterministic: a pixel's value does not depend on tiling, view batching or
- * launch configuration.
+ * launch configuration.  Each launch takes one of 256 work-counter slots of
+ * the model in turn: at most 256 renders of one model may be in flight at a
+ * time (across all streams).
  */
 mfa_status mfa_render(mfa_model m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                       const mfa_render_params* prm, const mfa_tiles* tiles, void* rgba_out,
@@ -388,8 +390,10 @@ mfa_status mfa_image_quality(int32_t width, int32_t height, const float* img_a, 
  *             device fp64 copy.  A knot layout that leaves a basis function
  *             without samples makes the normal equations singular:
  *             MFA_ERR_INVALID_ARG naming the axis.  Scratch is allocated
- *             internally (not a render-path call); returns after the stream
- *             is synchronised.
+ *             internally (not a render-path call) from the device's default
+ *             stream-ordered memory pool, whose release threshold is raised to
+ *             8 GiB once per device so repeated fits / refinement rounds reuse
+ *             it; returns after the stream is synchronised.
  */
 mfa_status mfa_fit_grid(const int64_t dims[3], const float* values, int32_t degree, const int64_t nctrl[3],
                         const double* const knots[3], float* ctrl_out, double* ctrl_out64, mfa_stream stream);
