@@ -164,7 +164,7 @@ static cudaError_t dispatch_eval(const EvalArgs& a, int layout, bool uni, bool g
 // Random points gather their (p+1)^3 neighbourhoods from random places: each
 // point touches ~16 separate 128-byte lines of a grid far larger than L2, so
 // the kernel is HBM-bound on over-fetched lines (C3: ~1.5 KB of DRAM reads per
-// point).  Grouping the points by a coarse parameter-space bin (about 16^3
+// point).  Grouping the points by a coarse parameter-space bin (about 8^3
 // knot spans per bin; bin = floor(u * NB) per axis) makes the points a CTA
 // processes share neighbourhoods, which then come from L1/L2: a counting sort
 // (per-CTA shared-memory histogram, one scan, an atomic-cursor scatter of
@@ -172,6 +172,10 @@ static cudaError_t dispatch_eval(const EvalArgs& a, int layout, bool uni, bool g
 // result at its original index.  The result of a point does not depend on
 // its position in the order, so outputs stay deterministic.
 // ---------------------------------------------------------------------------
+#ifndef MFA_BIN_SPANS    // knot spans per bin edge
+#define MFA_BIN_SPANS 8
+#endif
+
 struct BinGrid {
     int nb[3];
     int nbins;   // nb0 * nb1 * nb2; points outside [0,1]^3 (or NaN) go to bin nbins
@@ -263,7 +267,7 @@ static BinGrid make_bins(const Model* m) {
     int64_t total = 1;
     for (int d = 0; d < 3; ++d) {
         const int64_t S = m->n[d] - m->p;
-        g.nb[d] = (int)std::max<int64_t>(1, (S + 15) / 16);
+        g.nb[d] = (int)std::max<int64_t>(1, (S + MFA_BIN_SPANS - 1) / MFA_BIN_SPANS);
         total *= g.nb[d];
     }
     while (total > (1 << 22)) {   // keep the bin table small
