@@ -172,6 +172,9 @@ static cudaError_t dispatch_eval(const EvalArgs& a, int layout, bool uni, bool g
 // result at its original index.  The result of a point does not depend on
 // its position in the order, so outputs stay deterministic.
 // ---------------------------------------------------------------------------
+#ifndef MFA_CURSOR_STRIDE  // unsigned words between scatter cursors (8: one 32-byte sector each)
+#define MFA_CURSOR_STRIDE 8
+#endif
 #ifndef MFA_BIN_SPANS    // knot spans per bin edge
 #define MFA_BIN_SPANS 8
 #endif
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const unsigned* __restri
     }
     unsigned run = part[threadIdx.x] - s;
     for (int b = b0; b < b1; ++b) {
-        cursor[b] = run;
+        cursor[(size_t)b * MFA_CURSOR_STRIDE] = run;
         run += counts[b];
     }
 }
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(const float* __restric
                                                           int* __restrict__ bins, unsigned* __restrict__ cursor,
                                                           float4* __restrict__ rec) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned pos = atomicAdd(cursor + bins[i], 1u);
+        const unsigned pos = atomicAdd(cursor + (size_t)bins[i] * MFA_CURSOR_STRIDE, 1u);
         rec[pos] = make_float4(__ldg(u + i), __ldg(v + i), __ldg(w + i), __int_as_float((int)i));
         bins[i] = (int)pos;
     }
@@ -281,7 +284,8 @@ static BinGrid make_bins(const Model* m) {
 size_t bin_workspace_bytes(const Model* m, int64_t n) {
     const BinGrid g = make_bins(m);
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    return up(sizeof(int) * (size_t)n) + up(sizeof(float4) * (size_t)n) + 2 * up(sizeof(unsigned) * (g.nbins + 1));
+    return up(sizeof(int) * (size_t)n) + up(sizeof(float4) * (size_t)n) + up(sizeof(unsigned) * (g.nbins + 1)) +
+           up(sizeof(unsigned) * (g.nbins + 1) * MFA_CURSOR_STRIDE);
 }
 
 size_t eval_workspace_bytes(const Model* m, int64_t n) { return bin_workspace_bytes(m, n); }
