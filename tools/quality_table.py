@@ -24,7 +24,7 @@ ap.add_argument("--degrees", type=int, nargs="+", default=[2, 3])
 ap.add_argument("--ratio", type=float, nargs="+", default=[0.25, 0.5, 0.9], help="control points per data point per axis")
 a = ap.parse_args()
 
-print("data  p  nctrl  test      MSE       PSNR(dB)  SSIM")
+print("data  p  nctrl  test      MSE       PSNR(dB)  SSIM     render G samples/s (MFA image, device time)")
 for m in a.data:
     q = torch.from_numpy(WL.analytic_grid("ml", (m, m, m)).astype(np.float32)).cuda()
     for p in a.degrees:
@@ -49,5 +49,15 @@ for m in a.data:
                 img = model.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, field=f_mfa)
                 tru = model.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, field=f_true)
                 res = image_quality(img[0], tru[0])
-                print(f"{m:4d}^3 {p}  {n:4d}^3 {test:9s} {res['mse']:9.2f} {res['psnr']:9.2f} {res['ssim']:7.4f}")
+                # per-sample query cost (Fig. 12 methodology): the plain MFA render
+                cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                model.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, out=img)
+                e0.record()
+                for _ in range(5):
+                    model.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, out=img, samples=cnt)
+                e1.record()
+                torch.cuda.synchronize()
+                rate = int(cnt.item()) / (e0.elapsed_time(e1) / 1e3) / 1e9
+                print(f"{m:4d}^3 {p}  {n:4d}^3 {test:9s} {res['mse']:9.2f} {res['psnr']:9.2f} {res['ssim']:7.4f}  {rate:6.2f}")
                 del model
