@@ -361,3 +361,22 @@ def test_empty_tile_list_and_padding_only():
     m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params, tiles=pad, out=out)
     torch.cuda.synchronize()
     assert (out == 7.0).all()     # padding units are skipped: nothing written
+
+
+def test_more_than_64_views_and_tf_sizes():
+    """n_views > 64 is split into launches of <= 64 views (mfa_render); TF
+    tables of 2 and 1024 entries (the ABI's limits) against the oracle."""
+    c = 1
+    w = WL.make_config(c, width=24, height=20, n_views=70)
+    m = gpu_model(c)
+    img, _ = render_gpu(c, w=w)
+    for v in (0, 63, 64, 69):
+        ref = O.render(oracle_model(c), w.cameras[v], w.tf, w.v_lo, w.v_hi, w.params)
+        parity.check_image(img[v].reshape(-1, 4), ref, f"view {v} of 70")
+    for n in (2, 1024):
+        x = np.linspace(0, 1, n)
+        tf = np.stack([x, 1 - x, np.full(n, 0.4), 0.05 + 0.05 * np.sin(7 * x) ** 2], axis=1).astype(np.float32)
+        out = m.render(w.cameras[:1], cuda(tf), w.v_lo, w.v_hi, w.params)
+        torch.cuda.synchronize()
+        ref = O.render(oracle_model(c), w.cameras[0], tf, w.v_lo, w.v_hi, w.params)
+        parity.check_image(out[0].cpu().numpy().reshape(-1, 4), ref, f"TF with {n} entries")
