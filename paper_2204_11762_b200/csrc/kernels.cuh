@@ -298,13 +298,16 @@ struct NUAxis {
 #ifndef MFA_SPAN_REC
 #define MFA_SPAN_REC 1
 #endif
+#ifndef MFA_NU_SPLIT
+#define MFA_NU_SPLIT 1
+#endif
 
 __device__ __forceinline__ void nu_load(const AxisArgs& A, NUAxis& st) {
     MFA_DCHECK(st.s >= 0 && st.s < A.nsp);
 #if MFA_SPAN_REC
     // one 32-byte record: {lo, hi, bits(1/h), bits(tsc)} (model.cu span_rec_kernel)
     long long r0, r1, r2, r3;
-    asm volatile("ld.global.nc.v4.s64 {%0,%1,%2,%3}, [%4];"
+    asm("ld.global.nc.v4.s64 {%0,%1,%2,%3}, [%4];"
                  : "=l"(r0), "=l"(r1), "=l"(r2), "=l"(r3)
                  : "l"(A.srec + st.s));
     st.lo = r0;
@@ -350,6 +353,33 @@ __device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis&
         }
     }
     int d = (int)((F - st.lo) >> A.dshift);     // < 2^23 inside the span
+    d = min(max(d, 0), 8388607);
+    const float fd = __int_as_float(0x4b000000 | d) - 8388608.0f;
+    return fd * st.tsc;
+}
+
+// nu_span in two phases (MFA_NU_SPLIT, the render default): first every axis
+// moves into its neighbouring span and issues the record load (predicated, no
+// branch), then every axis consumes its record, so the crossings of the three
+// axes wait for one load round trip instead of three (C5 +6 %).
+__device__ __forceinline__ void nu_cross(const AxisArgs& A, long long F, NUAxis& st) {
+    const bool fwd = F >= st.hi;
+    const bool bwd = F < st.lo && st.s > 0;
+    if (fwd || bwd) {
+        st.s += fwd ? 1 : -1;
+        nu_load(A, st);
+    }
+}
+
+__device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxis& st) {
+    if (F >= st.hi || (F < st.lo && st.s > 0)) {   // rare: crossed more than one span this step
+        int s = st.s;
+        while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
+        while (s > 0 && F < __ldg(A.kfx + s)) --s;
+        st.s = s;
+        nu_load(A, st);
+    }
+    int d = (int)((F - st.lo) >> A.dshift);
     d = min(max(d, 0), 8388607);
     const float fd = __int_as_float(0x4b000000 | d) - 8388608.0f;
     return fd * st.tsc;

@@ -366,20 +366,6 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         float nb[CACHE ? P + 1 : 1][P + 1][P + 1];   // cached neighbourhood (CACHE)
         int64_t nb_key = -1;
 
-        // a4: span + local coordinate per axis of the sample at F
-        auto locate = [&](int (&s)[3], float (&t)[3], float (&gs)[3]) {
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                if (UNI) {
-                    uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
-                    gs[i] = args.gsc[i];
-                } else {
-                    t[i] = nu_span(args.ax[i], F[i], nu[i]);
-                    s[i] = nu[i].s;
-                    gs[i] = nu[i].invh * args.gsc[i];
-                }
-            }
-        };
         // a6: make the neighbourhood of span triple s resident (CACHE layouts)
         auto fetch = [&](const int (&s)[3]) {
             if constexpr (BEZ && CACHE) {
@@ -393,6 +379,33 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 if (e != nb_key) {
                     load_block<P>(args.Q + e, nb);
                     nb_key = e;
+                }
+            }
+        };
+        // a4: span + local coordinate per axis of the sample at F
+        auto locate = [&](int (&s)[3], float (&t)[3], float (&gs)[3]) {
+#if MFA_NU_SPLIT
+            if constexpr (!UNI) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) nu_cross(args.ax[i], F[i], nu[i]);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    t[i] = nu_finish(args.ax[i], F[i], nu[i]);
+                    s[i] = nu[i].s;
+                    gs[i] = nu[i].invh * args.gsc[i];
+                }
+                return;
+            }
+#endif
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (UNI) {
+                    uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
+                    gs[i] = args.gsc[i];
+                } else {
+                    t[i] = nu_span(args.ax[i], F[i], nu[i]);
+                    s[i] = nu[i].s;
+                    gs[i] = nu[i].invh * args.gsc[i];
                 }
             }
         };
