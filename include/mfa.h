@@ -439,6 +439,25 @@ mfa_status mfa_encode_grid(const int64_t dims[3], const float* values, const mfa
  */
 mfa_status mfa_enable_peer_access(int32_t peer_device);
 
+/*
+ * mfa_ipc_open -- map another process's device allocation into the CURRENT
+ * device's address space (cudaIpcOpenMemHandle with
+ * cudaIpcMemLazyEnablePeerAccess), for the direct-store multi-GPU path: every
+ * rank maps rank 0's image allocation on its own device, so its render kernel
+ * stores into it over NVLink (or locally when both are the same device).
+ * handle     host, the 64-byte cudaIpcMemHandle_t of the exporting process's
+ *            allocation (e.g. torch's UntypedStorage._share_cuda_()[1]).
+ * base_out   receives the device address of the allocation's first byte in
+ *            this process (add the exporter's byte offset of the tensor).
+ * The mapping stays until mfa_ipc_close(base).  NULL arguments:
+ * MFA_ERR_INVALID_ARG; a handle this process cannot map (same process, no
+ * P2P path, bad handle): MFA_ERR_CUDA with the CUDA error text.
+ */
+mfa_status mfa_ipc_open(const void* handle, void** base_out);
+
+/* mfa_ipc_close -- unmap an allocation mapped by mfa_ipc_open. */
+mfa_status mfa_ipc_close(void* base);
+
 /* Thread-local message for the last non-OK status on this thread ("" if none). */
 const char* mfa_last_error(void);
 

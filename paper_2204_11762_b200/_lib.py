@@ -26,7 +26,7 @@ EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_mod
            "mfa_render_field", "mfa_image_quality", "mfa_image_quality_workspace", "mfa_eval_hessian",
            "mfa_fit_grid", "mfa_encode_grid", "mfa_eval_batch_ws", "mfa_eval_workspace_bytes", "mfa_render_ex",
            "mfa_eval_hessian_ws", "mfa_hessian_workspace_bytes", "mfa_enable_peer_access",
-           "mfa_probe_fp32", "mfa_probe_read_bw")
+           "mfa_ipc_open", "mfa_ipc_close", "mfa_probe_fp32", "mfa_probe_read_bw")
 
 
 class MfaError(RuntimeError):
@@ -132,6 +132,10 @@ def lib():
                                       C.POINTER(C.POINTER(C.c_double)), vp, C.POINTER(EncodeResult_t), vp, vp]
         L.mfa_enable_peer_access.restype = C.c_int
         L.mfa_enable_peer_access.argtypes = [i32]
+        L.mfa_ipc_open.restype = C.c_int
+        L.mfa_ipc_open.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        L.mfa_ipc_close.restype = C.c_int
+        L.mfa_ipc_close.argtypes = [C.c_void_p]
         L.mfa_render_ex.restype = C.c_int
         L.mfa_render_ex.argtypes = [vp, i32, C.POINTER(Camera_t), C.POINTER(TF_t), C.POINTER(RenderParams_t),
                                     C.POINTER(RenderExt_t), C.POINTER(Tiles_t), vp, vp, vp]
@@ -450,6 +454,28 @@ def enable_peer_access(peer_device: int):
     """Let kernels on the current device access memory of peer_device
     (mfa_enable_peer_access; no-op if already enabled or the same device)."""
     _check(lib().mfa_enable_peer_access(int(peer_device)))
+
+
+class PeerBuffer:
+    """A device buffer of another process mapped on the current device
+    (mfa_ipc_open): data_ptr() for the entry points, shape / dtype for the
+    caller; close() unmaps it."""
+
+    def __init__(self, handle: bytes, offset: int, shape, dtype):
+        base = C.c_void_p(0)
+        _check(lib().mfa_ipc_open(bytes(handle), C.byref(base)))
+        self._base = base.value
+        self._ptr = base.value + int(offset)
+        self.shape = tuple(shape)
+        self.dtype = dtype
+
+    def data_ptr(self) -> int:
+        return self._ptr
+
+    def close(self):
+        if self._base:
+            _check(lib().mfa_ipc_close(C.c_void_p(self._base)))
+            self._base = self._ptr = 0
 
 
 def version() -> str:

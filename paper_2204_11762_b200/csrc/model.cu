@@ -15,6 +15,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -702,6 +703,21 @@ extern "C" mfa_status mfa_enable_peer_access(int32_t peer_device) {
         return MFA_OK;
     }
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "cudaDeviceEnablePeerAccess");
+}
+
+extern "C" mfa_status mfa_ipc_open(const void* handle, void** base_out) {
+    if (!handle || !base_out) return fail(MFA_ERR_INVALID_ARG, "mfa_ipc_open: NULL handle or base_out");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    *base_out = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? MFA_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+extern "C" mfa_status mfa_ipc_close(void* base) {
+    if (!base) return fail(MFA_ERR_INVALID_ARG, "mfa_ipc_close: NULL base");
+    const cudaError_t e = cudaIpcCloseMemHandle(base);
+    return e == cudaSuccess ? MFA_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
 }
 
 extern "C" mfa_status mfa_unpack_tiles(const void* packed, int32_t in_fp16, const int32_t* tiles, int64_t n_tiles,

@@ -85,27 +85,40 @@ def render_sharded(render_tiles, unpack, n_views, width, height, rank, world, de
     return unpack(gathered, tiles_all), len(lists[rank])
 
 
-def peer_image(img, rank: int, group=None):
-    """CUDA-IPC view of rank 0's image on every rank (rank 0 gets img back).
+def ipc_handle_bytes(h: bytes) -> bytes:
+    """The 64-byte cudaIpcMemHandle_t inside torch's shareable handle: raw
+    (older torch) or prefixed by a version byte and the segment type 'c'
+    (a cudaMalloc segment).  Expandable segments carry no cudaIpc handle."""
+    if len(h) == 64:
+        return h
+    if len(h) == 66 and h[1:2] == b"c":
+        return h[2:]
+    raise RuntimeError(f"unsupported CUDA IPC handle from torch (length {len(h)}, type {h[1:2]!r}); "
+                       "the direct-store path needs the default (non-expandable) CUDA allocator")
 
-    Rank 0 exports the tensor with torch's CUDA IPC reductions; the others
-    rebuild it (the memory stays on rank 0's device) and enable peer access
-    from their own device, so their kernels can store into it over NVLink."""
-    import torch
+
+def peer_image(img, rank: int, group=None):
+    """Rank 0's image on every rank: rank 0 gets img back, the others a
+    _lib.PeerBuffer mapping it on their OWN device.
+
+    Rank 0 exports the image's allocation (the CUDA IPC handle and the
+    tensor's byte offset in it, from torch's storage sharing); every other
+    rank maps it with mfa_ipc_open on its current device
+    (cudaIpcMemLazyEnablePeerAccess), so its render kernel stores into rank
+    0's HBM over NVLink -- or locally when both ranks share one device."""
     import torch.distributed as dist
-    from torch.multiprocessing.reductions import reduce_tensor
-    obj = [reduce_tensor(img) if rank == 0 else None]
+    if rank == 0:
+        st = img.untyped_storage()
+        info = st._share_cuda_()          # (device, handle, size, offset in the allocation, ...)
+        meta = (ipc_handle_bytes(bytes(info[1])), int(info[3]) + img.storage_offset() * img.element_size(),
+                tuple(img.shape), str(img.dtype))
+    obj = [meta if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     if rank == 0:
         return img
-    fn, args = obj[0]
-    cur = torch.cuda.current_device()
-    t = fn(*args)
-    torch.cuda.set_device(cur)
-    if t.device.index != cur:
-        from ._lib import enable_peer_access
-        enable_peer_access(t.device.index)
-    return t
+    handle, offset, shape, dtype = obj[0]
+    from ._lib import PeerBuffer
+    return PeerBuffer(handle, offset, shape, dtype)
 
 
 def render_direct(render_scatter, n_views, width, height, rank, world, peer_img, device=None, group=None):

@@ -74,3 +74,5 @@ def test_synchronous_validation_of_next_entry_points():
     assert st == 1 and b"model" in L.mfa_last_error()
     st = L.mfa_render_ex(None, 1, None, None, None, None, None, None, None, None)
     assert st == 1
+    assert L.mfa_ipc_open(None, None) == 1 and b"NULL" in L.mfa_last_error()
+    assert L.mfa_ipc_close(None) == 1

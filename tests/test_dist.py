@@ -93,3 +93,15 @@ def test_render_sharded_gloo_world2(V, W, H):
         np.testing.assert_array_equal(img[v, :, :, 1], xs)
         np.testing.assert_array_equal(img[v, :, :, 2], ys)
         np.testing.assert_array_equal(img[v, :, :, 3], 1.0)
+
+
+def test_ipc_handle_bytes():
+    """torch's shareable handle -> the raw 64-byte cudaIpcMemHandle_t."""
+    import pytest
+    raw = bytes(range(64))
+    assert D.ipc_handle_bytes(raw) == raw
+    assert D.ipc_handle_bytes(b"\x01c" + raw) == raw
+    with pytest.raises(RuntimeError):
+        D.ipc_handle_bytes(b"\x01e" + raw)
+    with pytest.raises(RuntimeError):
+        D.ipc_handle_bytes(raw[:10])

@@ -1,8 +1,9 @@
 """GPU tests of the multi-GPU direct-store path (dist.peer_image
 / render_direct): the render kernel stores a tile list's pixels at their image
 positions (mfa_tiles.scatter), into a buffer another process exported through
-CUDA IPC.  One GPU is available, so the two-process test maps rank 0's image
-into rank 1 on the same device (the same IPC and kernel path as across
+CUDA IPC (mfa_ipc_open on the mapping rank's own device).  One GPU is
+available, so the two-process test maps rank 0's image into rank 1 on the
+same device (the same IPC and kernel path as across
 NVLink; no kernel waits on another rank's kernel) with gloo for the handle
 exchange and barriers; the result must equal the 1-GPU full-frame render bit
 for bit."""
@@ -57,6 +58,9 @@ def _worker(rank, world, port, out_path):
     if rank == 0:
         full = _full(w, m)
         np.save(out_path, np.stack([img.cpu().numpy(), full.cpu().numpy()]))
+    dist.barrier()
+    if rank != 0:
+        peer.close()   # mfa_ipc_close
     dist.barrier()
     dist.destroy_process_group()
 
