@@ -36,6 +36,7 @@ struct AxisArgs {
     float S;
     int dshift;      // non-uniform render: (F - U_s) >> dshift fits 23 bits on every span
     float dscale;    // 2^(dshift - 62)
+    int multi;       // non-uniform render: 1 if one ray step can cross more than one span (set per launch)
 };
 
 __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
@@ -47,6 +48,7 @@ __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
     a.kfx = A.kfx;
     a.bucket = A.bucket;
     a.srec = A.srec;
+    a.multi = 1;
     a.nsp = A.nsp;
     a.M = A.M;
     int lg = 0;
@@ -372,7 +374,9 @@ __device__ __forceinline__ void nu_cross(const AxisArgs& A, long long F, NUAxis&
 }
 
 __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxis& st) {
-    if (F >= st.hi || (F < st.lo && st.s > 0)) {   // rare: crossed more than one span this step
+    // rare: crossed more than one span this step; impossible (and skipped by a
+    // warp-uniform branch) when every span is wider than the largest step
+    if (A.multi && (F >= st.hi || (F < st.lo && st.s > 0))) {
         int s = st.s;
         while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
         while (s > 0 && F < __ldg(A.kfx + s)) --s;
@@ -794,6 +798,13 @@ __device__ __forceinline__ const float4* bez_block(const float4* Q, const BezGri
     const int64_t b = ((int64_t)sw * g.S1 + sv) * g.S0 + su;
     MFA_DCHECK((b + 1) * (BezBlock<P>::FLOATS / 4) <= g.q_f4);
     return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Q) + b * BezBlock<P>::FLOATS);
+}
+
+// block b = (sw * S1 + sv) * S0 + su (< 2^31: mfa_model_create)
+template <int P>
+__device__ __forceinline__ const float4* bez_block_at(const float4* Q, const BezGrid& g, int b) {
+    MFA_DCHECK(b >= 0 && (int64_t)(b + 1) * (BezBlock<P>::FLOATS / 4) <= g.q_f4);
+    return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Q) + (int64_t)b * BezBlock<P>::FLOATS);
 }
 
 // slab c of a Bezier block: rows b = 0..P at consecutive compile-time offsets

@@ -78,6 +78,7 @@ struct AxisTables {
     int ic_lo = 0, ic_hi = -1;        // uniform: spans [ic_lo, ic_hi] use the interior constants
     int uniform = 0;
     int dshift = 0;                   // see kernels.cuh nu_span
+    long long hmin_fx = 0;            // smallest span width in 2^62 fixed point (0 with repeated knots)
     float S = 0.f;                    // uniform: number of spans as float
 };
 

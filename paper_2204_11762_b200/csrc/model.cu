@@ -451,6 +451,10 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
             int sh = 0;
             while (sh < 62 && ldexp(hmax, kNonUniFracBits - sh) >= 8388607.0) ++sh;
             A.dshift = sh;
+            long long hm = 0x7fffffffffffffffLL;   // the kfx of knot_tables_kernel, on the host
+            for (int64_t i = p; i < nctrl[d]; ++i)
+                hm = std::min(hm, llrint(ldexp(knots[d][i + 1], kNonUniFracBits)) - llrint(ldexp(knots[d][i], kNonUniFracBits)));
+            A.hmin_fx = hm;
         }
         A.uniform = uniform[d];
         A.S = (float)nsp;
@@ -479,6 +483,11 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
     const bool nonuni = !(uniform[0] && uniform[1] && uniform[2]);
     bool bez = want_layout == MFA_LAYOUT_BEZIER || (want_layout == MFA_LAYOUT_AUTO && nonuni && p <= 3);
     if (bez && p > 3) return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs degree <= 3"));
+    if (bez && (nctrl[0] - p) * (nctrl[1] - p) * (nctrl[2] - p) >= ((int64_t)1 << 31)) {   // 32-bit block index
+        if (want_layout == MFA_LAYOUT_BEZIER)
+            return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs < 2^31 span triples"));
+        bez = false;
+    }
     if (bez) {
         const int64_t S0 = nctrl[0] - p, S1 = nctrl[1] - p, S2 = nctrl[2] - p;
         const int64_t nblk = S0 * S1 * S2;

@@ -80,6 +80,12 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         a->gsc[d] = (float)((uni ? (double)m->ax[d].nsp : 1.0) / a->L[d]);
     }
     a->step = prm->step;
+    for (int d = 0; d < 3; ++d) {
+        // |DF_d| <= step / L_d * 2^62 (unit ray directions) plus rounding; a
+        // crossing lands in the next span whenever that is below every span width
+        const double maxdf = ldexp(prm->step / a->L[d], kNonUniFracBits) * (1.0 + 1e-9) + 64.0;
+        a->ax[d].multi = !(maxdf < (double)m->ax[d].hmin_fx * (1.0 - 1e-9));
+    }
     a->o_max = (float)prm->o_max;
     a->ka = (float)prm->ka;
     a->kd = (float)prm->kd;

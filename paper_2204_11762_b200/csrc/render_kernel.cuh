@@ -16,6 +16,7 @@
 //          termination per ray with a warp-vote exit.
 //   out  = premultiplied RGBA (fp32 or fp16) to the image or to a packed tile.
 #pragma once
+#include <type_traits>
 #include <cuda_fp16.h>
 #include <math.h>
 
@@ -364,14 +365,14 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         int k = 0;
         bool live = K > 0;
         float nb[CACHE ? P + 1 : 1][P + 1][P + 1];   // cached neighbourhood (CACHE)
-        int64_t nb_key = -1;
+        std::conditional_t<BEZ, int, int64_t> nb_key = -1;   // Bezier: 32-bit block index
 
         // a6: make the neighbourhood of span triple s resident (CACHE layouts)
         auto fetch = [&](const int (&s)[3]) {
             if constexpr (BEZ && CACHE) {
-                const int64_t e = ((int64_t)s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
+                const int e = (s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
                 if (e != nb_key) {       // reload only when the span triple changed
-                    load_bblock<P>(bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]), nb);
+                    load_bblock<P>(bez_block_at<P>(args.Q, args.bg, e), nb);
                     nb_key = e;
                 }
             } else if constexpr (CACHE) {
