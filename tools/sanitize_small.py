@@ -23,3 +23,29 @@ for c, kw in ((1, {}), (2, dict(width=96, height=64)), (5, dict(width=64, height
         unpack_tiles(packed, tiles, len(w.cameras), w.cameras[0].width, w.cameras[0].height)
         torch.cuda.synchronize()
         print(c, layout, "ok", float(img.sum()))
+
+# the other entry points: binned eval (>= 2^16 points) and Hessian, the
+# extended render (lights, curvature table, analytic field), image metrics,
+# least-squares fit and the adaptive encoder
+from paper_2204_11762_b200 import encode_grid, fit_grid, image_quality  # noqa: E402
+
+w = WL.make_config(2, width=96, height=64)
+for layout in ("quads", "bezier"):
+    m = Model.from_workload(w, layout=layout)
+    u, v, ww = (torch.from_numpy(x).cuda() for x in WL.query_points(2, 1 << 16))
+    m.eval(u, v, ww, binned=True)
+    m.eval_hessian(u, v, ww, binned=True)
+    m.eval_hessian(u[:999], v[:999], ww[:999], binned=False)
+    tf = torch.from_numpy(w.tf).cuda()
+    a = m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, lights=[((1.0, 0.5, 0.2), 0.7), ((0.0, -1.0, 0.3), 0.4)])
+    tab = torch.rand((9, 9, 4), device="cuda")
+    b = m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, curvature=(tab, 30.0))
+    c = m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, field=WL.AnalyticField.gaussian_beam(1, 1))
+    q = image_quality(a[0], c[0], err_map=True)
+    torch.cuda.synchronize()
+    print("next", layout, "ok", q["psnr"], float(b.sum()))
+g = torch.from_numpy(WL.analytic_grid("gb", (40, 36, 32)).astype(np.float32)).cuda()
+fit_grid(g, 3, [WL.clamped_uniform_knots(n, 3) for n in (12, 11, 10)])
+encode_grid(g, 2, (4, 4, 4), 1e-3, 3, (20, 20, 20))
+torch.cuda.synchronize()
+print("fit/encode ok")
