@@ -303,7 +303,7 @@ def test_nonuniform_multiple_knots(p):
 
 
 @pytest.mark.parametrize("p,n,uniform", [(1, 9, True), (5, 12, True), (5, 12, False), (4, 9, False), (2, 3, True),
-                                         (3, 4, False)])
+                                         (3, 4, False), (1, 7, False), (2, 8, False)])
 def test_render_degrees_and_single_span(p, n, uniform):
     """Degrees outside the configs (1, 5), non-uniform p = 4 / 5 (quads +
     span tables), and the single-span model n = p + 1 (every axis one span):
@@ -380,3 +380,30 @@ def test_more_than_64_views_and_tf_sizes():
         torch.cuda.synchronize()
         ref = O.render(oracle_model(c), w.cameras[0], tf, w.v_lo, w.v_hi, w.params)
         parity.check_image(out[0].cpu().numpy().reshape(-1, 4), ref, f"TF with {n} entries")
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_spans_narrower_than_a_step(p):
+    """Non-uniform axes with spans narrower than one ray step, so one step can
+    cross several spans (the multi-span path the per-launch flag otherwise
+    skips, render.cu): render parity, and the same image with every span wide
+    (flag off) still matches its own oracle."""
+    from paper_2204_11762_b200 import Model
+    r = np.random.default_rng(7 + p)
+    w = WL.make_config(2, width=64, height=48)
+    step = w.params.step
+    for narrow in (True, False):
+        knots = []
+        for d in range(3):
+            inner = [0.2, 0.45, 0.7] if not narrow else [0.2, 0.45, 0.45 + 0.3 * step, 0.45 + 0.6 * step, 0.7]
+            knots.append(np.concatenate([np.zeros(p + 1), inner, np.ones(p + 1)]))
+        n = len(knots[0]) - p - 1
+        ctrl = r.uniform(0, 1, (n, n, n)).astype(np.float32)
+        w.degree, w.knots, w.ctrl, w.nctrl, w.uniform = p, knots, ctrl, (n, n, n), False
+        w.v_lo, w.v_hi = float(ctrl.min()), float(ctrl.max())
+        m = Model.from_workload(w)
+        om = O.Model.from_workload(w)
+        img = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params)
+        torch.cuda.synchronize()
+        ref = O.render(om, w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
+        parity.check_image(img[0].cpu().numpy().reshape(-1, 4), ref, f"p={p} narrow={narrow}")
