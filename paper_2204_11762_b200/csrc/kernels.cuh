@@ -373,10 +373,12 @@ __device__ __forceinline__ void nu_cross(const AxisArgs& A, long long F, NUAxis&
     }
 }
 
+template <bool MULTI = true>
 __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxis& st) {
-    // rare: crossed more than one span this step; impossible (and skipped by a
-    // warp-uniform branch) when every span is wider than the largest step
-    if (A.multi && (F >= st.hi || (F < st.lo && st.s > 0))) {
+    // rare: crossed more than one span this step; impossible when every span is
+    // wider than the largest step (A.multi = 0; the render compiles a loop
+    // without the check, MULTI = false, for launches where no axis needs it)
+    if (MULTI && A.multi && (F >= st.hi || (F < st.lo && st.s > 0))) {
         int s = st.s;
         while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
         while (s > 0 && F < __ldg(A.kfx + s)) --s;

@@ -395,14 +395,15 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             }
         };
         // a4: span + local coordinate per axis of the sample at F
-        auto locate = [&](int (&s)[3], float (&t)[3], float (&gs)[3]) {
+        auto locate = [&](int (&s)[3], float (&t)[3], float (&gs)[3], auto multi_tag) {
+            constexpr bool MULTI = decltype(multi_tag)::value;
 #if MFA_NU_SPLIT
             if constexpr (!UNI) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i) nu_cross(args.ax[i], F[i], nu[i]);
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    t[i] = nu_finish(args.ax[i], F[i], nu[i]);
+                    t[i] = nu_finish<MULTI>(args.ax[i], F[i], nu[i]);
                     s[i] = nu[i].s;
                     gs[i] = nu[i].invh * args.gsc[i];
                 }
@@ -649,7 +650,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         if (live) {
             int s[3];
             float t[3];
-            locate(s, t, gs);
+            locate(s, t, gs, std::true_type{});
             if constexpr (EXT) {
                 if (args.curv.n > 0) curv_query(s, t, gs, ck1, ck2);
                 sample_field(s, t, val, gu, gv, gw, gs);
@@ -661,14 +662,14 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             for (int i = 0; i < 3; ++i) F[i] += (!kFlat || K > 1) ? DF[i] : 0;
         }
 #if MFA_FLAT_LOOP
-        if constexpr (kFlat) {
-            // branch-free body: every lane runs it; a finished lane's sample
-            // position is frozen (no reloads) and its compositing weight is 0.
-            // Iteration k composites sample k and queries sample min(k+1, K-1).
+        // branch-free body: every lane runs it; a finished lane's sample
+        // position is frozen (no reloads) and its compositing weight is 0.
+        // Iteration k composites sample k and queries sample min(k+1, K-1).
+        auto flat_loop = [&](auto multi_tag) {
             while (__any_sync(0xffffffffu, live)) {
                 int s[3];
                 float t[3], gs1[3];
-                locate(s, t, gs1);
+                locate(s, t, gs1, multi_tag);
                 fetch(s);
                 comp_on = live;
                 shade_composite(val, gu, gv, gw, gs, 0.f, 0.f);
@@ -685,6 +686,12 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 k += live ? 1 : 0;
                 live = live && !(A > args.o_max) && k < K;
             }
+        };
+        if constexpr (kFlat) {
+            if (!UNI && (args.ax[0].multi | args.ax[1].multi | args.ax[2].multi))   // launch-uniform
+                flat_loop(std::true_type{});
+            else
+                flat_loop(std::false_type{});
         }
 #endif
         while (!kFlat && __any_sync(0xffffffffu, live)) {
@@ -700,7 +707,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 if (k + 1 < K) {
                     int s[3];
                     float t[3], gs1[3];
-                    locate(s, t, gs1);
+                    locate(s, t, gs1, std::true_type{});
                     float val1 = 0.f, gu1 = 0.f, gv1 = 0.f, gw1 = 0.f;
                     if constexpr (EXT) {
                         float nk1 = 0.f, nk2 = 0.f;
