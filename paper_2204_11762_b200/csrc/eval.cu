@@ -192,9 +192,12 @@ __device__ __forceinline__ int point_bin(const BinGrid& g, float u, float v, flo
     return (bw * g.nb[1] + bv) * g.nb[0] + bu;
 }
 
-constexpr int kBinSmem = 12288;   // bins counted in shared memory (48 KB)
+#ifndef MFA_BIN_SMEM       // bins counted in shared memory (dynamic, opt-in above 48 KB)
+#define MFA_BIN_SMEM 53248 // 208 KB: C3's 32^3 bins fit
+#endif
+constexpr int kBinSmem = MFA_BIN_SMEM;
 
-__global__ void __launch_bounds__(256) bin_count_kernel(const float* __restrict__ u, const float* __restrict__ v,
+__global__ void __launch_bounds__(1024) bin_count_kernel(const float* __restrict__ u, const float* __restrict__ v,
                                                         const float* __restrict__ w, int64_t n, const BinGrid g,
                                                         int* __restrict__ bins, unsigned* __restrict__ counts) {
     extern __shared__ unsigned sh[];
@@ -305,7 +308,12 @@ BinnedPoints bin_points(const Model* m, int64_t n, const float* u, const float* 
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
     cudaMemsetAsync(counts, 0, sizeof(unsigned) * (g.nbins + 1), st);
     const size_t smem = g.nbins + 1 <= kBinSmem ? sizeof(unsigned) * (g.nbins + 1) : 0;
-    bin_count_kernel<<<grid, 256, smem, st>>>(u, v, w, n, g, bins, counts);
+    unsigned cgrid = grid;
+    if (smem > 48 * 1024) {   // one CTA per SM with a large table: fewer, longer CTAs amortise the flush
+        cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(unsigned) * kBinSmem));
+        cgrid = (unsigned)std::min<int64_t>((n + 1023) / 1024, (int64_t)sms);
+    }
+    bin_count_kernel<<<cgrid, smem > 48 * 1024 ? 1024 : 256, smem, st>>>(u, v, w, n, g, bins, counts);
     bin_scan_kernel<<<1, 1024, 0, st>>>(counts, g.nbins + 1, cursor);
     bin_scatter_kernel<<<grid, 256, 0, st>>>(u, v, w, n, bins, cursor, rec);
     return BinnedPoints{rec, bins};
