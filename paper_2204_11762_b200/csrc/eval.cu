@@ -196,6 +196,9 @@ __device__ __forceinline__ int point_bin(const BinGrid& g, float u, float v, flo
 #define MFA_BIN_SMEM 53248 // 208 KB: C3's 32^3 bins fit
 #endif
 constexpr int kBinSmem = MFA_BIN_SMEM;
+#ifndef MFA_BIN_FIT   // 1: coarsen the bins of large models until the histogram fits in shared memory
+#define MFA_BIN_FIT 1
+#endif
 
 __global__ void __launch_bounds__(1024) bin_count_kernel(const float* __restrict__ u, const float* __restrict__ v,
                                                         const float* __restrict__ w, int64_t n, const BinGrid g,
@@ -305,6 +308,17 @@ static BinGrid make_bins(const Model* m) {
         for (int d = 0; d < 3; ++d) g.nb[d] = std::max(1, g.nb[d] / 2);
         total = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
     }
+#if MFA_BIN_FIT
+    // coarsen the axis with the most bins until the histogram fits in shared memory
+    while (total + 1 > kBinSmem) {
+        int d = 0;
+        for (int e = 1; e < 3; ++e)
+            if (g.nb[e] > g.nb[d]) d = e;
+        if (g.nb[d] == 1) break;
+        g.nb[d] = (g.nb[d] + 1) / 2;
+        total = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
+    }
+#endif
     g.nbins = (int)total;
     return g;
 }
