@@ -461,11 +461,18 @@ class PeerBuffer:
     (mfa_ipc_open): data_ptr() for the entry points, shape / dtype for the
     caller; close() unmaps it."""
 
+    _open = {}   # handle -> [base, users]: an allocation is mapped once per process
+
     def __init__(self, handle: bytes, offset: int, shape, dtype):
-        base = C.c_void_p(0)
-        _check(lib().mfa_ipc_open(bytes(handle), C.byref(base)))
-        self._base = base.value
-        self._ptr = base.value + int(offset)
+        self._handle = bytes(handle)
+        ent = PeerBuffer._open.get(self._handle)
+        if ent is None:
+            base = C.c_void_p(0)
+            _check(lib().mfa_ipc_open(self._handle, C.byref(base)))
+            ent = PeerBuffer._open[self._handle] = [base.value, 0]
+        ent[1] += 1
+        self._base = ent[0]
+        self._ptr = ent[0] + int(offset)
         self.shape = tuple(shape)
         self.dtype = dtype
 
@@ -474,7 +481,11 @@ class PeerBuffer:
 
     def close(self):
         if self._base:
-            _check(lib().mfa_ipc_close(C.c_void_p(self._base)))
+            ent = PeerBuffer._open[self._handle]
+            ent[1] -= 1
+            if ent[1] == 0:
+                del PeerBuffer._open[self._handle]
+                _check(lib().mfa_ipc_close(C.c_void_p(self._base)))
             self._base = self._ptr = 0
 
 

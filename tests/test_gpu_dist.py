@@ -54,6 +54,10 @@ def _worker(rank, world, port, out_path):
     def render_scatter(tiles, out):
         m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=tiles, out=out, scatter=True)
 
+    again = D.peer_image(img0, rank)   # the same allocation exported twice: one mapping per process
+    if rank != 0:
+        assert again.data_ptr() == peer.data_ptr()
+        again.close()
     img, n = D.render_direct(render_scatter, 2, 160, 96, rank, world, peer, device="cuda")
     if rank == 0:
         full = _full(w, m)
