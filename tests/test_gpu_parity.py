@@ -385,17 +385,19 @@ def test_more_than_64_views_and_tf_sizes():
 @pytest.mark.parametrize("p", [2, 3])
 def test_spans_narrower_than_a_step(p):
     """Non-uniform axes with spans narrower than one ray step, so one step can
-    cross several spans (the multi-span path the per-launch flag otherwise
-    skips, render.cu): render parity, and the same image with every span wide
-    (flag off) still matches its own oracle."""
+    cross several spans (adjacent narrow spans: up to three crossings; an
+    isolated narrow span: two), and every span wide (the per-launch flag
+    drops the multi-span check, render.cu): render parity for each."""
     from paper_2204_11762_b200 import Model
     r = np.random.default_rng(7 + p)
     w = WL.make_config(2, width=64, height=48)
     step = w.params.step
-    for narrow in (True, False):
+    inners = {"adjacent": [0.2, 0.45, 0.45 + 0.3 * step, 0.45 + 0.6 * step, 0.7],
+              "isolated": [0.2, 0.45, 0.45 + 0.5 * step, 0.7],
+              "wide": [0.2, 0.45, 0.7]}
+    for narrow, inner in inners.items():
         knots = []
         for d in range(3):
-            inner = [0.2, 0.45, 0.7] if not narrow else [0.2, 0.45, 0.45 + 0.3 * step, 0.45 + 0.6 * step, 0.7]
             knots.append(np.concatenate([np.zeros(p + 1), inner, np.ones(p + 1)]))
         n = len(knots[0]) - p - 1
         ctrl = r.uniform(0, 1, (n, n, n)).astype(np.float32)
