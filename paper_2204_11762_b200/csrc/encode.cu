@@ -116,23 +116,31 @@ static mfa_status build_axis(int d, int m, int n, int p, const double* U, AxisFi
         Lat(i, i) = sqrt(s);
     }
     // dense pseudo-inverse N^+ = A^{-1} N^T (n x m, row-major): column j of N^T
-    // has p+1 entries at rows f_j .. f_j + p; forward then backward banded solve
+    // has p+1 entries at rows f_j .. f_j + p; forward then backward banded
+    // solve, all m columns at once row by row (contiguous rows of length m)
     A.M.assign((size_t)n * m, 0.0);
-    std::vector<double> y(n);
-    for (int j = 0; j < m; ++j) {
-        std::fill(y.begin(), y.end(), 0.0);
-        const int i0 = A.f[j];
-        for (int i = i0; i < n; ++i) {
-            double r = (i - i0 <= p) ? A.B[(size_t)j * (p + 1) + (i - i0)] : 0.0;
-            for (int l = std::max(i0, i - p); l < i; ++l) r -= Lat(i, l) * y[l];
-            y[i] = r / Lat(i, i);
+    double* Y = A.M.data();
+    for (int j = 0; j < m; ++j)
+        for (int a = 0; a <= p; ++a) Y[(size_t)(A.f[j] + a) * m + j] = A.B[(size_t)j * (p + 1) + a];
+    for (int i = 0; i < n; ++i) {
+        double* yi = Y + (size_t)i * m;
+        for (int l = std::max(0, i - p); l < i; ++l) {
+            const double c = Lat(i, l);
+            const double* yl = Y + (size_t)l * m;
+            for (int j = 0; j < m; ++j) yi[j] -= c * yl[j];
         }
-        for (int i = n - 1; i >= 0; --i) {
-            double r = y[i];
-            for (int l = i + 1; l <= std::min(n - 1, i + p); ++l) r -= Lat(l, i) * y[l];
-            y[i] = r / Lat(i, i);
+        const double dg = Lat(i, i);
+        for (int j = 0; j < m; ++j) yi[j] /= dg;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double* yi = Y + (size_t)i * m;
+        for (int l = i + 1; l <= std::min(n - 1, i + p); ++l) {
+            const double c = Lat(l, i);
+            const double* yl = Y + (size_t)l * m;
+            for (int j = 0; j < m; ++j) yi[j] -= c * yl[j];
         }
-        for (int i = 0; i < n; ++i) A.M[(size_t)i * m + j] = y[i];
+        const double dg = Lat(i, i);
+        for (int j = 0; j < m; ++j) yi[j] /= dg;
     }
     return MFA_OK;
 }
