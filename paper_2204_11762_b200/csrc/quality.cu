@@ -20,6 +20,9 @@
 
 namespace mfa {
 
+#ifndef MFA_SSIM_SEP   // 1: separable SSIM window passes
+#define MFA_SSIM_SEP 1
+#endif
 constexpr int kWin = 11;
 constexpr int kQThreads = 256;
 constexpr int kSTileX = 32, kSTileY = 8;   // SSIM outputs per CTA
@@ -115,6 +118,84 @@ __global__ void __launch_bounds__(kSTileX* kSTileY) ssim_kernel(const double* __
     if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = t;
 }
 
+// K_s, separable form (MFA_SSIM_SEP): the 11x11 Gaussian window is the outer
+// product of the normalised 1-D window g (w_ij = g_i g_j exactly, up to fp64
+// rounding), so the 5 moments are an 11-tap row pass into shared memory and
+// an 11-tap column pass: 55 + 55 * 18/8 weighted terms per output instead of 605
+struct GaussWin1 {
+    double g[kWin];
+};
+
+static GaussWin1 make_window1() {
+    GaussWin1 g;
+    double sum = 0.0;
+    for (int i = 0; i < kWin; ++i) {
+        const double di = i - kWin / 2;
+        g.g[i] = exp(-(di * di) / (2.0 * 1.5 * 1.5));
+        sum += g.g[i];
+    }
+    for (int i = 0; i < kWin; ++i) g.g[i] /= sum;
+    return g;
+}
+
+__global__ void __launch_bounds__(kSTileX* kSTileY) ssim_sep_kernel(const double* __restrict__ ya,
+                                                                    const double* __restrict__ yb, int W, int H,
+                                                                    const GaussWin1 gw, double* __restrict__ part) {
+    constexpr int TW = kSTileX + kWin - 1, TH = kSTileY + kWin - 1;
+    __shared__ double sa[TH][TW], sb[TH][TW];
+    __shared__ double hm[5][TH][kSTileX];
+    __shared__ double sh[kSTileX * kSTileY / 32];
+    const int ow = W - kWin + 1, oh = H - kWin + 1;
+    const int x0 = blockIdx.x * kSTileX, y0 = blockIdx.y * kSTileY;
+    for (int k = threadIdx.x; k < TW * TH; k += blockDim.x) {
+        const int ty = k / TW, tx = k % TW;
+        const int gx = min(x0 + tx, W - 1), gy = min(y0 + ty, H - 1);
+        sa[ty][tx] = ya[(int64_t)gy * W + gx];
+        sb[ty][tx] = yb[(int64_t)gy * W + gx];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < TH * kSTileX; k += blockDim.x) {   // row pass
+        const int r = k / kSTileX, c = k % kSTileX;
+        double ma = 0.0, mb = 0.0, saa = 0.0, sbb = 0.0, sab = 0.0;
+#pragma unroll
+        for (int dj = 0; dj < kWin; ++dj) {
+            const double w = gw.g[dj];
+            const double A = sa[r][c + dj], B = sb[r][c + dj];
+            ma += w * A;
+            mb += w * B;
+            saa += w * A * A;
+            sbb += w * B * B;
+            sab += w * A * B;
+        }
+        hm[0][r][c] = ma;
+        hm[1][r][c] = mb;
+        hm[2][r][c] = saa;
+        hm[3][r][c] = sbb;
+        hm[4][r][c] = sab;
+    }
+    __syncthreads();
+    const int lx = threadIdx.x % kSTileX, ly = threadIdx.x / kSTileX;
+    const int ox = x0 + lx, oy = y0 + ly;
+    double v = 0.0;
+    if (ox < ow && oy < oh) {   // column pass
+        double ma = 0.0, mb = 0.0, saa = 0.0, sbb = 0.0, sab = 0.0;
+#pragma unroll
+        for (int di = 0; di < kWin; ++di) {
+            const double w = gw.g[di];
+            ma += w * hm[0][ly + di][lx];
+            mb += w * hm[1][ly + di][lx];
+            saa += w * hm[2][ly + di][lx];
+            sbb += w * hm[3][ly + di][lx];
+            sab += w * hm[4][ly + di][lx];
+        }
+        const double va = saa - ma * ma, vb = sbb - mb * mb, cab = sab - ma * mb;
+        const double C1 = (0.01 * 255.0) * (0.01 * 255.0), C2 = (0.03 * 255.0) * (0.03 * 255.0);
+        v = ((2.0 * ma * mb + C1) * (2.0 * cab + C2)) / ((ma * ma + mb * mb + C1) * (va + vb + C2));
+    }
+    const double t = block_sum<kSTileX * kSTileY>(v, sh);
+    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = t;
+}
+
 // one CTA of 1024 threads: strided partial sums, then a fixed-order tree
 __global__ void __launch_bounds__(1024) quality_final_kernel(const double* __restrict__ pq, int nq,
                                                              const double* __restrict__ ps, int ns, int64_t npix,
@@ -186,8 +267,13 @@ extern "C" mfa_status mfa_image_quality(int32_t width, int32_t height, const flo
     const int64_t n = (int64_t)width * height;
     quality_pixels_kernel<<<p.nq, kQThreads, 0, st>>>(reinterpret_cast<const float4*>(img_a),
                                                       reinterpret_cast<const float4*>(img_b), n, ya, yb, err_map, pq);
+#if MFA_SSIM_SEP
+    static const GaussWin1 gw1 = make_window1();
+    ssim_sep_kernel<<<dim3(p.sx, p.sy), kSTileX * kSTileY, 0, st>>>(ya, yb, width, height, gw1, ps);
+#else
     static const GaussWin gw = make_window();
     ssim_kernel<<<dim3(p.sx, p.sy), kSTileX * kSTileY, 0, st>>>(ya, yb, width, height, gw, ps);
+#endif
     const int64_t nwin = (int64_t)(width - kWin + 1) * (height - kWin + 1);
     quality_final_kernel<<<1, 1024, 0, st>>>(pq, p.nq, ps, p.sx * p.sy, n, nwin, out3);
     cudaError_t e = cudaGetLastError();
