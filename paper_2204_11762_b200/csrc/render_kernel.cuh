@@ -29,6 +29,9 @@
 // first use (hides part of the reload latency; C5 +1.8 %)
 // MFA_FLAT_LOOP = 1: branch-free sample loop for the register-cached layouts
 // (finished lanes re-query a frozen sample, which never reloads); C5 +2 %, C3 +7 %
+#ifndef MFA_UNIT_SHAPE   // lanes of a warp unit: 0 = 8x4 pixels, 1 = 4x8 (C5 +0.8 %), 2 = 16x2
+#define MFA_UNIT_SHAPE 1
+#endif
 #ifndef MFA_FLAT_LOOP
 #define MFA_FLAT_LOOP 1
 #endif
@@ -290,8 +293,16 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         ViewFrame fr;
         compute_frame(args.cams[view], fr);
 #endif
+#if MFA_UNIT_SHAPE == 1   // 4 x 8 pixels per warp unit
+        const int lx = (sub & 3) * 4 + (lane & 3);
+        const int ly = (sub >> 2) * 8 + (lane >> 2);
+#elif MFA_UNIT_SHAPE == 2   // 16 x 2
+        const int lx = lane & 15;
+        const int ly = sub * 2 + (lane >> 4);
+#else                       // 8 x 4
         const int lx = (sub & 1) * 8 + (lane & 7);
         const int ly = (sub >> 1) * 4 + (lane >> 3);
+#endif
         const int px = tx * MFA_TILE + lx, py = ty * MFA_TILE + ly;
         const bool valid = px < args.W && py < args.H;
 
