@@ -2,7 +2,7 @@
 // truth.cu, which instantiate it without / with the extensions: the analytic
 // ground-truth field of NEXT-2 and several directional lights, NEXT-4).
 //
-//   work = warp units of 8x4 pixels (8 per 16x16 tile) handed out by a global
+//   work = warp units of 4x8 pixels (8 per 16x16 tile) handed out by a global
 //          atomic counter to persistent warps (grid = SMs x resident CTAs), so
 //          early-terminating rays never leave an SM idle and no warp waits on
 //          its CTA's slowest warp; consecutive units are neighbouring tiles.
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             round_sub = (round_sub + 1) % (8 / kWarps);
             if (tile_base >= args.n_units) break;
         } else {
-            // ---- next warp unit (8x4 pixels) from the global queue ---------
+            // ---- next warp unit (32 pixels, MFA_UNIT_SHAPE) from the global queue ---------
             if (lane == 0) unit = atomicAdd(args.queue, 1u);
             unit = __shfl_sync(0xffffffffu, unit, 0);
             if (unit >= args.n_units) break;
