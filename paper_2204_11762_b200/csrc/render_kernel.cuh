@@ -29,7 +29,7 @@
 // first use (hides part of the reload latency; C5 +1.8 %)
 // MFA_FLAT_LOOP = 1: branch-free sample loop for the register-cached layouts
 // (finished lanes re-query a frozen sample, which never reloads); C5 +2 %, C3 +7 %
-#ifndef MFA_UNIT_SHAPE   // lanes of a warp unit: 0 = 8x4 pixels, 1 = 4x8 (C5 +0.8 %), 2 = 16x2
+#ifndef MFA_UNIT_SHAPE   // lanes of a warp unit: 0 = 8x4 pixels, 1 = 4x8 (C5 +0.8 %, C4 +3 %), 2 = 16x2, 3 = 2x16
 #define MFA_UNIT_SHAPE 1
 #endif
 #ifndef MFA_FLAT_LOOP
@@ -299,6 +299,9 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
 #elif MFA_UNIT_SHAPE == 2   // 16 x 2
         const int lx = lane & 15;
         const int ly = sub * 2 + (lane >> 4);
+#elif MFA_UNIT_SHAPE == 3   // 2 x 16
+        const int lx = sub * 2 + (lane & 1);
+        const int ly = lane >> 1;
 #else                       // 8 x 4
         const int lx = (sub & 1) * 8 + (lane & 7);
         const int ly = (sub >> 1) * 4 + (lane >> 3);
