@@ -168,6 +168,14 @@ __device__ __forceinline__ void field_eval(const FieldArgs& f, const double (&u)
 // x^n for the Phong specular term: 2^(n log2 x) with the ftz approximations
 // (no denormal fix-up sequences; x = 0 -> 0 for n > 0; a specular term below
 // 2^-126 is flushed to 0, far under the image tolerance)
+// 1/sqrt(x) for x >= 1e-37 (a normal float): the ftz form has no denormal
+// fix-up (3 instructions per sample) and gives the same result on this domain
+__device__ __forceinline__ float rsqrt_normal(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ float pow_spec(float x, float n) {
 #if MFA_FAST_POW
     float l, r;
@@ -552,7 +560,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                     const float gx = gu * gs[0], gy = gv * gs[1], gz = gw * gs[2];
                     const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
                     const bool zero = n2 <= args.eps2;
-                    const float inv = rsqrtf(fmaxf(n2, 1e-37f));
+                    const float inv = rsqrt_normal(fmaxf(n2, 1e-37f));
                     const float ndv = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * inv;   // N . V, V = -d
                     float dif = 0.f, spe = 0.f;
                     for (int l = 0; l < args.lights.n; ++l) {
@@ -576,7 +584,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 const float gx = gu * gs[0], gy = gv * gs[1], gz = gw * gs[2];
                 const float n2 = fmaf(gx, gx, fmaf(gy, gy, gz * gz));
                 const bool zero = n2 <= args.eps2;
-                const float ndl = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * rsqrtf(fmaxf(n2, 1e-37f));
+                const float ndl = fmaf(gx, dx, fmaf(gy, dy, gz * dz)) * rsqrt_normal(fmaxf(n2, 1e-37f));
                 const float dif = fmaxf(ndl, 0.f);
                 const float rv = fmaxf(fmaf(2.f * ndl, ndl, -1.f), 0.f);
                 float spe = pow_spec(rv, args.shin);                  // rv = 0 -> 0 (shin > 0)
