@@ -117,7 +117,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
             delete a;
             return fail(MFA_ERR_UNSUPPORTED, "tiled render supports at most 64 views per call");
         }
-        for (int v = 0; v < n_views; ++v) a->cams[v] = cams[v];
+        for (int v = 0; v < n_views; ++v) compute_frame(cams[v], a->frames[v]);
         a->n_views = n_views;
         a->tiles = tiles->tiles;
         a->tile_scatter = tiles->scatter != 0;
@@ -131,7 +131,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         a->n_tiles = 0;
         for (int v0 = 0; v0 < n_views && e == cudaSuccess; v0 += kMaxViewsPerLaunch) {
             const int nv = std::min(kMaxViewsPerLaunch, n_views - v0);
-            for (int v = 0; v < nv; ++v) a->cams[v] = cams[v0 + v];
+            for (int v = 0; v < nv; ++v) compute_frame(cams[v0 + v], a->frames[v]);
             a->n_views = nv;
             a->view_base = v0;
             a->n_units = (int64_t)nv * a->st_x * a->st_y * 64 * 8;

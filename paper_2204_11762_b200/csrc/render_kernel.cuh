@@ -60,6 +60,11 @@ struct LightArgs {
     float intensity[kMaxLights];
 };
 
+struct ViewFrame {
+    double eye[3], f[3], A[3], B[3];
+    int ortho;
+};
+
 struct RenderArgs {
     const float4* Q;
     BrickGrid g;
@@ -91,15 +96,10 @@ struct RenderArgs {
         int n;                    // 0: off
         float scale, range;       // index = (kappa + range) * scale, scale = (n - 1) / (2 range)
     } curv;
-    mfa_camera cams[kMaxViewsPerLaunch];
+    ViewFrame frames[kMaxViewsPerLaunch];   // per view, computed on the host (compute_frame)
 };
 
-struct ViewFrame {
-    double eye[3], f[3], A[3], B[3];
-    int ortho;
-};
-
-__device__ __forceinline__ void compute_frame(const mfa_camera& c, ViewFrame& fr) {
+__host__ __device__ inline void compute_frame(const mfa_camera& c, ViewFrame& fr) {
     double f[3] = {c.look_at[0] - c.eye[0], c.look_at[1] - c.eye[1], c.look_at[2] - c.eye[2]};
     double lf = sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
     for (int i = 0; i < 3; ++i) f[i] /= lf;
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
 #endif
 
 #if MFA_SMEM_FRAMES
-    for (int v = threadIdx.x; v < args.n_views; v += blockDim.x) compute_frame(args.cams[v], s_frame[v]);
+    for (int v = threadIdx.x; v < args.n_views; v += blockDim.x) s_frame[v] = args.frames[v];
 #endif
     for (int i = threadIdx.x; i < args.tf_n; i += blockDim.x) s_tf[i] = __ldg(args.tf + i);
     __syncthreads();
@@ -295,11 +295,9 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
 #if MFA_SMEM_FRAMES
         const ViewFrame& fr = s_frame[view];
 #else
-        // the view's frame from its camera (kernel parameters, uniform across the
-        // warp): ~60 fp64 ops per 32 rays, and no shared memory, so the L1 keeps
-        // more of the unified 256 KB
-        ViewFrame fr;
-        compute_frame(args.cams[view], fr);
+        // the view's frame (kernel parameters, computed on the host by
+        // compute_frame; uniform across the warp, no shared memory)
+        const ViewFrame& fr = args.frames[view];
 #endif
 #if MFA_UNIT_SHAPE == 1   // 4 x 8 pixels per warp unit
         const int lx = (sub & 3) * 4 + (lane & 3);
