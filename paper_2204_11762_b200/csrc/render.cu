@@ -80,6 +80,11 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         a->gsc[d] = (float)((uni ? (double)m->ax[d].nsp : 1.0) / a->L[d]);
     }
     a->step = prm->step;
+    a->inv_step = 1.0 / prm->step;
+    a->inv_w2 = 2.0 / (double)cams[0].width;
+    a->inv_h2 = 2.0 / (double)cams[0].height;
+    for (int d = 0; d < 3; ++d)   // world offset -> fixed-point sample coordinate
+        a->fxs[d] = uni ? ldexp((double)m->ax[d].nsp, kUniFracBits) / a->L[d] : ldexp(1.0, kNonUniFracBits) / a->L[d];
     for (int d = 0; d < 3; ++d) {
         // |DF_d| <= step / L_d * 2^62 (unit ray directions) plus rounding; a
         // crossing lands in the next span whenever that is below every span width

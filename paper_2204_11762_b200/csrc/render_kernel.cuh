@@ -75,6 +75,9 @@ struct RenderArgs {
     float v_lo, s_scale;          // f = (v - v_lo) * s_scale = s * (n - 1)
     double bmin[3], L[3];
     double step;
+    // host-derived setup scales (render.cu): world offset -> fixed point per
+    // axis ((S or 1) * 2^frac / L), 1 / step, 2 / W, 2 / H
+    double fxs[3], inv_step, inv_w2, inv_h2;
     float gsc[3];                 // gradient scale to physical units (uniform: S/L; non-uniform: 1/L)
     float o_max, ka, kd, ks, shin, eps2;
     int W, H, tiles_x, tiles_y;
@@ -318,8 +321,8 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         // ---- a1: ray through the pixel centre (fp64) -----------------------
         double o[3], d[3];
         {
-            const double X = 2.0 * (px + 0.5) / args.W - 1.0;
-            const double Y = 1.0 - 2.0 * (py + 0.5) / args.H;
+            const double X = (px + 0.5) * args.inv_w2 - 1.0;
+            const double Y = 1.0 - (py + 0.5) * args.inv_h2;
             if (fr.ortho) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
@@ -352,13 +355,14 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                     if (o[i] < args.bmin[i] || o[i] > bmax) hit = false;
                     continue;
                 }
-                const double t0 = (args.bmin[i] - o[i]) / d[i], t1 = (bmax - o[i]) / d[i];
+                const double id = 1.0 / d[i];
+                const double t0 = (args.bmin[i] - o[i]) * id, t1 = (bmax - o[i]) * id;
                 tn = fmax(tn, fmin(t0, t1));
                 tf = fmin(tf, fmax(t0, t1));
             }
             t_in = fmax(tn, 0.0);
             if (hit && tf > t_in) {
-                const double frc = (tf - t_in) / args.step - 0.5;
+                const double frc = (tf - t_in) * args.inv_step - 0.5;
                 K = frc > 0.0 ? (int)ceil(frc) : 0;
             }
         }
@@ -369,15 +373,10 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             const double t0 = t_in + 0.5 * args.step;
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
-                const double u0 = (o[i] + t0 * d[i] - args.bmin[i]) / args.L[i];
-                const double du = args.step * d[i] / args.L[i];
-                if (UNI) {
-                    const double S = (double)args.ax[i].nsp;
-                    F[i] = llrint(ldexp(u0 * S, kUniFracBits));
-                    DF[i] = llrint(ldexp(du * S, kUniFracBits));
-                } else {
-                    F[i] = llrint(ldexp(u0, kNonUniFracBits));
-                    DF[i] = llrint(ldexp(du, kNonUniFracBits));
+                // u = (x - b) / L in fixed point: one scale per axis from the host
+                F[i] = llrint((o[i] + t0 * d[i] - args.bmin[i]) * args.fxs[i]);
+                DF[i] = llrint(args.step * d[i] * args.fxs[i]);
+                if (!UNI) {
                     if constexpr (!UNI) {
 #if MFA_FLAT_LOOP   // every lane keeps a valid span state (lanes without samples query a fixed point)
                         if (K == 0) F[i] = DF[i] = 0;
