@@ -42,6 +42,10 @@
     } while (0)
 #endif
 
+#ifndef MFA_SUPERTILE   // full-frame work order: supertiles of MFA_SUPERTILE x MFA_SUPERTILE 16x16 tiles
+#define MFA_SUPERTILE 2
+#endif
+
 namespace mfa {
 
 constexpr int kMaxP = MFA_MAX_DEGREE;

@@ -101,8 +101,8 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->H = cams[0].height;
     a->tiles_x = (a->W + MFA_TILE - 1) / MFA_TILE;
     a->tiles_y = (a->H + MFA_TILE - 1) / MFA_TILE;
-    a->st_x = (a->tiles_x + 7) / 8;
-    a->st_y = (a->tiles_y + 7) / 8;
+    a->st_x = (a->tiles_x + MFA_SUPERTILE - 1) / MFA_SUPERTILE;
+    a->st_y = (a->tiles_y + MFA_SUPERTILE - 1) / MFA_SUPERTILE;
     a->out = out;
     a->out_fp16 = prm->out_fp16;
     a->samples = samples;
@@ -139,7 +139,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
             for (int v = 0; v < nv; ++v) compute_frame(cams[v0 + v], a->frames[v]);
             a->n_views = nv;
             a->view_base = v0;
-            a->n_units = (int64_t)nv * a->st_x * a->st_y * 64 * 8;
+            a->n_units = (int64_t)nv * a->st_x * a->st_y * (MFA_SUPERTILE * MFA_SUPERTILE) * 8;
             e = run();
         }
     }

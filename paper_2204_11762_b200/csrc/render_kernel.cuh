@@ -81,7 +81,7 @@ struct RenderArgs {
     float gsc[3];                 // gradient scale to physical units (uniform: S/L; non-uniform: 1/L)
     float o_max, ka, kd, ks, shin, eps2;
     int W, H, tiles_x, tiles_y;
-    int st_x, st_y;               // supertiles (8x8 tiles) per view, full-frame order
+    int st_x, st_y;               // supertiles (MFA_SUPERTILE^2 tiles) per view, full-frame order
     int n_views;
     const int* tiles;             // NULL: full frames
     int tile_scatter;             // tiles: 1 = write pixels at their image position, 0 = packed tiles
@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
-    const int per_view = args.st_x * args.st_y * 64;   // units are ordered by 8x8-tile supertiles
+    constexpr int kST = MFA_SUPERTILE, kST2 = MFA_SUPERTILE * MFA_SUPERTILE;
+    const int per_view = args.st_x * args.st_y * kST2;   // units are ordered by supertiles of tiles
     unsigned long long my_samples = 0;
 #if MFA_LANE_STATS
     unsigned long long lane_slots = 0, lane_live = 0;
@@ -290,9 +291,9 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             // region, so neighbouring rays reuse control blocks from L1/L2
             view = (int)(tile_id / per_view);
             const int t = (int)(tile_id % per_view);
-            const int st = t >> 6, lt = t & 63;
-            tx = (st % args.st_x) * 8 + (lt & 7);
-            ty = (st / args.st_x) * 8 + (lt >> 3);
+            const int st = t / kST2, lt = t % kST2;
+            tx = (st % args.st_x) * kST + lt % kST;
+            ty = (st / args.st_x) * kST + lt / kST;
             if (tx >= args.tiles_x || ty >= args.tiles_y) continue;
         }
 #if MFA_SMEM_FRAMES
