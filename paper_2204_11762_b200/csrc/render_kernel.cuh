@@ -289,11 +289,13 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         } else {
             // supertile order: the ~200 tiles in flight form a compact image
             // region, so neighbouring rays reuse control blocks from L1/L2
-            view = (int)(tile_id / per_view);
-            const int t = (int)(tile_id % per_view);
-            const int st = t / kST2, lt = t % kST2;
-            tx = (st % args.st_x) * kST + lt % kST;
-            ty = (st / args.st_x) * kST + lt / kST;
+            const unsigned tid32 = (unsigned)tile_id;   // < 2^29 (n_units < 2^32)
+            view = (int)(tid32 / (unsigned)per_view);
+            const unsigned t = tid32 - (unsigned)view * (unsigned)per_view;
+            const unsigned st = t / kST2, lt = t % kST2;
+            const unsigned sty = st / (unsigned)args.st_x;
+            tx = (int)((st - sty * (unsigned)args.st_x) * kST + lt % kST);
+            ty = (int)(sty * kST + lt / kST);
             if (tx >= args.tiles_x || ty >= args.tiles_y) continue;
         }
 #if MFA_SMEM_FRAMES
