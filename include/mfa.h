@@ -81,9 +81,10 @@ mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3],
 
 /*
  * mfa_model_create_ex -- as mfa_model_create, with options (NULL = defaults).
- * layout: MFA_LAYOUT_AUTO chooses Bezier blocks for models with a non-uniform
- *   axis and degree <= 3 (falling back to quads if the blocks do not fit in
- *   device memory), else bricked row quads.  MFA_LAYOUT_QUADS / _BEZIER force
+ * layout: MFA_LAYOUT_AUTO chooses Bezier blocks for degree <= 3 models with a
+ *   non-uniform axis, or whose blocks take <= 64 MiB (they then stay in L2);
+ *   falling back to quads if the blocks do not fit in device memory; else
+ *   bricked row quads.  MFA_LAYOUT_QUADS / _BEZIER force
  *   one (Bezier needs degree <= 3: MFA_ERR_UNSUPPORTED otherwise).
  *   Bezier blocks: for every knot-span triple the (p+1)^3 Bernstein
  *   coefficients of the spline there (Bezier extraction; 256 B per triple for

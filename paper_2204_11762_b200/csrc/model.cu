@@ -23,6 +23,8 @@
 
 namespace mfa {
 
+constexpr double kBezSmallModelBytes = 64.0 * 1024 * 1024;   // AUTO layout: uniform models up to this use Bezier blocks
+
 static thread_local std::string g_err;
 
 void set_error(const std::string& msg) { g_err = msg; }
@@ -481,7 +483,11 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
 
     // ---- control-point layout ----------------------------
     const bool nonuni = !(uniform[0] && uniform[1] && uniform[2]);
-    bool bez = want_layout == MFA_LAYOUT_BEZIER || (want_layout == MFA_LAYOUT_AUTO && nonuni && p <= 3);
+    // AUTO: Bezier blocks for non-uniform models, and for uniform ones whose
+    // blocks fit in a fraction of L2 (small models: every reload is an L2 hit)
+    const double bez_bytes = 4.0 * (p + 1) * (p + 1) * (p + 1) * (double)(nctrl[0] - p) * (nctrl[1] - p) * (nctrl[2] - p);
+    bool bez = want_layout == MFA_LAYOUT_BEZIER ||
+               (want_layout == MFA_LAYOUT_AUTO && p <= 3 && (nonuni || bez_bytes <= kBezSmallModelBytes));
     if (bez && p > 3) return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs degree <= 3"));
     if (bez && (nctrl[0] - p) * (nctrl[1] - p) * (nctrl[2] - p) >= ((int64_t)1 << 31)) {   // 32-bit block index
         if (want_layout == MFA_LAYOUT_BEZIER)

@@ -271,6 +271,7 @@ def test_both_layouts_eval_and_render(c, layout):
 def test_default_layouts():
     assert gpu_model(3).info()["layout"] == "quads"
     assert gpu_model(5).info()["layout"] == "bezier"
+    assert gpu_model(2).info()["layout"] == "bezier"   # uniform, but 58 MB of blocks: L2-resident
 
 
 @pytest.mark.parametrize("p", [2, 3])
