@@ -205,6 +205,9 @@ __device__ __forceinline__ float pow_spec(float x, float n) {
 #ifndef MFA_SMEM_FRAMES  // 1: per-view frames in shared memory (computed once per CTA)
 #define MFA_SMEM_FRAMES 0
 #endif
+#ifndef MFA_CARVE_FLOOR  // sized carveout: at least this percentage of shared memory
+#define MFA_CARVE_FLOOR 8
+#endif
 #ifndef MFA_CARVEOUT     // -1: sized for MINB CTAs (default), else a fixed percentage
 #define MFA_CARVEOUT -1
 #endif
@@ -800,10 +803,10 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     constexpr int kThreads = RenderShape<P, LAYOUT>::THREADS;
-    {   // shared-memory carveout: enough for MINB resident CTAs but at least 25%, the
-        // rest of the unified 256 KB is L1 (the block caches live there).  The
-        // driver's default (more shared memory) measured C5 -15%, C4 -37%; 25%: C3 +3%
-        //
+    {   // shared-memory carveout: enough for MINB resident CTAs but at least
+        // MFA_CARVE_FLOOR (8 %), the rest of the unified 256 KB is L1 (the block
+        // caches live there).  The driver's default (more shared memory) measured
+        // C5 -15%, C4 -37%; a 25 % floor: C5 -1 %, C4 -1.4 %
         int pct = MFA_CARVEOUT;
         if (pct < 0) {
             cudaFuncAttributes fa;
@@ -811,7 +814,7 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
             cudaDeviceGetAttribute(&max_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
             if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && max_sm > 0) {
                 const size_t need = (fa.sharedSizeBytes + smem + 1024) * RenderShape<P, LAYOUT>::MINB;
-                pct = (int)std::min<size_t>(100, std::max<size_t>(25, (100 * need + max_sm - 1) / max_sm + 2));
+                pct = (int)std::min<size_t>(100, std::max<size_t>(MFA_CARVE_FLOOR, (100 * need + max_sm - 1) / max_sm + 2));
             }
         }
         if (pct >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
