@@ -4,7 +4,8 @@ bench.py.  Tolerances are north_star's (BASELINE.json):
     sigma = the abs-scale of the same contraction (DESIGN.md R-5);
   * images: per pixel e = max_channel |I - I*| (minimum over the oracle's
     stored alternative outcomes, R-19); 99.9th percentile of e <= 2e-3 and
-    max e <= 1e-2 over pixels that are not shading-sensitive.
+    max e <= 1e-2 over ALL pixels (shading-sensitive pixels are counted and
+    reported, not excluded: the round-1 data had max_all <= 8.3e-5).
 """
 from __future__ import annotations
 
@@ -50,8 +51,9 @@ def check_image(gpu, ref, what=""):
     e = image_errors(gpu, ref)
     shade = (ref["flags"] & 4) != 0
     p999 = float(np.percentile(e, 99.9)) if len(e) else 0.0
-    mx = float(e[~shade].max()) if (~shade).any() else 0.0
-    stats = dict(p999=p999, max=mx, max_all=float(e.max()) if len(e) else 0.0,
+    mx = float(e.max()) if len(e) else 0.0
+    mx_ns = float(e[~shade].max()) if (~shade).any() else 0.0
+    stats = dict(p999=p999, max=mx, max_not_sensitive=mx_ns,
                  n=len(e), n_shade=int(shade.sum()), n_ert=int(((ref["flags"] & 1) != 0).sum()),
                  n_exit=int(((ref["flags"] & 2) != 0).sum()))
     assert p999 <= IMG_P999, f"{what}: p99.9 error {p999:.3e} > {IMG_P999} ({stats})"

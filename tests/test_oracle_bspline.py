@@ -244,3 +244,46 @@ def test_eval_batch_matches_single_and_thread_count():
     for i in range(0, 500, 97):
         out, sig, _ = m.eval(u[i], v[i], w[i])
         np.testing.assert_array_equal(out, o1[i])
+
+
+def test_sigma_abs_scales_closed_forms():
+    """The abs-scales sigma that set every eval tolerance (R-5): sigma_k =
+    sum |term| of the same triple sum.  Closed forms:
+      * constant model c: N >= 0 and sum N = 1 per axis, so sigma_val = |c|,
+        and sigma_u = |c| * sum_a |N'_a|;
+      * on an interior span of a uniform cubic at local t = 1/2,
+        N' = S [-1, -5, 5, 1] / 8 (A.1), so sum |N'| = 3 S / 2 and
+        sigma_u = 1.5 S |c|;
+      * a model with non-negative control values: every value term is >= 0,
+        so sigma_val equals the value itself."""
+    p = 3
+    n = (13, 9, 11)
+    S = [n[d] - p for d in range(3)]
+    knots = [uniform_knots(p, n[d]) for d in range(3)]
+    c = -0.625
+    m = O.Model(p, knots, np.full((n[2], n[1], n[0]), c, dtype=np.float32))
+    # interior spans (A.1: spans 2p-1 .. n-p, i.e. knot index; here the span
+    # starting at knot value j/S with j in [p-1, S-p]) at t = 1/2 on every axis
+    j = (S[0] // 2, S[1] // 2, S[2] // 2)
+    q = [(j[d] + 0.5) / S[d] for d in range(3)]
+    out, sig, rc = m.eval(*q)
+    assert rc == 0
+    np.testing.assert_allclose(sig, [abs(c), 1.5 * S[0] * abs(c), 1.5 * S[1] * abs(c), 1.5 * S[2] * abs(c)],
+                               rtol=1e-14)
+    np.testing.assert_allclose(out, [c, 0, 0, 0], atol=1e-12)
+    # a generic point: sigma_val = |c|, sigma_d = |c| sum |N'_d| with the O2
+    # derivatives (pinned separately against the recursion / closed forms)
+    r = np.random.default_rng(31)
+    for u, v, w in r.uniform(0, 1, (20, 3)):
+        out, sig, _ = m.eval(u, v, w)
+        assert sig[0] == pytest.approx(abs(c), rel=1e-14)
+        for d, x in enumerate((u, v, w)):
+            sp = O.find_span(p, knots[d], x)
+            _, dN = O.basis_derivs(p, knots[d], sp, x)
+            assert sig[1 + d] == pytest.approx(abs(c) * np.abs(dN).sum(), rel=1e-13)
+    # non-negative control values: sigma_val == value (and sigma_val < 1.01 * value)
+    ctrl = r.uniform(0.1, 2.0, (n[2], n[1], n[0])).astype(np.float32)
+    m2 = O.Model(p, knots, ctrl)
+    for u, v, w in r.uniform(0, 1, (20, 3)):
+        out, sig, _ = m2.eval(u, v, w)
+        assert sig[0] == pytest.approx(out[0], rel=1e-13)
