@@ -51,11 +51,35 @@ def parse():
     ap.add_argument("--out-fp16", action="store_true")
     ap.add_argument("--no-shading", action="store_true",
                     help="NEXT-1: Algorithm 1 with ShadingOn = false (value-only basis and contraction)")
+    ap.add_argument("--skip-transparent-gradient", action="store_true",
+                    help="NEXT-1 variant: shading = 2 (no gradient / Phong for samples with TF opacity 0; "
+                         "identical image)")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: direct NVLink stores into rank 0's image (p2p) or packed tiles + NCCL all-gather")
     ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier"],
                     help="control-point layout (default: the library's choice)")
+    ap.add_argument("--assign", default="auto", choices=["auto", "views", "rows", "diagonal"],
+                    help="N > 1: how (view, tile) units are dealt to ranks (dist.assign_units)")
+    ap.add_argument("--emulate", type=int, default=0, metavar="G",
+                    help="one GPU: render each of G ranks' unit lists alone (every assignment mode) and "
+                         "report the projected G-GPU time = the slowest rank's")
     return ap.parse_args()
+
+
+def maybe_spawn(args):
+    """`python bench.py --gpus N` without a launcher: re-run this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1), so the line
+    printed always reports the N it ran on."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl != "ours" or args.emulate:
+        return None
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -200,16 +224,32 @@ def run_ours(args):
     from paper_2204_11762_b200 import Model, dist as D, roofline as RL, unpack_tiles, workloads as WL
 
     rank, world, local = dist_env()
-    assert world == args.gpus or world == 1, "launch N>1 with torch.distributed.run"
-    torch.cuda.set_device(local)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    ndev = torch.cuda.device_count()
+    if ndev < 1:
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    shared_dev = world > 1 and ndev < world     # functional multi-process run on fewer GPUs than ranks
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    notes = []
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_dev:
+            # NCCL refuses two ranks on one device: gloo for the control plane,
+            # the direct-store (CUDA IPC) image for the pixels
+            dist.init_process_group("gloo")
+            notes.append(f"{world} ranks share {ndev} GPU(s): functional run, not a scaling number")
+            if args.gather == "nccl":
+                notes.append("--gather nccl needs one GPU per rank: using p2p")
+                args.gather = "p2p"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     c = int(args.workload[1:])
     kw = {"n_views": args.views} if args.views else {}
     w = WL.make_config(c, **kw)
-    if args.no_shading:
+    if args.no_shading or args.skip_transparent_gradient:
         import dataclasses
-        w.params = dataclasses.replace(w.params, shading=0)
+        w.params = dataclasses.replace(w.params, shading=0 if args.no_shading else 2)
     V = len(w.cameras)
     W, H = w.cameras[0].width, w.cameras[0].height
     stream = torch.cuda.current_stream()
@@ -219,6 +259,8 @@ def run_ours(args):
     out_dt = torch.float16 if args.out_fp16 else torch.float32
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     launches_per_step = 0
+    mode = D.pick_mode(V, world) if args.assign == "auto" else args.assign
+    img = None
 
     if world == 1:
         img = torch.empty((V, H, W, 4), dtype=out_dt, device="cuda")
@@ -226,33 +268,52 @@ def run_ours(args):
 
         def step():
             m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, out=img, samples=cnt, out_fp16=args.out_fp16)
-    elif args.gather == "p2p":
-        # every rank's render kernel stores its pixels straight into rank 0's
-        # image over NVLink (CUDA IPC mapping): compute and transfer in one kernel
-        lists = D.assign_units(V, W, H, world)
-        mine = torch.from_numpy(lists[rank]).cuda()
-        img0 = torch.empty((V, H, W, 4), dtype=out_dt, device="cuda") if rank == 0 else None
-        img = D.peer_image(img0, rank)
-        launches_per_step = 1
-
-        def step():
-            m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=mine, out=img, samples=cnt,
-                     out_fp16=args.out_fp16, scatter=True)
     else:
-        lists = D.assign_units(V, W, H, world)
-        mine = torch.from_numpy(lists[rank]).cuda()
-        tiles_all = torch.from_numpy(np.concatenate(lists)).cuda()
-        packed = torch.empty((len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
-        gathered = torch.empty((world * len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
-        img = torch.empty((V, H, W, 4), dtype=torch.float32, device="cuda") if rank == 0 else None
-        launches_per_step = 1 + (1 if rank == 0 else 0)
+        if args.gather == "p2p":
+            # every rank's render kernel stores its pixels straight into rank 0's
+            # image over NVLink (libmfa-allocated, CUDA IPC mapped): compute and
+            # transfer in one kernel
+            img, err = D.shared_image((V, H, W, 4), out_dt, rank)
+            if img is None:
+                notes.append(f"direct-store image unavailable ({err}): NCCL fallback")
+                args.gather = "nccl"
+        if args.gather == "p2p":
+            mine = torch.from_numpy(D.assign_units(V, W, H, world, mode, pad=False)[rank]).cuda()
+            launches_per_step = 1
 
-        def step():
-            m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=mine, out=packed, samples=cnt,
-                     out_fp16=args.out_fp16)
-            dist.all_gather_into_tensor(gathered, packed)
-            if rank == 0:
-                unpack_tiles(gathered, tiles_all, V, W, H, out=img)
+            def step():
+                m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=mine, out=img, samples=cnt,
+                         out_fp16=args.out_fp16, scatter=True)
+        elif mode == "views":
+            # per view: render, then send on a comm stream while the next view
+            # renders; rank 0 receives straight into its image slices
+            img = torch.empty((V, H, W, 4), dtype=out_dt, device="cuda") if rank == 0 else None
+            bufs = [torch.empty((H, W, 4), dtype=out_dt, device="cuda") for _ in range(2)] if rank else None
+            comm = torch.cuda.Stream()
+            launches_per_step = len(D.rank_views(V, world, rank))
+
+            def render_view(v, out):
+                m.render([w.cameras[v]], tf, w.v_lo, w.v_hi, w.params, out=out.view(1, H, W, 4), samples=cnt,
+                         out_fp16=args.out_fp16)
+
+            def step():
+                for wk in D.gather_views_nccl(render_view, img, V, rank, world, bufs=bufs, comm=comm):
+                    wk.wait()
+        else:
+            lists = D.assign_units(V, W, H, world, mode)
+            mine = torch.from_numpy(lists[rank]).cuda()
+            tiles_all = torch.from_numpy(np.concatenate(lists)).cuda()
+            packed = torch.empty((len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
+            gathered = torch.empty((world * len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
+            img = torch.empty((V, H, W, 4), dtype=torch.float32, device="cuda") if rank == 0 else None
+            launches_per_step = 1 + (1 if rank == 0 else 0)
+
+            def step():
+                m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=mine, out=packed, samples=cnt,
+                         out_fp16=args.out_fp16)
+                dist.all_gather_into_tensor(gathered, packed)
+                if rank == 0:
+                    unpack_tiles(gathered, tiles_all, V, W, H, out=img)
 
     # ---- warm-up, then exactly K timed steps ------------------------------
     for _ in range(args.warmup):
@@ -281,8 +342,9 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1)
     kernel_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
     samples = int(cnt.item())
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    s = torch.tensor([samples], dtype=torch.int64, device="cuda")
+    red_dev = "cuda" if (world > 1 and dist.get_backend() == "nccl") else "cpu"
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+    s = torch.tensor([samples], dtype=torch.int64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(s, op=dist.ReduceOp.SUM)
@@ -294,8 +356,8 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (render) --------------------------
     p = w.degree
     F = RL.flops_per_sample(p, bool(w.params.shading))
-    per_launch_samples = samples / args.steps / max(1, (V + 63) // 64 if world == 1 else 1)
-    launch_ms = kernel_ms / max(1, (V + 63) // 64 if world == 1 else 1)
+    per_launch_samples = samples / args.steps / max(1, launches_per_step)
+    launch_ms = kernel_ms / max(1, launches_per_step)
     achieved_tf = F * per_launch_samples / (launch_ms / 1e3) / 1e12
     peak_tf, peak_src = RL.fp32_peak_tflops()
     Bs = RL.bytes_per_sample(p)
@@ -305,6 +367,9 @@ def run_ours(args):
             "launch_ms": launch_ms, "peak_source": peak_src,
             "counted_bytes_per_sample": Bs,
             "l2_counted_GBps": Bs * per_launch_samples / (launch_ms / 1e3) / 1e9}
+    if int(w.params.shading) == 2:
+        roof["note"] = ("NEXT-1 variant (shading = 2): samples with TF opacity 0 skip the gradient contraction and "
+                        "Phong, so F(p) overstates the work done; not a roofline claim")
     if clocks.get("sm_mhz"):
         pk_clk, _ = RL.fp32_peak_tflops(clocks["sm_mhz"])
         roof["frac_at_observed_clock"] = achieved_tf / pk_clk
@@ -385,10 +450,15 @@ def run_ours(args):
                        "layout": info["layout"],
                        "shading": int(w.params.shading), "o_max": w.params.o_max,
                        "out": "fp16" if args.out_fp16 else "fp32",
-                       "parallelism": (f"screen-tile sharding x{world}, model replicated, "
-                                       + ("render kernels store into rank 0's image over NVLink (CUDA IPC)"
-                                          if args.gather == "p2p" else "NCCL all-gather + unpack"))
+                       "parallelism": (f"screen-tile sharding x{world} (assignment: {mode}), model replicated, "
+                                       + ("render kernels store into rank 0's image over NVLink (CUDA IPC, "
+                                          "libmfa-allocated)" if args.gather == "p2p" else
+                                          ("per-view NCCL send/recv on a comm stream, overlapped with the next "
+                                           "view's render" if mode == "views" else "NCCL all-gather + unpack")))
                        if world > 1 else "single GPU",
+                       "model_bytes": info["model_bytes"], "device_bytes": info["device_bytes"],
+                       "footprint_ratio": info["device_bytes"] / info["model_bytes"],
+                       "create_ms": info["create_ms"],
                        "l2": f"inputs larger than L2: {info['layout']} control-point layout {info['device_bytes'] / 2**20:.0f} MiB, "
                              f"image {V * H * W * (8 if args.out_fp16 else 16) / 2**20:.0f} MiB per step"},
             "frames_per_s": V * args.steps / (ms_max / 1e3),
@@ -401,6 +471,8 @@ def run_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }
+        if notes:
+            res["notes"] = notes
         print(json.dumps(res))
     if world > 1:
         dist.destroy_process_group()
@@ -508,7 +580,41 @@ def run_e2e(args, w, m, world, rank, local, out_dt):
         return {"value": tot / dt, "unit": UNIT, "h2d_bytes_per_step": tf_bytes + cam_bytes,
                 "d2h_bytes_per_step": V * H * W * 4 * el + 8, "api": "mfa_render_host (C ABI, host buffers)",
                 "steps": K, "timer": "wall clock around the blocking call"}
-    lists = D.assign_units(V, W, H, world)
+    mode = D.pick_mode(V, world) if args.assign == "auto" else args.assign
+    if mode == "views":
+        # every rank renders its own views and copies them over its own PCIe
+        # link straight into their slots of ONE host image shared by all ranks
+        # (a /dev/shm mapping, page-locked with cudaHostRegister in each rank)
+        host, cleanup = shared_host_image(V, H, W, el, rank, world)
+        mv = D.rank_views(V, world, rank)
+        cams = [w.cameras[v] for v in mv]
+        view_bytes = H * W * 4 * el
+        ptrs = [host.data_ptr() + v * view_bytes for v in mv]
+        m.render_host_views(cams, w.tf, w.v_lo, w.v_hi, w.params, ptrs, out_fp16=(out_dt == torch.float16))
+        dist.barrier()
+        tot = 0
+        t0 = time.perf_counter()
+        for _ in range(K):
+            tot += m.render_host_views(cams, w.tf, w.v_lo, w.v_hi, w.params, ptrs,
+                                       out_fp16=(out_dt == torch.float16))
+        dt_local = time.perf_counter() - t0
+        dist.barrier()
+        ok = True
+        if rank == 0:   # spot check: every view landed (alpha of the centre pixel is finite)
+            ok = bool(torch.isfinite(host.view(-1)[::max(1, host.numel() // 4096)].float()).all())
+        dt = torch.tensor([dt_local], dtype=torch.float64)
+        s = torch.tensor([tot], dtype=torch.int64)
+        if dist.get_backend() == "nccl":
+            dt, s = dt.cuda(), s.cuda()
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        cleanup()
+        return {"value": int(s.item()) / float(dt.item()), "unit": UNIT, "h2d_bytes_per_step": (tf_bytes + cam_bytes) * world,
+                "d2h_bytes_per_step": V * view_bytes + 8 * world,
+                "api": "mfa_render_host_views (C ABI, host buffers): each rank's views straight into a host image "
+                       "shared by the ranks (/dev/shm + cudaHostRegister)",
+                "steps": K, "timer": "wall clock around the blocking calls, max over ranks", "host_image_ok": ok}
+    lists = D.assign_units(V, W, H, world, mode)
     mine = torch.from_numpy(lists[rank]).cuda()
     tiles_all = torch.from_numpy(np.concatenate(lists)).cuda()
     tf_host = torch.from_numpy(w.tf).pin_memory()
@@ -518,8 +624,11 @@ def run_e2e(args, w, m, world, rank, local, out_dt):
     img = torch.empty((V, H, W, 4), dtype=torch.float32, device="cuda") if rank == 0 else None
     packed = torch.empty((len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
     gathered = torch.empty((world * len(lists[rank]), 16, 16, 4), dtype=out_dt, device="cuda")
-
-    peer = D.peer_image(img, rank) if args.gather == "p2p" else None
+    peer = None
+    if args.gather == "p2p":
+        peer, _ = D.shared_image((V, H, W, 4), torch.float32, rank)
+        if rank == 0 and peer is not None:
+            img = peer
 
     def step():
         tf_dev.copy_(tf_host, non_blocking=True)
@@ -544,21 +653,132 @@ def run_e2e(args, w, m, world, rank, local, out_dt):
     for _ in range(K):
         step()
     torch.cuda.synchronize()
-    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-    s = cnt.clone()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    s = cnt.clone().cpu()
+    if dist.get_backend() == "nccl":
+        dt, s = dt.cuda(), s.cuda()
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     dist.all_reduce(s, op=dist.ReduceOp.SUM)
     return {"value": int(s.item()) / float(dt.item()), "unit": UNIT, "h2d_bytes_per_step": tf_bytes + cam_bytes,
             "d2h_bytes_per_step": V * H * W * 16,
-            "api": "Model.render (tiles) + " + ("NVLink stores into rank 0's image" if args.gather == "p2p"
-                                                 else "NCCL + unpack") + ", host copies",
+            "api": "Model.render (tiles) + " + ("NVLink stores into rank 0's image" if peer is not None
+                                                 else "NCCL + unpack") + ", rank 0 host copy",
             "steps": K, "timer": "wall clock, max over ranks"}
+
+
+def shared_host_image(V, H, W, el, rank, world):
+    """A [V,H,W,4] host image shared by the ranks of this node: rank 0
+    creates a /dev/shm file, every rank maps it and page-locks its mapping
+    (cudaHostRegister) so its device->host copies run at full PCIe speed.
+    Returns (uint8-backed torch tensor [V*H*W*4*el bytes], cleanup)."""
+    import mmap
+
+    import torch
+    import torch.distributed as dist
+    nbytes = V * H * W * 4 * el
+    name = [f"/dev/shm/mfa_bench_img_{os.getpid()}" if rank == 0 else None]
+    if rank == 0:
+        with open(name[0], "wb") as f:
+            f.truncate(nbytes)
+    dist.broadcast_object_list(name, src=0)
+    fd = os.open(name[0], os.O_RDWR)
+    mm = mmap.mmap(fd, nbytes)
+    os.close(fd)
+    t = torch.frombuffer(mm, dtype=torch.uint8)
+    cr = torch.cuda.cudart()
+    reg = cr.cudaHostRegister(t.data_ptr(), nbytes, 0) == 0 if hasattr(cr, "cudaHostRegister") else False
+
+    def cleanup():
+        nonlocal t
+        if reg:
+            cr.cudaHostUnregister(t.data_ptr())
+        dist.barrier()
+        del t
+        try:
+            mm.close()
+        except BufferError:
+            pass
+        if rank == 0:
+            os.unlink(name[0])
+    return t, cleanup
+
+
+def run_emulate(args):
+    """One GPU, G emulated ranks: for each assignment mode render every
+    rank's unit list alone (tiles, stored at their image positions) and time
+    it with CUDA events.  The projected G-GPU step is the slowest rank; its
+    efficiency against the 1-GPU full-frame launch shows what the partition
+    costs in locality and balance (no transfer is modelled: the direct-store
+    path overlaps it with the render)."""
+    import torch
+
+    from paper_2204_11762_b200 import Model, dist as D, workloads as WL
+    G = args.emulate
+    torch.cuda.set_device(0)
+    c = int(args.workload[1:])
+    kw = {"n_views": args.views} if args.views else {}
+    w = WL.make_config(c, **kw)
+    V = len(w.cameras)
+    W, H = w.cameras[0].width, w.cameras[0].height
+    m = Model.from_workload(w, layout=args.layout)
+    tf = torch.from_numpy(w.tf).cuda()
+    stream = torch.cuda.current_stream()
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    full = torch.empty((V, H, W, 4), device="cuda")
+    reps = max(1, args.steps)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cnt.zero_()
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps, int(cnt.item()) // reps
+
+    t1, s1 = timed(lambda: m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, out=full, samples=cnt))
+    res = {"metric": "emulated multi-GPU step (slowest rank), 1 GPU", "workload": w.name, "G": G,
+           "one_gpu_ms": t1, "one_gpu_samples_per_s": s1 / (t1 / 1e3), "modes": {}}
+    img = torch.empty_like(full)
+    for mode in ("views", "rows", "diagonal"):
+        if mode == "views" and V < G:
+            continue
+        lists = D.assign_units(V, W, H, G, mode, pad=False)
+        img.fill_(-1.0)
+        per = []
+        tot = 0
+        for r in range(G):
+            tl = torch.from_numpy(lists[r]).cuda()
+            if len(tl) == 0:
+                per.append(0.0)
+                continue
+            ms, sr = timed(lambda: m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=tl, out=img,
+                                            samples=cnt, scatter=True))
+            per.append(ms)
+            tot += sr
+        tmax = max(per)
+        res["modes"][mode] = {"rank_ms": per, "step_ms": tmax, "samples": tot,
+                              "projected_samples_per_s": tot / (tmax / 1e3),
+                              "efficiency_vs_1gpu": t1 / (G * tmax),
+                              "work_sum_vs_1gpu": sum(per) / t1,
+                              "balance_max_over_mean": tmax / (sum(per) / G),
+                              "bit_identical_to_1gpu": bool(torch.equal(img, full))}
+    print(json.dumps(res))
+    return 0
 
 
 def main():
     args = parse()
+    r = maybe_spawn(args)
+    if r is not None:
+        return r
     if args.impl == "reference":
         return run_reference(args)
+    if args.emulate:
+        return run_emulate(args)
     return run_ours(args)
 
 

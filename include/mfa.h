@@ -26,6 +26,7 @@
 #ifndef MFA_H
 #define MFA_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -39,7 +40,9 @@ typedef enum {
     MFA_OK = 0,
     MFA_ERR_INVALID_ARG = 1,  /* NULL pointer, bad size, inconsistent shapes */
     MFA_ERR_KNOTS = 2,        /* knot vector violates S:24-27 (length, order, clamping, multiplicity) */
-    MFA_ERR_UNSUPPORTED = 3,  /* degree outside {1..5} or unequal per axis; > MFA_MAX_VIEWS handled by splitting */
+    MFA_ERR_UNSUPPORTED = 3,  /* degree outside {1..5} or unequal per axis; a tiled render of more than
+                                 64 views in one call; more than 256 renders of one model in flight
+                                 on distinct streams */
     MFA_ERR_DOMAIN = 4,       /* non-finite control value */
     MFA_ERR_CUDA = 5,         /* a CUDA runtime error (message has the CUDA error string) */
     MFA_ERR_OOM = 6,          /* device allocation failed */
@@ -72,8 +75,11 @@ typedef enum {
  *             before returning.
  * out         receives the model handle (NULL on failure).
  *
- * Device memory: bricked row quads ~ 16 (1 + p/16)^2 n_u n_v n_w bytes, or
- * Bezier blocks (see mfa_model_create_ex), plus per-axis span tables (< 1 MB).
+ * Device memory: bricked row quads ~ 16 quad_f4(p) (1 + p/16)^2 n_u n_v n_w
+ * bytes (quad_f4 = 2 for p <= 3: 32-byte row pairs, about 45 B per control
+ * point at p = 3; 1 for p >= 4), or Bezier blocks (see
+ * mfa_model_create_ex), plus per-axis span tables (< 1 MB); mfa_model_info
+ * reports device_bytes / model_bytes.
  * ---------------------------------------------------------------------- */
 mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3],
                             const double* const knots[3], const float* ctrl,
@@ -111,6 +117,10 @@ typedef struct {
     int64_t device_bytes;   /* device memory owned by the model */
     int32_t device;         /* CUDA ordinal the model lives on */
     int32_t layout;         /* MFA_LAYOUT_QUADS or MFA_LAYOUT_BEZIER */
+    int64_t model_bytes;    /* the fp32 control grid as passed: 4 n_u n_v n_w (the model
+                               size depends on the control-point count) */
+    double create_ms;       /* wall time of mfa_model_create (validation, upload, relayout,
+                               span tables, the closing stream synchronisation) */
 } mfa_model_desc;
 
 mfa_status mfa_model_info(mfa_model m, mfa_model_desc* out);
@@ -132,6 +142,11 @@ mfa_status mfa_model_destroy(mfa_model m);
  *             by the number of points outside [0,1]^3 or NaN.  Those points
  *             get NaN outputs (batched form of S:74's domain error, R-18).
  * n == 0 is valid and enqueues nothing.
+ * For n >= 2^16 the call takes the binned path of mfa_eval_batch_ws with
+ * STREAM-ORDERED scratch (cudaMallocAsync / cudaFreeAsync on `stream` from
+ * the device's default memory pool, ~20 B per point; the pool's release
+ * threshold is raised once so the blocks stay cached between calls); if the
+ * pool cannot serve it, the unbinned kernel runs instead (same outputs).
  * ---------------------------------------------------------------------- */
 mfa_status mfa_eval_batch(mfa_model m, int64_t n, const float* u, const float* v, const float* w,
                           float* value, float* du, float* dv, float* dw,
@@ -141,12 +156,12 @@ mfa_status mfa_eval_batch(mfa_model m, int64_t n, const float* u, const float* v
  * mfa_eval_batch_ws -- mfa_eval_batch with a caller-owned device workspace of
  * at least mfa_eval_workspace_bytes(m, n) bytes (~20 B per point).  For
  * n >= 2^16 the points are first grouped by a coarse parameter-space bin
- * (~16^3 knot spans per bin; a counting sort into (u, v, w, index) records)
+ * (~8^3 knot spans per bin; a counting sort into (u, v, w, index) records)
  * and evaluated in bin order, results written at their original indices:
  * neighbouring points then share control-point neighbourhoods in L1/L2
  * instead of each pulling ~16 separate lines from HBM.  Same outputs as
- * mfa_eval_batch (each point's arithmetic is unchanged); workspace == NULL is
- * mfa_eval_batch.
+ * mfa_eval_batch (each point's arithmetic is unchanged); workspace == NULL runs
+ * the unbinned kernel (one point per thread in input order).
  */
 size_t mfa_eval_workspace_bytes(mfa_model m, int64_t n);
 mfa_status mfa_eval_batch_ws(mfa_model m, int64_t n, const float* u, const float* v, const float* w,
@@ -165,7 +180,8 @@ mfa_status mfa_eval_batch_ws(mfa_model m, int64_t n, const float* u, const float
  * hess        device fp32 [6][n] (required): d2F/du2, d2F/dv2, d2F/dw2,
  *             d2F/dudv, d2F/dudw, d2F/dvdw (parameter space).
  * n_domain_errors, errors, n == 0: as mfa_eval_batch (NaN outputs for points
- * outside [0,1]^3).  Async on stream.
+ * outside [0,1]^3).  Async on stream.  For n >= 2^16 the binned path runs with
+ * stream-ordered scratch (~68 B per point), as mfa_eval_batch.
  * ---------------------------------------------------------------------- */
 mfa_status mfa_eval_hessian(mfa_model m, int64_t n, const float* u, const float* v, const float* w,
                             float* value, float* grad, float* hess,
@@ -208,7 +224,12 @@ typedef struct {
     double box_min[3], box_max[3];   /* world placement of the parameter cube */
     double step;                     /* sample distance, world units (> 0) */
     double o_max;                    /* ERT threshold O_Max (l.14); >= 1 disables ERT */
-    int32_t shading;                 /* ShadingOn (l.8) */
+    int32_t shading;                 /* ShadingOn (l.8): 0 off (value only), 1 on (the gradient is
+                                        queried for every sample, R-20), 2 on with the gradient and
+                                        Phong skipped for samples whose TF opacity is 0 (NEXT-1's
+                                        variant: they composite with weight 0, so the image and the
+                                        sample count equal shading = 1's; degree <= 3 models, other
+                                        layouts run shading = 1) */
     double ka, kd, ks, shininess;    /* Phong constants */
     double grad_eps;                 /* |physical gradient| <= grad_eps -> ambient only (R-11) */
     int32_t out_fp16;                /* 0: fp32 RGBA (16 B/px); 1: fp16 RGBA (8 B/px) */
@@ -252,15 +273,30 @@ mfa_status mfa_render(mfa_model m, int32_t n_views, const mfa_camera* cams, cons
  * HOST buffers: tf_rgba_host (n_entries x 4 fp32) is copied in, and the image
  * [n_views][H][W][4] (fp32 or fp16 per prm->out_fp16) is written to
  * rgba_host, view by view, with the device->host copy of view v overlapping
- * the rendering of view v+1 (two device staging buffers, two streams).
- * rgba_host should be page-locked for the copies to overlap.  samples_host
- * (optional) receives the composited-sample count.  Returns after the image
- * is on the host.
+ * the rendering of view v+1 (two device staging buffers, the caller's stream
+ * and a copy stream).  The staging buffers, copy stream, events and the
+ * device TF / counter are owned by the MODEL: created on the first call
+ * (2 x one view of device memory), reused by later calls, freed by
+ * mfa_model_destroy; host-buffer renders of one model are serialised (a
+ * mutex).  rgba_host should be page-locked for the copies to overlap.
+ * samples_host (optional) receives the composited-sample count.  Returns
+ * after the image is on the host.
  */
 mfa_status mfa_render_host(mfa_model m, int32_t n_views, const mfa_camera* cams,
                            const float* tf_rgba_host, int32_t tf_n_entries, float v_lo, float v_hi,
                            const mfa_render_params* prm, void* rgba_host,
                            unsigned long long* samples_host, mfa_stream stream);
+
+/*
+ * mfa_render_host_views -- mfa_render_host with one host destination per view
+ * (rgba_host_views[v] receives view v, [H][W][4]); e.g. the views a rank of a
+ * multi-GPU job renders, written straight into their slots of a host image
+ * shared by all ranks.  Same ownership, overlap and errors as mfa_render_host.
+ */
+mfa_status mfa_render_host_views(mfa_model m, int32_t n_views, const mfa_camera* cams,
+                                 const float* tf_rgba_host, int32_t tf_n_entries, float v_lo, float v_hi,
+                                 const mfa_render_params* prm, void* const* rgba_host_views,
+                                 unsigned long long* samples_host, mfa_stream stream);
 
 /*
  * mfa_unpack_tiles -- scatter a packed tile buffer [n_tiles][16][16][4] (as
@@ -458,6 +494,20 @@ mfa_status mfa_ipc_open(const void* handle, void** base_out);
 
 /* mfa_ipc_close -- unmap an allocation mapped by mfa_ipc_open. */
 mfa_status mfa_ipc_close(void* base);
+
+/*
+ * mfa_ipc_alloc -- allocate `bytes` of device memory on the CURRENT device
+ * (cudaMalloc: a whole allocation, so its IPC handle maps exactly this
+ * buffer) and export it: *ptr_out = the device pointer, handle_out (64
+ * bytes, caller-owned) = its cudaIpcMemHandle_t for mfa_ipc_open in another
+ * process.  Used for the multi-GPU direct-store image (rank 0's image that
+ * every rank's render kernel stores into over NVLink).  The caller owns the
+ * buffer: mfa_ipc_free(ptr) after every mapping process has closed it.
+ * Errors: MFA_ERR_INVALID_ARG (NULL outputs, bytes == 0), MFA_ERR_OOM,
+ * MFA_ERR_CUDA (export failed).
+ */
+mfa_status mfa_ipc_alloc(size_t bytes, void** ptr_out, void* handle_out);
+mfa_status mfa_ipc_free(void* ptr);
 
 /* Thread-local message for the last non-OK status on this thread ("" if none). */
 const char* mfa_last_error(void);

@@ -22,11 +22,11 @@ LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2}
 
 # C-ABI symbols declared in include/mfa.h (checked by tests/test_abi.py)
 EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
-           "mfa_render_host", "mfa_unpack_tiles", "mfa_last_error", "mfa_version",
+           "mfa_render_host", "mfa_render_host_views", "mfa_unpack_tiles", "mfa_last_error", "mfa_version",
            "mfa_render_field", "mfa_image_quality", "mfa_image_quality_workspace", "mfa_eval_hessian",
            "mfa_fit_grid", "mfa_encode_grid", "mfa_eval_batch_ws", "mfa_eval_workspace_bytes", "mfa_render_ex",
            "mfa_eval_hessian_ws", "mfa_hessian_workspace_bytes", "mfa_enable_peer_access",
-           "mfa_ipc_open", "mfa_ipc_close", "mfa_probe_fp32", "mfa_probe_read_bw")
+           "mfa_ipc_open", "mfa_ipc_close", "mfa_ipc_alloc", "mfa_ipc_free", "mfa_probe_fp32", "mfa_probe_read_bw")
 
 
 class MfaError(RuntimeError):
@@ -59,7 +59,8 @@ class Tiles_t(C.Structure):
 class ModelDesc_t(C.Structure):
     _fields_ = [("degree", C.c_int32 * 3), ("nctrl", C.c_int64 * 3), ("uniform", C.c_int32 * 3),
                 ("v_min", C.c_float), ("v_max", C.c_float), ("device_bytes", C.c_int64),
-                ("device", C.c_int32), ("layout", C.c_int32)]
+                ("device", C.c_int32), ("layout", C.c_int32), ("model_bytes", C.c_int64),
+                ("create_ms", C.c_double)]
 
 
 class Field_t(C.Structure):
@@ -149,6 +150,13 @@ def lib():
         L.mfa_render_host.restype = C.c_int
         L.mfa_render_host.argtypes = [vp, i32, C.POINTER(Camera_t), vp, i32, C.c_float, C.c_float,
                                       C.POINTER(RenderParams_t), vp, vp, vp]
+        L.mfa_render_host_views.restype = C.c_int
+        L.mfa_render_host_views.argtypes = [vp, i32, C.POINTER(Camera_t), vp, i32, C.c_float, C.c_float,
+                                            C.POINTER(RenderParams_t), C.POINTER(C.c_void_p), vp, vp]
+        L.mfa_ipc_alloc.restype = C.c_int
+        L.mfa_ipc_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p), C.c_char_p]
+        L.mfa_ipc_free.restype = C.c_int
+        L.mfa_ipc_free.argtypes = [vp]
         L.mfa_unpack_tiles.restype = C.c_int
         L.mfa_unpack_tiles.argtypes = [vp, i32, vp, i64, i32, i32, i32, vp, vp]
         L.mfa_last_error.restype = C.c_char_p
@@ -259,7 +267,8 @@ class Model:
         _check(lib().mfa_model_info(self._h, C.byref(d)))
         return dict(degree=tuple(d.degree), nctrl=tuple(d.nctrl), uniform=tuple(d.uniform),
                     v_min=d.v_min, v_max=d.v_max, device_bytes=d.device_bytes, device=d.device,
-                    layout={1: "quads", 2: "bezier"}.get(d.layout, d.layout))
+                    layout={1: "quads", 2: "bezier"}.get(d.layout, d.layout), model_bytes=d.model_bytes,
+                    create_ms=d.create_ms)
 
     def close(self):
         if self._h and self._h.value:
@@ -273,11 +282,13 @@ class Model:
             pass
 
     # -- queryValueMFA / queryGradientMFA (mfa_eval_batch) --------------------
-    def eval(self, u, v, w, grad=True, out=None, n_domain_errors=None, stream=None, binned=True):
+    def eval(self, u, v, w, grad=True, out=None, n_domain_errors=None, stream=None, binned="auto"):
         """u, v, w: CUDA fp32 tensors (n,).  Returns (value, du, dv, dw)
-        (parameter-space partials), or (value,) if grad is False.  binned:
-        large batches go through mfa_eval_batch_ws (spatial binning, a
-        workspace from torch's allocator)."""
+        (parameter-space partials), or (value,) if grad is False.
+        binned: "auto" = the north_star call mfa_eval_batch (large batches are
+        binned with stream-ordered scratch from the device pool); True =
+        mfa_eval_batch_ws with a workspace from torch's allocator; False =
+        mfa_eval_batch_ws without a workspace (the unbinned kernel)."""
         import torch
         n = u.numel()
         dev = u.device
@@ -285,32 +296,37 @@ class Model:
             out = tuple(torch.empty(n, device=dev, dtype=torch.float32) for _ in range(4 if grad else 1))
         val = out[0]
         du, dv, dw = (out[1], out[2], out[3]) if grad else (None, None, None)
+        if binned == "auto":
+            _check(lib().mfa_eval_batch(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(du), _ptr(dv),
+                                        _ptr(dw), _ptr(n_domain_errors), _stream_ptr(stream)))
+            return out
+        ws, nb = None, 0
         if binned and n >= (1 << 16):
             nb = int(lib().mfa_eval_workspace_bytes(self._h, n))
             ws = torch.empty(nb, dtype=torch.uint8, device=dev)   # stream-ordered by torch's allocator
-            _check(lib().mfa_eval_batch_ws(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(du), _ptr(dv),
-                                           _ptr(dw), _ptr(n_domain_errors), _ptr(ws), nb, _stream_ptr(stream)))
-        else:
-            _check(lib().mfa_eval_batch(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(du), _ptr(dv),
-                                        _ptr(dw), _ptr(n_domain_errors), _stream_ptr(stream)))
+        _check(lib().mfa_eval_batch_ws(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(du), _ptr(dv),
+                                       _ptr(dw), _ptr(n_domain_errors), _ptr(ws), nb, _stream_ptr(stream)))
         return out
 
-    def eval_hessian(self, u, v, w, n_domain_errors=None, stream=None, binned=True):
+    def eval_hessian(self, u, v, w, n_domain_errors=None, stream=None, binned="auto"):
         """NEXT-4 (mfa_eval_hessian): returns (value [n], grad [3,n], hess [6,n]),
-        hess rows = d2/du2, d2/dv2, d2/dw2, d2/dudv, d2/dudw, d2/dvdw (parameter space)."""
+        hess rows = d2/du2, d2/dv2, d2/dw2, d2/dudv, d2/dudw, d2/dvdw (parameter space).
+        binned: as eval ("auto" = mfa_eval_hessian, False = the unbinned kernel)."""
         import torch
         n = u.numel()
         val = torch.empty(n, device=u.device, dtype=torch.float32)
         grad = torch.empty((3, n), device=u.device, dtype=torch.float32)
         hess = torch.empty((6, n), device=u.device, dtype=torch.float32)
+        if binned == "auto":
+            _check(lib().mfa_eval_hessian(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(grad), _ptr(hess),
+                                          _ptr(n_domain_errors), _stream_ptr(stream)))
+            return val, grad, hess
+        ws, nb = None, 0
         if binned and n >= (1 << 16):
             nb = int(lib().mfa_hessian_workspace_bytes(self._h, n))
             ws = torch.empty(nb, dtype=torch.uint8, device=u.device)
-            _check(lib().mfa_eval_hessian_ws(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(grad),
-                                             _ptr(hess), _ptr(n_domain_errors), _ptr(ws), nb, _stream_ptr(stream)))
-        else:
-            _check(lib().mfa_eval_hessian(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(grad), _ptr(hess),
-                                          _ptr(n_domain_errors), _stream_ptr(stream)))
+        _check(lib().mfa_eval_hessian_ws(self._h, n, _ptr(u), _ptr(v), _ptr(w), _ptr(val), _ptr(grad),
+                                         _ptr(hess), _ptr(n_domain_errors), _ptr(ws), nb, _stream_ptr(stream)))
         return val, grad, hess
 
     # -- Algorithm 1 (mfa_render) ---------------------------------------------
@@ -369,6 +385,60 @@ class Model:
                                      tfh.shape[0], float(v_lo), float(v_hi), C.byref(params_t(params, out_fp16)),
                                      C.c_void_p(out_host.data_ptr()), C.byref(cnt), _stream_ptr(stream)))
         return int(cnt.value)
+
+
+def _render_host_views(self, cams, tf_host: np.ndarray, v_lo, v_hi, params, view_ptrs, out_fp16=False,
+                       stream=None) -> int:
+    """mfa_render_host_views: view v of cams goes to host address view_ptrs[v]
+    ([H,W,4] fp32 or fp16, page-locked).  Returns the composited-sample count."""
+    tfh = np.ascontiguousarray(tf_host, dtype=np.float32)
+    cnt = C.c_ulonglong(0)
+    ptrs = (C.c_void_p * len(cams))(*[int(x) for x in view_ptrs])
+    _check(lib().mfa_render_host_views(self._h, len(cams), cameras_t(cams), C.c_void_p(tfh.ctypes.data),
+                                       tfh.shape[0], float(v_lo), float(v_hi), C.byref(params_t(params, out_fp16)),
+                                       ptrs, C.byref(cnt), _stream_ptr(stream)))
+    return int(cnt.value)
+
+
+Model.render_host_views = _render_host_views
+
+
+class IpcBuffer:
+    """A device buffer allocated by libmfa (mfa_ipc_alloc: cudaMalloc on the
+    current device) together with its CUDA IPC handle, so another process can
+    map it (mfa_ipc_open) -- the multi-GPU direct-store image.  tensor(shape,
+    dtype) views it as a torch tensor (zero copy, __cuda_array_interface__)."""
+
+    def __init__(self, nbytes: int):
+        ptr = C.c_void_p(0)
+        h = C.create_string_buffer(64)
+        _check(lib().mfa_ipc_alloc(int(nbytes), C.byref(ptr), h))
+        self.ptr = ptr.value
+        self.nbytes = int(nbytes)
+        self.handle = h.raw[:64]
+
+    def tensor(self, shape, dtype):
+        import torch
+        typestr = {torch.float32: "<f4", torch.float16: "<f2", torch.uint8: "|u1"}[dtype]
+        buf = self
+
+        class _View:
+            __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (buf.ptr, False),
+                                        "version": 3, "strides": None}
+        t = torch.as_tensor(_View(), device="cuda")
+        t._mfa_owner = self   # keep the allocation alive with the tensor
+        return t
+
+    def close(self):
+        if self.ptr:
+            _check(lib().mfa_ipc_free(C.c_void_p(self.ptr)))
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def unpack_tiles(packed, tiles, n_views, width, height, out=None, stream=None):

@@ -207,6 +207,18 @@ extern "C" size_t mfa_hessian_workspace_bytes(mfa_model h, int64_t n) {
 extern "C" mfa_status mfa_eval_hessian(mfa_model h, int64_t n, const float* u, const float* v, const float* w,
                                        float* value, float* grad, float* hess, unsigned long long* n_domain_errors,
                                        mfa_stream stream) {
+    if (h && n >= ((int64_t)1 << 16) && n < ((int64_t)1 << 31) &&
+        check_device(reinterpret_cast<const Model*>(h)) == MFA_OK) {
+        // the binned path with stream-ordered scratch (no caller workspace)
+        const size_t bytes = hessian_workspace_bytes(reinterpret_cast<const Model*>(h), n);
+        void* ws = scratch_alloc(bytes, (cudaStream_t)stream);
+        if (ws) {
+            const mfa_status s = mfa_eval_hessian_ws(h, n, u, v, w, value, grad, hess, n_domain_errors, ws, bytes,
+                                                     stream);
+            cudaFreeAsync(ws, (cudaStream_t)stream);
+            return s;
+        }
+    }
     return mfa_eval_hessian_ws(h, n, u, v, w, value, grad, hess, n_domain_errors, nullptr, 0, stream);
 }
 

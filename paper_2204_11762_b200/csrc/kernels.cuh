@@ -695,6 +695,28 @@ __device__ __forceinline__ void contract_vg_cached(const float (&nb)[P + 1][P + 
     gu = gvu.y;
 }
 
+// value only, from the (value, derivative) basis pairs of the shaded path,
+// with exactly contract_vg_cached's operation order for the value component
+// (so the value -- and the TF opacity decided from it -- is bit-identical)
+template <int P>
+__device__ __forceinline__ float contract_v_pairs(const float (&nb)[P + 1][P + 1][P + 1], const float2 (&Bu)[P + 1],
+                                                  const float2 (&Bvs)[P + 1], const float2 (&Bw)[P + 1]) {
+    float val = 0.f;
+#pragma unroll
+    for (int c = 0; c <= P; ++c) {
+        float B = 0.f;
+#pragma unroll
+        for (int b = 0; b <= P; ++b) {
+            float a0 = __fmul_rn(Bu[0].x, nb[c][b][0]);
+#pragma unroll
+            for (int a = 1; a <= P; ++a) a0 = fmaf(Bu[a].x, nb[c][b][a], a0);
+            B = fmaf(Bvs[b].y, a0, B);
+        }
+        val = fmaf(Bw[c].x, B, val);
+    }
+    return val;
+}
+
 template <int P>
 __device__ __forceinline__ float contract_v_cached(const float (&nb)[P + 1][P + 1][P + 1], const float (&Nu)[P + 1],
                                                    const float (&Nv)[P + 1], const float (&Nw)[P + 1]) {

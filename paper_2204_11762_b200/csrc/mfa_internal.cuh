@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 
 #include "../../include/mfa.h"
@@ -102,7 +103,43 @@ struct Model {
     AxisTables ax[3];
     void* table_mem = nullptr;   // one allocation for all axis tables
     int64_t device_bytes = 0;
+    int64_t model_bytes = 0;       // the fp32 control grid the caller passed (n_u n_v n_w * 4)
+    double create_ms = 0.0;        // wall time of mfa_model_create (validation, upload, relayout, tables)
+
+    // persistent-kernel work counters: a slot is owned by one launch until
+    // its completion event fires; another launch on the SAME stream may reuse
+    // it (stream order); more than kQueueSlots renders in flight on distinct
+    // streams are refused (acquire_queue_slot)
+    struct QueueSlot {
+        cudaEvent_t done = nullptr;
+        cudaStream_t stream = nullptr;
+        bool used = false;
+        bool pending = false;
+    };
+    mutable std::mutex slot_mu;
+    mutable QueueSlot slots[kQueueSlots];
+
+    // mfa_render_host resources, created on first use and reused (one
+    // host-buffer render at a time per model: host_mu)
+    struct HostRes {
+        cudaStream_t copy = nullptr;
+        cudaEvent_t rendered[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+        void* stage[2] = {nullptr, nullptr};
+        size_t stage_bytes = 0;
+        float* tf = nullptr;           // 1024 x 4 fp32
+        unsigned long long* cnt = nullptr;
+    };
+    mutable std::mutex host_mu;
+    mutable HostRes host;
 };
+
+// queue-slot ownership (render.cu): index of a free slot for a launch on st,
+// or -1 if every slot is held by an unfinished launch on another stream
+int acquire_queue_slot(const Model* m, cudaStream_t st);
+void release_queue_slot(const Model* m, int slot, cudaStream_t st);   // records the completion event
+void free_model_resources(Model* m);                                  // slot events, render_host resources
+void* scratch_alloc(size_t bytes, cudaStream_t st);                   // stream-ordered, default pool (model.cu)
+size_t hessian_workspace_bytes(const Model* m, int64_t n);             // hessian.cu
 
 // Power-basis coefficients of the p+1 non-zero basis functions on knot span
 // i (local t = (u - U_i)/h, u = U_i + h t): P[r][m] = coefficient of t^m of

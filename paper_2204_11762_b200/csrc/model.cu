@@ -15,6 +15,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -333,6 +334,7 @@ mfa_status mfa::validate_knots(int d, int p, int64_t n, const double* U, int* un
 extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t nctrl[3],
                                           const double* const knots[3], const float* ctrl, int32_t ctrl_on_device,
                                           const mfa_model_options* opt, mfa_stream stream, mfa_model* out) {
+    const auto t_create = std::chrono::steady_clock::now();
     if (!out) return fail(MFA_ERR_INVALID_ARG, "out is NULL");
     const int want_layout = opt ? opt->layout : MFA_LAYOUT_AUTO;
     if (want_layout < MFA_LAYOUT_AUTO || want_layout > MFA_LAYOUT_BEZIER)
@@ -549,6 +551,8 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
         return cleanup(fail(MFA_ERR_DOMAIN, std::to_string(hmm[2]) + " non-finite control values"));
     m->vmin = ord2f(hmm[0]);
     m->vmax = ord2f(hmm[1]);
+    m->model_bytes = npts * (int64_t)sizeof(float);
+    m->create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create).count();
     cleanup(MFA_OK);
     *out = reinterpret_cast<mfa_model>(m);
     return MFA_OK;
@@ -573,6 +577,8 @@ extern "C" mfa_status mfa_model_info(mfa_model h, mfa_model_desc* out) {
     out->device_bytes = m->device_bytes;
     out->device = m->device;
     out->layout = m->layout == kBezier ? MFA_LAYOUT_BEZIER : MFA_LAYOUT_QUADS;
+    out->model_bytes = m->model_bytes;
+    out->create_ms = m->create_ms;
     return MFA_OK;
 }
 
@@ -582,6 +588,7 @@ extern "C" mfa_status mfa_model_destroy(mfa_model h) {
     int cur = -1;
     cudaGetDevice(&cur);
     if (cur != m->device) cudaSetDevice(m->device);
+    free_model_resources(m);
     if (m->Q) cudaFree(m->Q);
     if (m->queue) cudaFree(m->queue);
     if (m->table_mem) cudaFree(m->table_mem);
@@ -602,7 +609,48 @@ extern "C" mfa_status mfa_eval_batch(mfa_model h, int64_t n, const float* u, con
     const Model* m = reinterpret_cast<const Model*>(h);
     mfa_status s = check_device(m);
     if (s != MFA_OK) return s;
-    return launch_eval(m, n, u, v, w, value, du, dv, dw, n_domain_errors, (cudaStream_t)stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n >= ((int64_t)1 << 16) && n < ((int64_t)1 << 31)) {
+        // the binned path with stream-ordered scratch (no caller workspace)
+        const size_t bytes = eval_workspace_bytes(m, n);
+        void* ws = scratch_alloc(bytes, st);
+        if (ws) {
+            s = launch_eval(m, n, u, v, w, value, du, dv, dw, n_domain_errors, st, ws, bytes);
+            cudaFreeAsync(ws, st);
+            return s;
+        }
+    }
+    return launch_eval(m, n, u, v, w, value, du, dv, dw, n_domain_errors, st);
+}
+
+// Stream-ordered scratch for the calls without a caller workspace
+// (mfa_eval_batch, mfa_eval_hessian): cudaMallocAsync from the device's
+// default memory pool, whose release threshold is raised once per device so
+// freed blocks stay cached for the next call (no cudaMalloc / sync on the
+// hot path).  NULL if the pool cannot serve it (the caller then runs the
+// unbinned kernels).
+void* mfa::scratch_alloc(size_t bytes, cudaStream_t st) {
+    static std::mutex mu;
+    static uint64_t warmed = 0;   // bit per device ordinal < 64
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev < 64 && !(warmed >> dev & 1)) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            warmed |= (uint64_t)1 << dev;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
 }
 
 extern "C" size_t mfa_eval_workspace_bytes(mfa_model h, int64_t n) {
@@ -729,6 +777,31 @@ extern "C" mfa_status mfa_ipc_open(const void* handle, void** base_out) {
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
 }
 
+extern "C" mfa_status mfa_ipc_alloc(size_t bytes, void** ptr_out, void* handle_out) {
+    if (!ptr_out || !handle_out || bytes == 0) return fail(MFA_ERR_INVALID_ARG, "mfa_ipc_alloc: NULL output or 0 bytes");
+    *ptr_out = nullptr;
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MFA_ERR_OOM, std::string("mfa_ipc_alloc: cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    cudaIpcMemHandle_t h;
+    if ((e = cudaIpcGetMemHandle(&h, p)) != cudaSuccess) {
+        cudaFree(p);
+        return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    std::memcpy(handle_out, &h, sizeof h);
+    *ptr_out = p;
+    return MFA_OK;
+}
+
+extern "C" mfa_status mfa_ipc_free(void* ptr) {
+    if (!ptr) return fail(MFA_ERR_INVALID_ARG, "mfa_ipc_free: NULL");
+    const cudaError_t e = cudaFree(ptr);
+    return e == cudaSuccess ? MFA_OK : cuda_fail(e, "cudaFree");
+}
+
 extern "C" mfa_status mfa_ipc_close(void* base) {
     if (!base) return fail(MFA_ERR_INVALID_ARG, "mfa_ipc_close: NULL base");
     const cudaError_t e = cudaIpcCloseMemHandle(base);
@@ -747,68 +820,99 @@ extern "C" mfa_status mfa_unpack_tiles(const void* packed, int32_t in_fp16, cons
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "unpack_tiles launch");
 }
 
-extern "C" mfa_status mfa_render_host(mfa_model h, int32_t n_views, const mfa_camera* cams, const float* tf_rgba_host,
-                                      int32_t tf_n_entries, float v_lo, float v_hi, const mfa_render_params* prm,
-                                      void* rgba_host, unsigned long long* samples_host, mfa_stream stream) {
+// mfa_render_host / mfa_render_host_views: per view, render into one of two
+// model-owned staging buffers on the caller's stream while the copy stream
+// moves the previous view to the host (D2H of view v overlaps the render of
+// view v+1).  The staging buffers, events, copy stream, TF and counter are
+// created on first use and reused (Model::host, one host-buffer render per
+// model at a time).
+static mfa_status render_host_impl(const Model* m, int32_t n_views, const mfa_camera* cams, const float* tf_rgba_host,
+                                   int32_t tf_n_entries, float v_lo, float v_hi, const mfa_render_params* prm,
+                                   void* const* dst, unsigned long long* samples_host, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(m->host_mu);
+    Model::HostRes& H = m->host;
+    const size_t px = (size_t)cams[0].width * cams[0].height;
+    const size_t view_bytes = px * (prm->out_fp16 ? 8 : 16);
+    cudaError_t e;
+    if (!H.copy) {
+        if ((e = cudaStreamCreateWithFlags(&H.copy, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+        for (int i = 0; i < 2; ++i) {
+            if ((e = cudaEventCreateWithFlags(&H.rendered[i], cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&H.copied[i], cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "event");
+        }
+        if ((e = cudaMalloc((void**)&H.tf, sizeof(float) * 4 * 1024)) != cudaSuccess) return cuda_fail(e, "tf");
+        if ((e = cudaMalloc((void**)&H.cnt, sizeof(unsigned long long))) != cudaSuccess) return cuda_fail(e, "count");
+    }
+    if (H.stage_bytes < view_bytes) {
+        cudaStreamSynchronize(H.copy);
+        for (int i = 0; i < 2; ++i) {
+            if (H.stage[i]) cudaFree(H.stage[i]);
+            H.stage[i] = nullptr;
+        }
+        H.stage_bytes = 0;
+        for (int i = 0; i < 2; ++i)
+            if ((e = cudaMalloc(&H.stage[i], view_bytes)) != cudaSuccess) return cuda_fail(e, "staging");
+        H.stage_bytes = view_bytes;
+    }
+    // the previous call's copies are complete (it synchronised); order this
+    // call's uploads after the caller's earlier work on st
+    cudaMemcpyAsync(H.tf, tf_rgba_host, sizeof(float) * 4 * tf_n_entries, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(H.cnt, 0, sizeof(unsigned long long), st);
+    mfa_tf tf{H.tf, tf_n_entries, v_lo, v_hi};
+    mfa_status s = MFA_OK;
+    for (int v = 0; v < n_views; ++v) {
+        const int b = v & 1;
+        if (v >= 2) cudaStreamWaitEvent(st, H.copied[b], 0);  // staging buffer b free again
+        s = launch_render(m, 1, cams + v, &tf, prm, nullptr, H.stage[b], H.cnt, st);
+        if (s != MFA_OK) break;
+        cudaEventRecord(H.rendered[b], st);
+        cudaStreamWaitEvent(H.copy, H.rendered[b], 0);
+        cudaMemcpyAsync(dst[v], H.stage[b], view_bytes, cudaMemcpyDeviceToHost, H.copy);
+        cudaEventRecord(H.copied[b], H.copy);
+    }
+    if (s == MFA_OK && samples_host) {
+        cudaStreamWaitEvent(st, H.copied[(n_views - 1) & 1], 0);
+        cudaMemcpyAsync(samples_host, H.cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+    }
+    cudaStreamSynchronize(H.copy);
+    cudaStreamSynchronize(st);
+    if (s == MFA_OK && (e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "render_host");
+    return s;
+}
+
+static mfa_status render_host_check(mfa_model h, int32_t n_views, const mfa_camera* cams, const float* tf_rgba_host,
+                                    int32_t tf_n_entries, float v_lo, float v_hi, const mfa_render_params* prm,
+                                    const void* dst) {
     if (!h) return fail(MFA_ERR_INVALID_ARG, "model is NULL");
     const Model* m = reinterpret_cast<const Model*>(h);
     mfa_status s = validate_render(m, n_views, cams, prm);
     if (s != MFA_OK) return s;
-    if (!tf_rgba_host || tf_n_entries < 2 || tf_n_entries > 1024 || !(v_hi > v_lo) || !rgba_host)
+    if (!tf_rgba_host || tf_n_entries < 2 || tf_n_entries > 1024 || !(v_hi > v_lo) || !dst)
         return fail(MFA_ERR_INVALID_ARG, "tf / rgba_host");
-    if ((s = check_device(m)) != MFA_OK) return s;
-    cudaStream_t st = (cudaStream_t)stream;
-    const size_t px = (size_t)cams[0].width * cams[0].height;
-    const size_t view_bytes = px * (prm->out_fp16 ? 8 : 16);
-    cudaStream_t cs = nullptr;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    void* stage[2] = {nullptr, nullptr};
-    float* dtf = nullptr;
-    unsigned long long* dcnt = nullptr;
-    cudaError_t e;
-    auto done = [&](mfa_status r) {
-        if (cs) cudaStreamSynchronize(cs);
-        cudaStreamSynchronize(st);
-        for (int i = 0; i < 2; ++i) {
-            if (stage[i]) cudaFreeAsync(stage[i], st);
-            if (ev[i]) cudaEventDestroy(ev[i]);
-        }
-        if (dtf) cudaFreeAsync(dtf, st);
-        if (dcnt) cudaFreeAsync(dcnt, st);
-        cudaStreamSynchronize(st);
-        if (cs) cudaStreamDestroy(cs);
-        return r;
-    };
-    if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess) return done(cuda_fail(e, "stream"));
-    for (int i = 0; i < 2; ++i) {
-        if ((e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming)) != cudaSuccess) return done(cuda_fail(e, "event"));
-        if ((e = cudaMallocAsync(&stage[i], view_bytes, st)) != cudaSuccess) return done(cuda_fail(e, "staging"));
-    }
-    if ((e = cudaMallocAsync((void**)&dtf, sizeof(float) * 4 * tf_n_entries, st)) != cudaSuccess) return done(cuda_fail(e, "tf"));
-    if ((e = cudaMallocAsync((void**)&dcnt, sizeof(unsigned long long), st)) != cudaSuccess) return done(cuda_fail(e, "count"));
-    cudaMemcpyAsync(dtf, tf_rgba_host, sizeof(float) * 4 * tf_n_entries, cudaMemcpyHostToDevice, st);
-    cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long), st);
-    mfa_tf tf{dtf, tf_n_entries, v_lo, v_hi};
-    cudaEvent_t copied[2] = {nullptr, nullptr};
-    for (int i = 0; i < 2; ++i)
-        if ((e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming)) != cudaSuccess) return done(cuda_fail(e, "event"));
-    for (int v = 0; v < n_views; ++v) {
-        const int b = v & 1;
-        if (v >= 2) cudaStreamWaitEvent(st, copied[b], 0);  // staging buffer b free again
-        s = launch_render(m, 1, cams + v, &tf, prm, nullptr, stage[b], dcnt, st);
-        if (s != MFA_OK) break;
-        cudaEventRecord(ev[b], st);
-        cudaStreamWaitEvent(cs, ev[b], 0);
-        cudaMemcpyAsync((char*)rgba_host + v * view_bytes, stage[b], view_bytes, cudaMemcpyDeviceToHost, cs);
-        cudaEventRecord(copied[b], cs);
-    }
-    if (s == MFA_OK && samples_host) {
-        cudaStreamWaitEvent(st, copied[(n_views - 1) & 1], 0);
-        cudaMemcpyAsync(samples_host, dcnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
-    }
-    mfa_status r = done(s);
-    for (int i = 0; i < 2; ++i)
-        if (copied[i]) cudaEventDestroy(copied[i]);
-    if (r == MFA_OK && (e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "render_host");
-    return r;
+    return check_device(m);
+}
+
+extern "C" mfa_status mfa_render_host(mfa_model h, int32_t n_views, const mfa_camera* cams, const float* tf_rgba_host,
+                                      int32_t tf_n_entries, float v_lo, float v_hi, const mfa_render_params* prm,
+                                      void* rgba_host, unsigned long long* samples_host, mfa_stream stream) {
+    mfa_status s = render_host_check(h, n_views, cams, tf_rgba_host, tf_n_entries, v_lo, v_hi, prm, rgba_host);
+    if (s != MFA_OK) return s;
+    const size_t view_bytes = (size_t)cams[0].width * cams[0].height * (prm->out_fp16 ? 8 : 16);
+    std::vector<void*> dst((size_t)n_views);
+    for (int v = 0; v < n_views; ++v) dst[v] = (char*)rgba_host + v * view_bytes;
+    return render_host_impl(reinterpret_cast<const Model*>(h), n_views, cams, tf_rgba_host, tf_n_entries, v_lo, v_hi,
+                            prm, dst.data(), samples_host, (cudaStream_t)stream);
+}
+
+extern "C" mfa_status mfa_render_host_views(mfa_model h, int32_t n_views, const mfa_camera* cams,
+                                            const float* tf_rgba_host, int32_t tf_n_entries, float v_lo, float v_hi,
+                                            const mfa_render_params* prm, void* const* rgba_host_views,
+                                            unsigned long long* samples_host, mfa_stream stream) {
+    mfa_status s = render_host_check(h, n_views, cams, tf_rgba_host, tf_n_entries, v_lo, v_hi, prm, rgba_host_views);
+    if (s != MFA_OK) return s;
+    for (int v = 0; v < n_views; ++v)
+        if (!rgba_host_views[v]) return fail(MFA_ERR_INVALID_ARG, "rgba_host_views[" + std::to_string(v) + "] is NULL");
+    return render_host_impl(reinterpret_cast<const Model*>(h), n_views, cams, tf_rgba_host, tf_n_entries, v_lo, v_hi,
+                            prm, rgba_host_views, samples_host, (cudaStream_t)stream);
 }

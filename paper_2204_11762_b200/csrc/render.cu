@@ -4,15 +4,57 @@
 #include <math.h>
 
 #include <algorithm>
-#include <atomic>
 
 #include "render_kernel.cuh"
 
 namespace mfa {
 
-static std::atomic<unsigned> g_slot{0};
+int acquire_queue_slot(const Model* m, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(m->slot_mu);
+    int pick = -1, fresh = -1, done = -1;
+    for (int i = 0; i < kQueueSlots && pick < 0; ++i) {
+        const Model::QueueSlot& q = m->slots[i];
+        if (q.pending) continue;                            // being launched by another thread
+        if (q.used && q.stream == st) pick = i;             // stream-ordered after its last user
+        else if (!q.used) { if (fresh < 0) fresh = i; }
+        else if (done < 0 && cudaEventQuery(q.done) == cudaSuccess) done = i;
+    }
+    if (pick < 0) pick = fresh >= 0 ? fresh : done;
+    if (pick < 0) {
+        cudaGetLastError();   // clear cudaErrorNotReady left by the queries
+        return -1;
+    }
+    m->slots[pick].pending = true;
+    return pick;
+}
 
-cudaError_t dispatch_render_main(const RenderArgs& a, int p, int layout, bool uni, bool shade, cudaStream_t st) {
+void release_queue_slot(const Model* m, int slot, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(m->slot_mu);
+    Model::QueueSlot& q = m->slots[slot];
+    if (!q.done) cudaEventCreateWithFlags(&q.done, cudaEventDisableTiming);
+    cudaEventRecord(q.done, st);
+    q.stream = st;
+    q.used = true;
+    q.pending = false;
+}
+
+void free_model_resources(Model* m) {
+    for (int i = 0; i < kQueueSlots; ++i)
+        if (m->slots[i].done) cudaEventDestroy(m->slots[i].done);
+    Model::HostRes& h = m->host;
+    if (h.copy) cudaStreamSynchronize(h.copy);
+    for (int i = 0; i < 2; ++i) {
+        if (h.stage[i]) cudaFree(h.stage[i]);
+        if (h.rendered[i]) cudaEventDestroy(h.rendered[i]);
+        if (h.copied[i]) cudaEventDestroy(h.copied[i]);
+    }
+    if (h.tf) cudaFree(h.tf);
+    if (h.cnt) cudaFree(h.cnt);
+    if (h.copy) cudaStreamDestroy(h.copy);
+    h = Model::HostRes{};
+}
+
+cudaError_t dispatch_render_main(const RenderArgs& a, int p, int layout, bool uni, int shade, cudaStream_t st) {
     switch (p) {
         case 1: return dispatch_render<1, false>(a, layout, uni, shade, st);
         case 2: return dispatch_render<2, false>(a, layout, uni, shade, st);
@@ -106,16 +148,24 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->out = out;
     a->out_fp16 = prm->out_fp16;
     a->samples = samples;
-    const bool shade = prm->shading != 0;
+    const int shade = prm->shading == 2 ? 2 : (prm->shading != 0);   // 2: NEXT-1 skip variant
     cudaError_t e = cudaSuccess;
+    bool exhausted = false;
     auto run = [&]() -> cudaError_t {
         if (a->n_units == 0) return cudaSuccess;
         if (a->n_units >= (int64_t)0xffffffffu) return cudaErrorInvalidValue;
-        a->queue = m->queue + (g_slot.fetch_add(1) % kQueueSlots);
+        const int slot = acquire_queue_slot(m, st);
+        if (slot < 0) {   // every work counter is held by an unfinished launch on another stream
+            exhausted = true;
+            return cudaErrorNotReady;
+        }
+        a->queue = m->queue + slot;
         cudaError_t r = cudaMemsetAsync(a->queue, 0, sizeof(unsigned int), st);
         if (r != cudaSuccess) return r;
-        return (field || lights || curv) ? dispatch_render_ext(*a, m->p, m->layout, uni, shade, st)
-                     : dispatch_render_main(*a, m->p, m->layout, uni, shade, st);
+        r = (field || lights || curv) ? dispatch_render_ext(*a, m->p, m->layout, uni, shade, st)
+                                      : dispatch_render_main(*a, m->p, m->layout, uni, shade, st);
+        release_queue_slot(m, slot, st);
+        return r;
     };
     if (tiles) {
         if (n_views > kMaxViewsPerLaunch) {
@@ -144,6 +194,8 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         }
     }
     delete a;
+    if (exhausted)
+        return fail(MFA_ERR_UNSUPPORTED, "render: more than 256 renders in flight on distinct streams for one model");
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "render launch");
 }
 

@@ -32,6 +32,12 @@
 #ifndef MFA_UNIT_SHAPE   // lanes of a warp unit: 0 = 8x4 pixels, 1 = 4x8 (C5 +0.8 %, C4 +3 %), 2 = 16x2, 3 = 2x16
 #define MFA_UNIT_SHAPE 1
 #endif
+#ifndef MFA_VIEW_GROUP   // full-frame work order: >1 interleaves groups of orbit-adjacent views
+#define MFA_VIEW_GROUP 1
+#endif
+#ifndef MFA_VIEW_ORDER   // with MFA_VIEW_GROUP > 1: 1 = per supertile, 2 = per supertile row, 3 = per tile
+#define MFA_VIEW_ORDER 1
+#endif
 #ifndef MFA_FLAT_LOOP
 #define MFA_FLAT_LOOP 1
 #endif
@@ -233,7 +239,11 @@ struct RenderShape {
     static constexpr bool CTA_TILES = MFA_CTA_TILES < 0 ? (P >= 4 && THREADS == 256) : (bool)MFA_CTA_TILES;
 };
 
-template <int P, int LAYOUT, bool UNI, bool SHADE, bool EXT>
+// SHADE: 0 = ShadingOn false (value only, Alg. 1 l.8), 1 = the ★ path (value
+// + gradient for every sample, R-20), 2 = NEXT-1's measured variant: the
+// gradient contraction and Phong are skipped for a sample whose TF opacity is
+// 0 (it composites with weight 0, so the image is bit-identical to SHADE = 1)
+template <int P, int LAYOUT, bool UNI, int SHADE, bool EXT>
 __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P, LAYOUT>::MINB)
     render_kernel(const __grid_constant__ RenderArgs args) {
     constexpr bool BEZ = LAYOUT == kBezier;
@@ -293,9 +303,40 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             // supertile order: the ~200 tiles in flight form a compact image
             // region, so neighbouring rays reuse control blocks from L1/L2
             const unsigned tid32 = (unsigned)tile_id;   // < 2^29 (n_units < 2^32)
+#if MFA_VIEW_GROUP > 1
+            // cross-view order: groups of MFA_VIEW_GROUP consecutive (orbit-
+            // adjacent) views; inside a group the same supertile (ORDER 1) or
+            // supertile row (ORDER 2) of every view is issued back to back
+            unsigned st, lt;
+            {
+                constexpr unsigned G = MFA_VIEW_GROUP;
+                const unsigned grp = tid32 / ((unsigned)per_view * G);
+                const unsigned r = tid32 - grp * (unsigned)per_view * G;
+                const unsigned gv = min(G, (unsigned)args.n_views - grp * G);   // views in this group
+#if MFA_VIEW_ORDER == 2
+                const unsigned row = (unsigned)args.st_x * kST2;                 // tiles per supertile row
+                const unsigned rr = r / (row * gv), rem = r - rr * row * gv;
+                const unsigned vin = rem / row, q = rem - vin * row;
+                st = rr * (unsigned)args.st_x + q / kST2;
+                lt = q % kST2;
+#elif MFA_VIEW_ORDER == 3   // per tile: tile (st, lt) of every view of the group back to back
+                st = r / (kST2 * gv);
+                const unsigned rem = r - st * kST2 * gv;
+                lt = rem / gv;
+                const unsigned vin = rem - lt * gv;
+#else
+                st = r / (kST2 * gv);
+                const unsigned rem = r - st * kST2 * gv;
+                const unsigned vin = rem / kST2;
+                lt = rem - vin * kST2;
+#endif
+                view = (int)(grp * G + vin);
+            }
+#else
             view = (int)(tid32 / (unsigned)per_view);
             const unsigned t = tid32 - (unsigned)view * (unsigned)per_view;
             const unsigned st = t / kST2, lt = t % kST2;
+#endif
             const unsigned sty = st / (unsigned)args.st_x;
             tx = (int)((st - sty * (unsigned)args.st_x) * kST + lt % kST);
             ty = (int)(sty * kST + lt / kST);
@@ -447,6 +488,25 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 }
             }
         };
+        // a8 lookup position: f = s (n - 1) clamped, i0 = round(f - 1/2) via the
+        // 2^23 magic number (no F2I; any i0 in {floor(f), f - 1 at integers}
+        // gives the same lerp), weight wt (shared by shade_composite and the
+        // SHADE == 2 opacity test, so both see the same alpha)
+        auto tf_pos = [&](float v, int& i0, float& wt) {
+            float f = (v - args.v_lo) * args.s_scale;
+            f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
+            const float fm = f + 8388607.5f;
+            i0 = __float_as_int(fm) - 0x4b000000;
+            i0 = min(max(i0, 0), args.tf_n - 2);
+            wt = f - (float)i0;
+        };
+        auto tf_alpha = [&](float v) {
+            int i0;
+            float wt;
+            tf_pos(v, i0, wt);
+            const float a0 = s_tf[i0].w, a1 = s_tf[i0 + 1].w;
+            return fmaf(wt, a1 - a0, a0);
+        };
         // a5 + a7: value and t-space gradient of the sample (after fetch)
         auto query = [&](const int (&s)[3], const float (&t)[3], float& val, float& gu, float& gv, float& gw) {
             gu = gv = gw = 0.f;
@@ -475,7 +535,12 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                     bernstein<P, false>(t[0], Bu);
                     bernstein<P, true>(t[1], Bv);
                     bernstein<P, false>(t[2], Bw);
-                    contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                    if constexpr (SHADE == 2) {   // value first; the gradient only where the TF is not transparent
+                        val = contract_v_pairs<P>(nb, Bu, Bv, Bw);
+                        if (tf_alpha(val) > 0.f) contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                    } else {
+                        contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                    }
                 } else {
                     float Nu[P + 1], Nv[P + 1], Nw[P + 1];
                     bernstein_value<P>(t[0], Nu);
@@ -489,7 +554,12 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                     axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
                     axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
                     axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
-                    contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                    if constexpr (SHADE == 2) {
+                        val = contract_v_pairs<P>(nb, Bu, Bv, Bw);
+                        if (tf_alpha(val) > 0.f) contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                    } else {
+                        contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                    }
                 } else {
                     float Nu[P + 1], Nv[P + 1], Nw[P + 1];
                     axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
@@ -524,14 +594,9 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         auto shade_composite = [&](float val, float gu, float gv, float gw, const float (&gs)[3], float k1,
                                    float k2) {
             // a8: transfer function (l.7)
-            float f = (val - args.v_lo) * args.s_scale;
-            f = fminf(fmaxf(f, 0.f), (float)(args.tf_n - 1));
-            // i0 = round(f - 1/2) via the 2^23 magic number (no F2I): any
-            // i0 in {floor(f), f - 1 at integers} gives the same lerp
-            const float fm = f + 8388607.5f;
-            int i0 = __float_as_int(fm) - 0x4b000000;
-            i0 = min(max(i0, 0), args.tf_n - 2);
-            const float wt = f - (float)i0;
+            int i0;
+            float wt;
+            tf_pos(val, i0, wt);
             MFA_DCHECK(i0 >= 0 && i0 + 1 < args.tf_n);
             const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
             float cr = fmaf(wt, T1.x - T0.x, T0.x);
@@ -795,7 +860,7 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
     }
 }
 
-template <int P, int LAYOUT, bool UNI, bool SHADE, bool EXT>
+template <int P, int LAYOUT, bool UNI, int SHADE, bool EXT>
 static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(float4) * a.tf_n;
     auto kern = render_kernel<P, LAYOUT, UNI, SHADE, EXT>;
@@ -829,16 +894,23 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
 }
 
 template <int P, int LAYOUT, bool EXT>
-static cudaError_t dispatch_render_l(const RenderArgs& a, bool uni, bool shade, cudaStream_t st) {
-    if (uni)
-        return shade ? launch_render_t<P, LAYOUT, true, true, EXT>(a, st)
-                     : launch_render_t<P, LAYOUT, true, false, EXT>(a, st);
-    return shade ? launch_render_t<P, LAYOUT, false, true, EXT>(a, st)
-                 : launch_render_t<P, LAYOUT, false, false, EXT>(a, st);
+static cudaError_t dispatch_render_l(const RenderArgs& a, bool uni, int shade, cudaStream_t st) {
+    constexpr bool kSkip = !EXT && RenderShape<P, LAYOUT>::CACHE;   // SHADE = 2 is built for the hot path only
+    if (shade == 2 && !kSkip) shade = 1;
+    if (uni) {
+        if (shade == 0) return launch_render_t<P, LAYOUT, true, 0, EXT>(a, st);
+        if constexpr (kSkip)
+            if (shade == 2) return launch_render_t<P, LAYOUT, true, 2, EXT>(a, st);
+        return launch_render_t<P, LAYOUT, true, 1, EXT>(a, st);
+    }
+    if (shade == 0) return launch_render_t<P, LAYOUT, false, 0, EXT>(a, st);
+    if constexpr (kSkip)
+        if (shade == 2) return launch_render_t<P, LAYOUT, false, 2, EXT>(a, st);
+    return launch_render_t<P, LAYOUT, false, 1, EXT>(a, st);
 }
 
 template <int P, bool EXT>
-static cudaError_t dispatch_render(const RenderArgs& a, int layout, bool uni, bool shade, cudaStream_t st) {
+static cudaError_t dispatch_render(const RenderArgs& a, int layout, bool uni, int shade, cudaStream_t st) {
     if constexpr (P <= 3) {
         if (layout == kBezier) return dispatch_render_l<P, kBezier, EXT>(a, uni, shade, st);
     }
@@ -846,7 +918,7 @@ static cudaError_t dispatch_render(const RenderArgs& a, int layout, bool uni, bo
 }
 
 // defined in render.cu (the hot path) and truth.cu (analytic field, several lights)
-cudaError_t dispatch_render_main(const RenderArgs& a, int p, int layout, bool uni, bool shade, cudaStream_t st);
-cudaError_t dispatch_render_ext(const RenderArgs& a, int p, int layout, bool uni, bool shade, cudaStream_t st);
+cudaError_t dispatch_render_main(const RenderArgs& a, int p, int layout, bool uni, int shade, cudaStream_t st);
+cudaError_t dispatch_render_ext(const RenderArgs& a, int p, int layout, bool uni, int shade, cudaStream_t st);
 
 }  // namespace mfa

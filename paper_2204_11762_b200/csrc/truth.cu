@@ -11,7 +11,7 @@
 
 namespace mfa {
 
-cudaError_t dispatch_render_ext(const RenderArgs& a, int p, int layout, bool uni, bool shade, cudaStream_t st) {
+cudaError_t dispatch_render_ext(const RenderArgs& a, int p, int layout, bool uni, int shade, cudaStream_t st) {
     switch (p) {
         case 1: return dispatch_render<1, true>(a, layout, uni, shade, st);
         case 2: return dispatch_render<2, true>(a, layout, uni, shade, st);

@@ -15,9 +15,10 @@ import torch.multiprocessing as mp
 from paper_2204_11762_b200 import dist as D
 
 
-def test_assign_units_cover_and_balance():
-    for V, W, H, G in [(1, 64, 64, 1), (3, 100, 75, 2), (64, 3840, 2160, 8), (2, 17, 33, 4)]:
-        lists = D.assign_units(V, W, H, G)
+@pytest.mark.parametrize("mode", ["auto", "views", "rows", "diagonal"])
+def test_assign_units_cover_and_balance(mode):
+    for V, W, H, G in [(1, 64, 64, 1), (3, 100, 75, 2), (16, 480, 270, 8), (2, 17, 33, 4), (1, 2048, 2048, 8)]:
+        lists = D.assign_units(V, W, H, G, mode)
         assert len(lists) == G and len({len(x) for x in lists}) == 1
         allu = np.concatenate(lists)
         real = allu[allu[:, 0] >= 0]
@@ -26,7 +27,34 @@ def test_assign_units_cover_and_balance():
         keys = {tuple(r) for r in real}
         assert len(keys) == len(real)                      # no duplicates
         counts = [int((x[:, 0] >= 0).sum()) for x in lists]
-        assert max(counts) - min(counts) <= 1              # balanced
+        m = D.pick_mode(V, G) if mode == "auto" else mode
+        if m == "diagonal":
+            assert max(counts) - min(counts) <= 1          # balanced to one tile
+        elif m == "views":
+            per_view = tx * ty
+            assert max(counts) - min(counts) <= per_view   # balanced to one view
+            for r, x in enumerate(lists):                  # rank r owns views r, r+G, ...
+                assert set(x[x[:, 0] >= 0][:, 0].tolist()) <= set(range(r, V, G))
+        else:
+            band = V * tx * D.SUPERTILE                     # one supertile row of every view
+            assert max(counts) - min(counts) <= band
+
+
+def test_rank_lists_keep_the_single_gpu_order():
+    """Each rank's list is a subsequence of the 1-GPU supertile order, so a
+    rank's kernel visits neighbouring tiles back to back (the locality the
+    render kernel depends on)."""
+    V, W, H = 3, 200, 120
+    full = D.supertile_order(range(V), W, H)
+    pos = {tuple(u): i for i, u in enumerate(full)}
+    assert len(pos) == len(full) == V * np.prod(D.tile_grid(W, H))
+    for mode in ("views", "rows"):
+        for x in D.assign_units(V, W, H, 2, mode, pad=False):
+            idx = [pos[tuple(u)] for u in x]
+            assert idx == sorted(idx)
+    # the supertile order itself: 2x2 tiles, row-major inside, supertiles row-major
+    o = D.supertile_order([0], 64, 48).tolist()
+    assert o[:8] == [[0, 0, 0], [0, 1, 0], [0, 0, 1], [0, 1, 1], [0, 2, 0], [0, 3, 0], [0, 2, 1], [0, 3, 1]]
 
 
 def _fake_render(tiles):
@@ -95,13 +123,44 @@ def test_render_sharded_gloo_world2(V, W, H):
         np.testing.assert_array_equal(img[v, :, :, 3], 1.0)
 
 
-def test_ipc_handle_bytes():
-    """torch's shareable handle -> the raw 64-byte cudaIpcMemHandle_t."""
-    import pytest
-    raw = bytes(range(64))
-    assert D.ipc_handle_bytes(raw) == raw
-    assert D.ipc_handle_bytes(b"\x01c" + raw) == raw
-    with pytest.raises(RuntimeError):
-        D.ipc_handle_bytes(b"\x01e" + raw)
-    with pytest.raises(RuntimeError):
-        D.ipc_handle_bytes(raw[:10])
+def _view_worker(rank, world, port, V, H, W, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    img0 = torch.full((V, H, W, 4), -1.0) if rank == 0 else None
+    bufs = [torch.empty((H, W, 4)) for _ in range(2)] if rank else None
+    rendered = []
+
+    def render_view(v, out):
+        assert v % world == rank                       # only this rank's views
+        out.copy_(torch.arange(H * W * 4, dtype=torch.float32).view(H, W, 4) + 1000.0 * v)
+        rendered.append(v)
+
+    for _ in range(2):                                  # two steps reuse the buffers
+        for wk in D.gather_views_nccl(render_view, img0, V, rank, world, bufs=bufs):
+            wk.wait()
+    assert rendered == D.rank_views(V, world, rank) * 2
+    if rank == 0:
+        q.put(img0.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("V", [5, 2])
+def test_gather_views_world2(V):
+    """The per-view gather schedule (dist.gather_views_nccl; NCCL on GPUs,
+    gloo here): every view arrives in rank 0's image slot; the sender's two
+    buffers are reused only after their sends completed."""
+    H, W = 6, 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_view_worker, args=(r, 2, port, V, H, W, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    img = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    base = np.arange(H * W * 4, dtype=np.float32).reshape(H, W, 4)
+    for v in range(V):
+        np.testing.assert_array_equal(img[v], base + 1000.0 * v)

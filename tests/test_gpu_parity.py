@@ -40,7 +40,7 @@ def gpu_eval(m, u, v, w, grad=True):
     return np.stack([o.cpu().numpy() for o in outs], axis=1)
 
 
-EVAL_N = {1: 1 << 16, 2: 1 << 18, 3: 1 << 24, 4: 1 << 16, 5: 1 << 19}
+EVAL_N = {1: 1 << 20, 2: 1 << 20, 3: 1 << 24, 4: 1 << 20, 5: 1 << 20}   # SURVEY §8(c) acceptance sizes
 
 
 @pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
@@ -60,22 +60,24 @@ def test_eval_parity(c):
 
 @pytest.mark.parametrize("c,layout", [(3, "auto"), (5, "auto"), (5, "quads"), (2, "auto")])
 def test_eval_binned_equals_direct(c, layout):
-    """mfa_eval_batch_ws (spatially binned order) returns exactly the outputs
-    of mfa_eval_batch, including NaN rows and the domain-error count for
-    points outside [0,1]^3."""
+    """The three eval paths return identical outputs, NaN rows and domain-error
+    counts: mfa_eval_batch (binned, stream-ordered scratch), mfa_eval_batch_ws
+    with a caller workspace (binned) and without one (the unbinned kernel)."""
     m = gpu_model(c, layout)
     u, v, w = WL.query_points(c, 1 << 18)
     u = u.copy()
     u[[5, 77, 1000]] = [1.5, np.nan, -0.25]
     cu, cv, cw = cuda(u), cuda(v), cuda(w)
     outs = []
-    for binned in (True, False):
+    for binned in ("auto", True, False):
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         r = m.eval(cu, cv, cw, n_domain_errors=cnt, binned=binned)
         torch.cuda.synchronize()
         outs.append((np.stack([t.cpu().numpy() for t in r], axis=1), int(cnt.item())))
-    np.testing.assert_array_equal(outs[0][0], outs[1][0])
-    assert outs[0][1] == outs[1][1] == 3
+    for o in outs[1:]:
+        np.testing.assert_array_equal(outs[0][0], o[0])
+        assert o[1] == 3
+    assert outs[0][1] == 3
 
 
 def test_eval_value_only_matches():
@@ -133,10 +135,24 @@ def test_render_subset_parity_full_size(c, views, frac):
     img, ns = render_gpu(c)
     H, W = w.cameras[0].height, w.cameras[0].width
     sub = WL.tile_subset(c, W, H, frac, views=views)
+    tiles, ref_count, window = [], 0, 0
     for v, pix in sub.items():
         ref = O.render(oracle_model(c), w.cameras[v], w.tf, w.v_lo, w.v_hi, w.params, pixels=pix)
         st = parity.check_image(img[v].reshape(-1, 4)[pix], ref, f"C{c} view {v}")
         print(f"C{c} view {v}: {st}")
+        ref_count += int(ref["count"].sum())
+        window += parity.count_window(ref)
+        t = np.unique(np.stack([(pix % W) // 16, (pix // W) // 16], axis=1), axis=0)
+        tiles.append(np.concatenate([np.full((len(t), 1), v), t], axis=1))
+    # composited-sample count of exactly the subset's tiles (SURVEY §8(c)
+    # acceptance: GPU total = oracle total within the R-19 windows)
+    tl = torch.from_numpy(np.ascontiguousarray(np.concatenate(tiles), dtype=np.int32)).cuda()
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    gpu_model(c).render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params, tiles=tl, samples=cnt)
+    torch.cuda.synchronize()
+    got = int(cnt.item())
+    assert abs(got - ref_count) <= max(window, 1e-4 * ref_count), (got, ref_count, window)
+    print(f"C{c} subset samples gpu {got} oracle {ref_count} window {window}")
 
 
 def test_tiled_render_bit_identical_and_unpack():
@@ -410,3 +426,78 @@ def test_spans_narrower_than_a_step(p):
         torch.cuda.synchronize()
         ref = O.render(om, w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
         parity.check_image(img[0].cpu().numpy().reshape(-1, 4), ref, f"p={p} narrow={narrow}")
+
+
+def test_mfa_render_entry_point_itself():
+    """The north_star symbol mfa_render (not mfa_render_ex) called through
+    ctypes: the same image as Model.render bit for bit, parity with the
+    oracle on C1, and the sample count."""
+    import ctypes as C
+
+    from paper_2204_11762_b200 import _lib as LB
+    c = 1
+    w = workload(c)
+    m = gpu_model(c)
+    tf = cuda(w.tf)
+    out = torch.empty((1, 64, 64, 4), dtype=torch.float32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tft = LB.TF_t(C.c_void_p(tf.data_ptr()), tf.shape[0], float(w.v_lo), float(w.v_hi))
+    st = LB.lib().mfa_render(m.handle, 1, LB.cameras_t(w.cameras), C.byref(tft), C.byref(LB.params_t(w.params)),
+                             None, C.c_void_p(out.data_ptr()), C.c_void_p(cnt.data_ptr()),
+                             C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == 0, LB.lib().mfa_last_error()
+    torch.cuda.synchronize()
+    img, ns = render_gpu(c)
+    np.testing.assert_array_equal(out.cpu().numpy(), img)
+    assert int(cnt.item()) == ns
+    ref = O.render(oracle_model(c), w.cameras[0], w.tf, w.v_lo, w.v_hi, w.params)
+    parity.check_image(out[0].cpu().numpy().reshape(-1, 4), ref, "mfa_render C1")
+
+
+def test_many_renders_in_flight_on_distinct_streams():
+    """More than 256 renders of one model queued on distinct streams (one
+    persistent-kernel work counter each): every image is correct, or the
+    call refuses cleanly (MFA_ERR_UNSUPPORTED) -- never a shared counter."""
+    from paper_2204_11762_b200._lib import MfaError
+    w = workload(2, width=48, height=40)
+    m = gpu_model(2)
+    tf = cuda(w.tf)
+    ref = m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(300)]
+    outs, refused = [], 0
+    for s in streams:
+        with torch.cuda.stream(s):
+            o = torch.empty_like(ref)
+            try:
+                m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, out=o)
+                outs.append(o)
+            except MfaError as e:
+                assert "in flight" in str(e)
+                refused += 1
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref)
+    assert len(outs) + refused == 300 and len(outs) >= 256
+
+
+@pytest.mark.parametrize("c,layout", [(2, "auto"), (3, "auto"), (5, "auto"), (5, "quads"), (1, "auto")])
+def test_skip_transparent_gradient_is_bit_identical(c, layout):
+    """NEXT-1 variant (shading = 2): the gradient contraction and Phong are
+    skipped where the TF opacity is 0; those samples composite with weight 0,
+    so the image and the composited-sample count equal the shaded render's
+    bit for bit (C5 on a reduced 4-view batch, both layouts)."""
+    import dataclasses
+    kw = {"n_views": 4, "width": 640, "height": 360} if c == 5 else {}
+    w = workload(c, **kw)
+    m = gpu_model(c, layout) if not kw else __import__("paper_2204_11762_b200").Model.from_workload(w, layout=layout)
+    tf = cuda(w.tf)
+    res = []
+    for sh in (1, 2):
+        prm = dataclasses.replace(w.params, shading=sh)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        img = m.render(w.cameras, tf, w.v_lo, w.v_hi, prm, samples=cnt)
+        torch.cuda.synchronize()
+        res.append((img.cpu().numpy(), int(cnt.item())))
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1]
