@@ -56,7 +56,7 @@ def parse():
                          "identical image)")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: direct NVLink stores into rank 0's image (p2p) or packed tiles + NCCL all-gather")
-    ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier"],
+    ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier", "bricks"],
                     help="control-point layout (default: the library's choice)")
     ap.add_argument("--assign", default="auto", choices=["auto", "views", "rows", "diagonal"],
                     help="N > 1: how (view, tile) units are dealt to ranks (dist.assign_units)")

@@ -96,10 +96,17 @@ mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3],
  *   coefficients of the spline there (Bezier extraction; 256 B per triple for
  *   p = 3), so evaluation needs no per-span basis tables.  Device memory:
  *   4 (p+1)^2 * 4 * S_u S_v S_w bytes (C5: 16.7 GB).
+ *   MFA_LAYOUT_BRICKS (degree <= 3, never chosen by AUTO): plain haloed
+ *   bricks, one fp32 per control point in bricks of 16^3 knot spans plus the
+ *   p halo points, rows padded to 16 bytes: <= 1.86 x the grid (C5: 1.85 x,
+ *   473 MB) -- the compact option of P:133 / P:263 (model size proportional to
+ *   the control points); the kernels read each neighbourhood row as two
+ *   aligned 16-byte loads and shift it (slower than the Bezier blocks).
  */
 #define MFA_LAYOUT_AUTO 0
 #define MFA_LAYOUT_QUADS 1
 #define MFA_LAYOUT_BEZIER 2
+#define MFA_LAYOUT_BRICKS 3
 typedef struct {
     int32_t layout;
 } mfa_model_options;
@@ -116,7 +123,7 @@ typedef struct {
     float v_min, v_max;     /* min / max control value (a TF domain default) */
     int64_t device_bytes;   /* device memory owned by the model */
     int32_t device;         /* CUDA ordinal the model lives on */
-    int32_t layout;         /* MFA_LAYOUT_QUADS or MFA_LAYOUT_BEZIER */
+    int32_t layout;         /* MFA_LAYOUT_QUADS, MFA_LAYOUT_BEZIER or MFA_LAYOUT_BRICKS */
     int64_t model_bytes;    /* the fp32 control grid as passed: 4 n_u n_v n_w (the model
                                size depends on the control-point count) */
     double create_ms;       /* wall time of mfa_model_create (validation, upload, relayout,
@@ -239,8 +246,12 @@ typedef struct {
 
 typedef struct {
     int64_t n_tiles;
-    const int32_t* tiles;      /* device, n_tiles x {view, tile_x, tile_y}, 16x16-pixel tiles;
-                                  view < 0 marks a padding entry (skipped) */
+    const int32_t* tiles;      /* device, n_tiles x {view, tile_x, tile_y}, 16x16-pixel tiles.
+                                  Contract: 0 <= view < n_views (of this call, at most 64),
+                                  0 <= tile_x < ceil(W/16), 0 <= tile_y < ceil(H/16); view < 0
+                                  marks a padding entry.  Padding and any entry outside that
+                                  range are skipped by the kernels (never read frames or store
+                                  outside the image); listing a tile twice renders it twice. */
     int32_t scatter;           /* 0: rgba_out is the packed [n_tiles][16][16][4] buffer;
                                   1: each pixel is stored at its image position, rgba_out is
                                   [n_views][H][W][4] -- which may be another GPU's image mapped
@@ -426,7 +437,8 @@ mfa_status mfa_image_quality(int32_t width, int32_t height, const float* img_a, 
  * ctrl_out    device fp32 [n_w][n_v][n_u] (required); ctrl_out64 optional
  *             device fp64 copy.  A knot layout that leaves a basis function
  *             without samples makes the normal equations singular:
- *             MFA_ERR_INVALID_ARG naming the axis.  Scratch is allocated
+ *             MFA_ERR_INVALID_ARG naming the axis.  A non-finite input
+ *             value: MFA_ERR_DOMAIN (checked before any fit).  Scratch is allocated
  *             internally (not a render-path call) from the device's default
  *             stream-ordered memory pool, whose release threshold is raised to
  *             8 GiB once per device so repeated fits / refinement rounds reuse
@@ -461,7 +473,8 @@ typedef struct {
  *               [n_w][n_v][n_u] with n = res->nctrl.
  * round_log     optional host fp64 [(max_rounds+1)][5]: per fit n_u, n_v, n_w,
  *               max error, rms error.
- * Deterministic except for the rms summation order.  Synchronous.
+ * Deterministic except for the rms summation order.  Synchronous.  A
+ * non-finite input value: MFA_ERR_DOMAIN before the first fit.
  */
 mfa_status mfa_encode_grid(const int64_t dims[3], const float* values, const mfa_encode_config* cfg,
                            double* const knots_out[3], float* ctrl_out, mfa_encode_result* res,

@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
         raise RuntimeError("nvcc failed")
     tmp = LIB + ".tmp"
     cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-L" + cudalib, "-lcublas",
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-L" + cudalib,
                            "-Xlinker", "-rpath=" + cudalib, "-lrt", "-ldl", "-lpthread"])
     os.replace(tmp, LIB)
     return LIB

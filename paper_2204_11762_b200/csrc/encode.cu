@@ -7,19 +7,24 @@
 //
 // Fit (R-27): grid samples at uniform parameters t_j = j/(m-1) per axis; the
 // least-squares solution of (N_w (x) N_v (x) N_u) c = q is separable,
-// c = q x_u N_u^+ x_v N_v^+ x_w N_w^+ with N^+ = (N^T N)^{-1} N^T:
-//   host    per axis: sample spans, basis values (power form per span, fp64),
-//           the banded normal matrix A = N^T N (bandwidth p), its banded
-//           Cholesky factor (a span without samples -> singular -> error), and
-//           the dense n x m operator N^+ by banded solves with the sparse
-//           columns of N^T (fp64)
-//   device  the three axis passes are plain dense fp64 GEMMs over all grid
-//           lines (cuBLAS DGEMM: w pass one GEMM, v pass a strided batch over
-//           the w slices, u pass one GEMM with the operator transposed), with
-//           fp32 <-> fp64 conversion kernels at the ends.  A dense operator
-//           costs 2 m n flops per line instead of the banded solve's ~4 m p,
-//           but every line is independent and the GEMMs run at fp64 tensor
-//           rate; the banded solve is a chain of 2n dependent steps per line.
+// c = q x_u N_u^+ x_v N_v^+ x_w N_w^+ with N^+ = (N^T N)^{-1} N^T.  All on
+// the device, hand-written (no cuBLAS):
+//   K_fs  per sample j: span and the p+1 basis values (Cox-de Boor as power
+//         polynomials per span, fp64) -- one thread per sample
+//   K_fn  the banded normal matrix A = N^T N (bandwidth p), one thread per row
+//         (samples in ascending order: deterministic sums)
+//   K_fc  its banded Cholesky factor, one thread (n p^2 flops, sequential by
+//         nature); a basis function without samples -> singular -> error
+//   K_fm  the dense n x m operator N^+ = A^{-1} N^T: one thread per column j
+//         (forward + backward banded substitution, p-wide register windows)
+//   K_gemm the three axis passes as dense fp64 GEMMs over all grid lines (w
+//         pass one GEMM, v pass a batch over the w slices, u pass one GEMM
+//         with the operator transposed): 64x64 CTA tiles, 4x4 register tiles
+//         per thread, k-slabs of 16 double-buffered in shared memory, DFMA on
+//         the CUDA cores.  A dense operator costs 2 m n flops per line instead
+//         of the banded solve's ~4 m p, but every line is independent; the
+//         banded solve is a chain of 2n dependent steps per line.
+//   fp32 <-> fp64 conversion kernels at the ends.
 // Residual (adaptive loop): K_expand applies N along each axis (the spline
 // at every grid sample, separable), K_err forms |v - q| / (max q - min q) and
 // per-axis per-span maxima (atomicMax on the ordered bits of non-negative
@@ -33,8 +38,6 @@
 #include <string>
 #include <vector>
 
-#include <cublas_v2.h>
-
 #include <map>
 #include <mutex>
 
@@ -42,22 +45,15 @@
 
 namespace mfa {
 
-struct AxisFit {
-    int m = 0, n = 0, p = 0;
-    std::vector<int> f;          // [m] index of the first non-zero function at sample j (= local span)
-    std::vector<double> B;       // [m][p+1] basis values N_{f_j + a}(t_j)
-    std::vector<double> L;       // [n][p+1] banded Cholesky factor, L[i][k] = L(i, i-k)
-    std::vector<double> M;       // [n][m] dense N^+ = (N^T N)^{-1} N^T
-};
-
 struct AxisFitDev {
     int m, n;
-    const int* f;       // [m]
-    const double* B;    // [m][p+1]
+    const int* f;       // [m] first non-zero function at sample j (= local span)
+    const double* B;    // [m][p+1] basis values N_{f_j + a}(t_j)
     const double* M;    // [n][m] dense N^+
 };
 
-// host: the knot span of parameter t (right-continuous; t = 1 -> last non-degenerate span)
+// host: the knot span of parameter t (right-continuous; t = 1 -> last
+// non-degenerate span); the adaptive loop's split rule counts samples per span
 static int host_span(const double* U, int p, int n, double t) {
     if (t >= U[n]) {
         int i = n - 1;
@@ -72,77 +68,135 @@ static int host_span(const double* U, int p, int n, double t) {
     return lo;
 }
 
-static mfa_status build_axis(int d, int m, int n, int p, const double* U, AxisFit& A) {
-    A.m = m;
-    A.n = n;
-    A.p = p;
-    A.f.assign(m, 0);
-    A.B.assign((size_t)m * (p + 1), 0.0);
-    for (int j = 0; j < m; ++j) {
-        const double t = (double)j / (double)(m - 1);
-        const int span = host_span(U, p, n, t);
-        double P[kMaxP + 1][kMaxP + 1];
-        span_poly(U, p, span, P);
-        const double h = U[span + 1] - U[span];
-        const double x = (t - U[span]) / h;
-        for (int a = 0; a <= p; ++a) {
-            double v = P[a][p];
-            for (int k = p - 1; k >= 0; --k) v = v * x + P[a][k];
-            A.B[(size_t)j * (p + 1) + a] = v;
+static std::vector<int> sample_spans(const double* U, int p, int n, int m) {
+    std::vector<int> f(m);
+    for (int j = 0; j < m; ++j) f[j] = host_span(U, p, n, (double)j / (double)(m - 1)) - p;
+    return f;
+}
+
+// ---- K_fs: span and basis values of every sample ---------------------------
+__global__ void fit_samples_kernel(const double* __restrict__ U, int p, int n, int m, int* __restrict__ f,
+                                   double* __restrict__ B) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const double t = (double)j / (double)(m - 1);
+    int span;
+    if (t >= U[n]) {
+        span = n - 1;
+        while (span > p && U[span] == U[n]) --span;
+    } else {
+        int lo = p, hi = n;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) / 2;
+            if (t < U[mid]) hi = mid; else lo = mid;
         }
-        A.f[j] = span - p;
+        span = lo;
     }
-    // banded normal matrix: Ab[i][k] = (N^T N)(i, i-k)
-    std::vector<double> Ab((size_t)n * (p + 1), 0.0);
-    for (int j = 0; j < m; ++j)
-        for (int a = 0; a <= p; ++a)
-            for (int b = 0; b <= a; ++b)
-                Ab[(size_t)(A.f[j] + a) * (p + 1) + (a - b)] += A.B[(size_t)j * (p + 1) + a] * A.B[(size_t)j * (p + 1) + b];
-    // banded Cholesky A = L L^T
-    A.L.assign((size_t)n * (p + 1), 0.0);
-    auto Lat = [&](int r, int c) -> double& { return A.L[(size_t)r * (p + 1) + (r - c)]; };
+    double P[kMaxP + 1][kMaxP + 1];
+    span_poly(U, p, span, P);
+    const double x = (t - U[span]) / (U[span + 1] - U[span]);
+    for (int a = 0; a <= p; ++a) {
+        double v = P[a][p];
+        for (int k = p - 1; k >= 0; --k) v = v * x + P[a][k];
+        B[(size_t)j * (p + 1) + a] = v;
+    }
+    f[j] = span - p;
+}
+
+// first sample index j with f[j] >= key (f is nondecreasing in j)
+__device__ __forceinline__ int lower_bound_f(const int* __restrict__ f, int m, int key) {
+    int lo = 0, hi = m;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (f[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// ---- K_fn: banded normal matrix Ab[r][k] = (N^T N)(r, r - k) ----------------
+// entry (r, c = r - k) sums B[j][r - f_j] B[j][c - f_j] over the samples with
+// f_j in [r - p, c], in ascending j (deterministic)
+__global__ void fit_normal_kernel(const int* __restrict__ f, const double* __restrict__ B, int p, int n, int m,
+                                  double* __restrict__ Ab) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    for (int k = 0; k <= p; ++k) {
+        const int c = r - k;
+        double acc = 0.0;
+        if (c >= 0) {
+            const int j1 = lower_bound_f(f, m, c + 1);
+            for (int j = lower_bound_f(f, m, r - p); j < j1; ++j)
+                acc += B[(size_t)j * (p + 1) + (r - f[j])] * B[(size_t)j * (p + 1) + (c - f[j])];
+        }
+        Ab[(size_t)r * (p + 1) + k] = acc;
+    }
+}
+
+// ---- K_fc: banded Cholesky A = L L^T, L[i][k] = L(i, i - k) -----------------
+// status[0] = -1 on success, else the first control point whose pivot failed
+__global__ void fit_cholesky_kernel(const double* __restrict__ Ab, int p, int n, double* __restrict__ L,
+                                    int* __restrict__ status) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    status[0] = -1;
     for (int i = 0; i < n; ++i) {
-        for (int c = std::max(0, i - p); c < i; ++c) {
-            double s = Ab[(size_t)i * (p + 1) + (i - c)];
-            for (int l = std::max(0, i - p); l < c; ++l) s -= Lat(i, l) * Lat(c, l);
-            Lat(i, c) = s / Lat(c, c);
+        for (int c = max(0, i - p); c < i; ++c) {
+            double sum = Ab[(size_t)i * (p + 1) + (i - c)];
+            for (int l = max(0, i - p); l < c; ++l) sum -= L[(size_t)i * (p + 1) + (i - l)] * L[(size_t)c * (p + 1) + (c - l)];
+            L[(size_t)i * (p + 1) + (i - c)] = sum / L[(size_t)c * (p + 1)];
         }
-        double s = Ab[(size_t)i * (p + 1)];
-        for (int l = std::max(0, i - p); l < i; ++l) s -= Lat(i, l) * Lat(i, l);
-        if (!(s > 1e-14 * std::max(1.0, Ab[(size_t)i * (p + 1)])))
-            return fail(MFA_ERR_INVALID_ARG, std::string("fit: normal equations singular on axis ") + "uvw"[d] +
-                                                 " at control point " + std::to_string(i) +
-                                                 " (a basis function without samples: too many control points for the grid)");
-        Lat(i, i) = sqrt(s);
-    }
-    // dense pseudo-inverse N^+ = A^{-1} N^T (n x m, row-major): column j of N^T
-    // has p+1 entries at rows f_j .. f_j + p; forward then backward banded
-    // solve, all m columns at once row by row (contiguous rows of length m)
-    A.M.assign((size_t)n * m, 0.0);
-    double* Y = A.M.data();
-    for (int j = 0; j < m; ++j)
-        for (int a = 0; a <= p; ++a) Y[(size_t)(A.f[j] + a) * m + j] = A.B[(size_t)j * (p + 1) + a];
-    for (int i = 0; i < n; ++i) {
-        double* yi = Y + (size_t)i * m;
-        for (int l = std::max(0, i - p); l < i; ++l) {
-            const double c = Lat(i, l);
-            const double* yl = Y + (size_t)l * m;
-            for (int j = 0; j < m; ++j) yi[j] -= c * yl[j];
+        double sum = Ab[(size_t)i * (p + 1)];
+        for (int l = max(0, i - p); l < i; ++l) sum -= L[(size_t)i * (p + 1) + (i - l)] * L[(size_t)i * (p + 1) + (i - l)];
+        if (!(sum > 1e-14 * fmax(1.0, Ab[(size_t)i * (p + 1)]))) {
+            status[0] = i;
+            return;
         }
-        const double dg = Lat(i, i);
-        for (int j = 0; j < m; ++j) yi[j] /= dg;
+        L[(size_t)i * (p + 1)] = sqrt(sum);
     }
+}
+
+// ---- K_fm: N^+ = A^{-1} N^T, one thread per column j --------------------------
+// column j of N^T has p+1 entries B[j][a] at rows f_j + a; forward substitution
+// from row f_j (rows above are 0), then backward over all rows; a p-wide
+// window of the latest results stays in registers
+template <int P>
+__global__ void fit_pinv_kernel(const int* __restrict__ f, const double* __restrict__ B, const double* __restrict__ L,
+                                int n, int m, double* __restrict__ M) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const int fj = f[j];
+    for (int i = 0; i < fj; ++i) M[(size_t)i * m + j] = 0.0;
+    double win[P + 1];   // win[q] = y_{i-1-q}
+#pragma unroll
+    for (int q = 0; q <= P; ++q) win[q] = 0.0;
+    for (int i = fj; i < n; ++i) {
+        double sum = (i - fj <= P) ? B[(size_t)j * (P + 1) + (i - fj)] : 0.0;
+        // L(i, l) for l = i-P .. i-1 (ascending l, as the row-wise host order)
+#pragma unroll
+        for (int q = P - 1; q >= 0; --q) {
+            const int l = i - 1 - q;
+            if (l >= fj) sum -= L[(size_t)i * (P + 1) + (i - l)] * win[q];
+        }
+        const double y = sum / L[(size_t)i * (P + 1)];
+#pragma unroll
+        for (int q = P; q > 0; --q) win[q] = win[q - 1];
+        win[0] = y;
+        M[(size_t)i * m + j] = y;
+    }
+#pragma unroll
+    for (int q = 0; q <= P; ++q) win[q] = 0.0;   // win[q] = x_{i+1+q}
     for (int i = n - 1; i >= 0; --i) {
-        double* yi = Y + (size_t)i * m;
-        for (int l = i + 1; l <= std::min(n - 1, i + p); ++l) {
-            const double c = Lat(l, i);
-            const double* yl = Y + (size_t)l * m;
-            for (int j = 0; j < m; ++j) yi[j] -= c * yl[j];
+        double sum = M[(size_t)i * m + j];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const int l = i + 1 + q;
+            if (l < n) sum -= L[(size_t)l * (P + 1) + (l - i)] * win[q];
         }
-        const double dg = Lat(i, i);
-        for (int j = 0; j < m; ++j) yi[j] /= dg;
+        const double x = sum / L[(size_t)i * (P + 1)];
+#pragma unroll
+        for (int q = P; q > 0; --q) win[q] = win[q - 1];
+        win[0] = x;
+        M[(size_t)i * m + j] = x;
     }
-    return MFA_OK;
 }
 
 __global__ void f32_to_f64_kernel(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
@@ -227,12 +281,19 @@ __global__ void grid_error_kernel(const double* __restrict__ V, const float* __r
     }
 }
 
-__global__ void range_kernel(const float* __restrict__ Q, int64_t n, double* __restrict__ out /*min,max*/) {
+// value range of the grid (ordered-bits min / max in out[0..1]) and the
+// number of non-finite samples (out[2], as an unsigned long long)
+__global__ void range_kernel(const float* __restrict__ Q, int64_t n, double* __restrict__ out /*min,max,bad*/) {
     double lo = INFINITY, hi = -INFINITY;
+    unsigned bad = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        lo = fmin(lo, (double)Q[i]);
-        hi = fmax(hi, (double)Q[i]);
+        const float q = Q[i];
+        bad += !isfinite(q);
+        lo = fmin(lo, (double)q);
+        hi = fmax(hi, (double)q);
     }
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(reinterpret_cast<unsigned long long*>(out) + 2, (unsigned long long)bad);
     for (int o = 16; o > 0; o >>= 1) {
         lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
@@ -253,8 +314,9 @@ static double ord_to_double(unsigned long long u) {
     return d;
 }
 
-// device copy of one axis' tables (one allocation)
-struct AxisDevMem {     // stream-ordered allocations (the pool makes repeated fits cheap)
+// one axis' device tables (one stream-ordered allocation; the pool makes
+// repeated fits cheap)
+struct AxisDevMem {
     void* mem = nullptr;
     AxisFitDev d{};
     void release(cudaStream_t st) {
@@ -263,20 +325,44 @@ struct AxisDevMem {     // stream-ordered allocations (the pool makes repeated f
     }
 };
 
-static cudaError_t upload_axis(const AxisFit& A, AxisDevMem& D, cudaStream_t st) {
-    const size_t nf = sizeof(int) * A.m, nb = sizeof(double) * A.B.size(), nm = sizeof(double) * A.M.size();
+// the operator of axis d on the device: samples, normal matrix, Cholesky,
+// N^+ (K_fs, K_fn, K_fc, K_fm); synchronises once to report a singular fit
+static mfa_status build_axis_dev(int d, int m, int n, int p, const double* U_host, AxisDevMem& D, cudaStream_t st) {
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    cudaError_t e = cudaMallocAsync(&D.mem, up(nf) + up(nb) + up(nm), st);
-    if (e != cudaSuccess) return e;
+    const size_t nu = sizeof(double) * (n + p + 1), nf = sizeof(int) * m, nb = sizeof(double) * (size_t)m * (p + 1),
+                 nab = sizeof(double) * (size_t)n * (p + 1), nm = sizeof(double) * (size_t)n * m;
+    cudaError_t e = cudaMallocAsync(&D.mem, up(nu) + up(nf) + up(nb) + 2 * up(nab) + up(nm) + 256, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fit tables");
     char* b = (char*)D.mem;
-    int* f = (int*)b;
-    double* B = (double*)(b + up(nf));
-    double* M = (double*)(b + up(nf) + up(nb));
-    cudaMemcpyAsync(f, A.f.data(), nf, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(B, A.B.data(), nb, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(M, A.M.data(), nm, cudaMemcpyHostToDevice, st);
-    D.d = AxisFitDev{A.m, A.n, f, B, M};
-    return cudaSuccess;
+    double* U = (double*)b;
+    int* f = (int*)(b + up(nu));
+    double* B = (double*)(b + up(nu) + up(nf));
+    double* Ab = (double*)(b + up(nu) + up(nf) + up(nb));
+    double* L = (double*)(b + up(nu) + up(nf) + up(nb) + up(nab));
+    double* M = (double*)(b + up(nu) + up(nf) + up(nb) + 2 * up(nab));
+    int* status = (int*)(b + up(nu) + up(nf) + up(nb) + 2 * up(nab) + up(nm));
+    cudaMemcpyAsync(U, U_host, nu, cudaMemcpyHostToDevice, st);
+    fit_samples_kernel<<<(m + 127) / 128, 128, 0, st>>>(U, p, n, m, f, B);
+    fit_normal_kernel<<<(n + 127) / 128, 128, 0, st>>>(f, B, p, n, m, Ab);
+    fit_cholesky_kernel<<<1, 32, 0, st>>>(Ab, p, n, L, status);
+    const unsigned g = (unsigned)((m + 127) / 128);
+    switch (p) {
+        case 1: fit_pinv_kernel<1><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
+        case 2: fit_pinv_kernel<2><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
+        case 3: fit_pinv_kernel<3><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
+        case 4: fit_pinv_kernel<4><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
+        default: fit_pinv_kernel<5><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
+    }
+    int hs = -1;
+    cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "fit operator");
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fit operator kernels");
+    if (hs >= 0)
+        return fail(MFA_ERR_INVALID_ARG, std::string("fit: normal equations singular on axis ") + "uvw"[d] +
+                                             " at control point " + std::to_string(hs) +
+                                             " (a basis function without samples: too many control points for the grid)");
+    D.d = AxisFitDev{m, n, f, B, M};
+    return MFA_OK;
 }
 
 // Keep the device's default stream-ordered pool from returning memory to the
@@ -297,21 +383,6 @@ static void keep_pool() {
     done[dev] = true;
 }
 
-// one cuBLAS handle per (host thread, device)
-static cublasStatus_t blas_handle(cublasHandle_t* h) {
-    static thread_local std::map<int, cublasHandle_t> handles;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    auto it = handles.find(dev);
-    if (it != handles.end()) {
-        *h = it->second;
-        return CUBLAS_STATUS_SUCCESS;
-    }
-    cublasStatus_t r = cublasCreate(h);
-    if (r == CUBLAS_STATUS_SUCCESS) handles[dev] = *h;
-    return r;
-}
-
 static unsigned grid_for(int64_t work) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -319,28 +390,122 @@ static unsigned grid_for(int64_t work) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 127) / 128, (int64_t)sms * 16));
 }
 
-// the three axis passes as fp64 GEMMs (row-major views; cuBLAS is column-major):
+// ---- K_gemm: C[z][M][N] = A[z][M][K] . op(B)[z][K][N], fp64, row-major -----
+// op(B) = B[K][N] (BT = false) or B^T with B stored [N][K] (BT = true).
+// 64 x 64 tile per 256-thread CTA, each thread a 4 x 4 register tile; k-slabs
+// of 16 staged through shared memory (double-buffered: the next slab's global
+// loads are in flight while the current one is multiplied).  Batch z via
+// blockIdx.z with element strides sa, sb, sc (0 = shared operand).
+constexpr int kGM = 64, kGN = 64, kGK = 16;
+
+template <bool BT>
+__global__ void __launch_bounds__(256) dgemm_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                                    double* __restrict__ C, int M, int N, int K, int64_t sa,
+                                                    int64_t sb, int64_t sc) {
+    __shared__ double As[2][kGK][kGM + 2];   // As[k][m]
+    __shared__ double Bs[2][kGK][kGN + 2];   // Bs[k][n]
+    const int z = blockIdx.z;
+    A += z * sa;
+    B += z * sb;
+    C += z * sc;
+    const int m0 = blockIdx.y * kGM, n0 = blockIdx.x * kGN;
+    const int tid = threadIdx.x;
+    const int tm = (tid / 16) * 4, tn = (tid % 16) * 4;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    // each thread stages 4 elements of A and 4 of B per slab
+    double ra[4], rb[4];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + 256 * q;              // 0..1023
+            // A tile 64 (m) x 16 (k): k fastest in memory (row-major A)
+            const int am = e / kGK, ak = e % kGK;
+            const int gm = m0 + am, gk = k0 + ak;
+            ra[q] = (gm < M && gk < K) ? A[(int64_t)gm * K + gk] : 0.0;
+            if (BT) {   // B stored [N][K]: k fastest
+                const int bn = e / kGK, bk = e % kGK;
+                const int gn = n0 + bn, gk2 = k0 + bk;
+                rb[q] = (gn < N && gk2 < K) ? B[(int64_t)gn * K + gk2] : 0.0;
+            } else {    // B stored [K][N]: n fastest
+                const int bk = e / kGN, bn = e % kGN;
+                const int gn = n0 + bn, gk2 = k0 + bk;
+                rb[q] = (gn < N && gk2 < K) ? B[(int64_t)gk2 * N + gn] : 0.0;
+            }
+        }
+    };
+    auto stash = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + 256 * q;
+            As[buf][e % kGK][e / kGK] = ra[q];
+            if (BT) Bs[buf][e % kGK][e / kGK] = rb[q];
+            else Bs[buf][e / kGN][e % kGN] = rb[q];
+        }
+    };
+    load(0);
+    stash(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = 0; k0 < K; k0 += kGK) {
+        const bool more = k0 + kGK < K;
+        if (more) load(k0 + kGK);
+#pragma unroll
+        for (int k = 0; k < kGK; ++k) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[buf][k][tm + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[buf][k][tn + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        if (more) {
+            stash(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gm = m0 + tm + i;
+        if (gm >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gn = n0 + tn + j;
+            if (gn < N) C[(int64_t)gm * N + gn] = acc[i][j];
+        }
+    }
+}
+
+static cudaError_t dgemm(bool bt, const double* A, const double* B, double* C, int M, int N, int K, int batch,
+                         int64_t sa, int64_t sb, int64_t sc, cudaStream_t st) {
+    const dim3 grid((unsigned)((N + kGN - 1) / kGN), (unsigned)((M + kGM - 1) / kGM), (unsigned)batch);
+    if (bt) dgemm_kernel<true><<<grid, 256, 0, st>>>(A, B, C, M, N, K, sa, sb, sc);
+    else dgemm_kernel<false><<<grid, 256, 0, st>>>(A, B, C, M, N, K, sa, sb, sc);
+    return cudaGetLastError();
+}
+
+// the three axis passes (row-major):
 //   w: T1[nw][mv*mu]  = M_w[nw][mw] . Q64[mw][mv*mu]
 //   v: T2[k][nv][mu]  = M_v[nv][mv] . T1[k][mv][mu]      (batch over k < nw)
-//   u: C64[nw*nv][nu] = T2[nw*nv][mu] . M_u^T
+//   u: C64[nw*nv][nu] = T2[nw*nv][mu] . M_u^T             (M_u stored [nu][mu])
 static mfa_status fit_all(const double* Q64, const AxisFitDev (&ax)[3], double* T1, double* T2, float* C32,
                           double* C64, cudaStream_t st) {
     const int mu = ax[0].m, mv = ax[1].m, mw = ax[2].m, nu = ax[0].n, nv = ax[1].n, nw = ax[2].n;
-    cublasHandle_t h;
-    if (blas_handle(&h) != CUBLAS_STATUS_SUCCESS) return fail(MFA_ERR_CUDA, "cublasCreate failed");
-    cublasSetStream(h, st);
-    const double one = 1.0, zero = 0.0;
-    cublasStatus_t r = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, mv * mu, nw, mw, &one, Q64, mv * mu, ax[2].M, mw,
-                                   &zero, T1, mv * mu);
-    if (r == CUBLAS_STATUS_SUCCESS)
-        r = cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, mu, nv, mv, &one, T1, mu, (long long)mv * mu,
-                                      ax[1].M, mv, 0, &zero, T2, mu, (long long)nv * mu, nw);
-    if (r == CUBLAS_STATUS_SUCCESS)
-        r = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, nu, nw * nv, mu, &one, ax[0].M, mu, T2, mu, &zero, C64, nu);
-    if (r != CUBLAS_STATUS_SUCCESS) return fail(MFA_ERR_CUDA, "cublasDgemm failed (" + std::to_string((int)r) + ")");
+    cudaError_t e = dgemm(false, ax[2].M, Q64, T1, nw, mv * mu, mw, 1, 0, 0, 0, st);
+    if (e == cudaSuccess)
+        e = dgemm(false, ax[1].M, T1, T2, nv, mu, mv, nw, 0, (int64_t)mv * mu, (int64_t)nv * mu, st);
+    if (e == cudaSuccess) e = dgemm(true, T2, ax[0].M, C64, nw * nv, nu, mu, 1, 0, 0, 0, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fit GEMM");
     const int64_t nc = (int64_t)nu * nv * nw;
     f64_to_f32_kernel<<<grid_for(nc), 128, 0, st>>>(C64, C32, nc);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "fit conversion");
 }
 
@@ -399,12 +564,10 @@ extern "C" mfa_status mfa_fit_grid(const int64_t dims[3], const float* values, i
     if (s != MFA_OK) return s;
     if (!knots || !ctrl_out) return fail(MFA_ERR_INVALID_ARG, "knots and ctrl_out are required");
     const int p = degree;
-    AxisFit A[3];
     for (int d = 0; d < 3; ++d) {
         int uni = 0;
         if (!knots[d]) return fail(MFA_ERR_INVALID_ARG, "knots[d] is NULL");
         if ((s = validate_knots(d, p, nctrl[d], knots[d], &uni)) != MFA_OK) return s;
-        if ((s = build_axis(d, (int)dims[d], (int)nctrl[d], p, knots[d], A[d])) != MFA_OK) return s;
     }
     cudaStream_t st = (cudaStream_t)stream;
     keep_pool();
@@ -417,8 +580,19 @@ extern "C" mfa_status mfa_fit_grid(const int64_t dims[3], const float* values, i
         return r;
     };
     cudaError_t e;
+    {   // non-finite samples would turn every control value NaN: refuse up front
+        double* rng_dev = nullptr;
+        if ((e = cudaMallocAsync(&rng_dev, 3 * sizeof(double), st)) != cudaSuccess) return done(cuda_fail(e, "fit scratch"));
+        unsigned long long rb[3] = {~0ULL, 0ULL, 0ULL};
+        cudaMemcpyAsync(rng_dev, rb, sizeof(rb), cudaMemcpyHostToDevice, st);
+        range_kernel<<<grid_for(dims[0] * dims[1] * dims[2]), 128, 0, st>>>(values, dims[0] * dims[1] * dims[2], rng_dev);
+        cudaMemcpyAsync(rb, rng_dev, sizeof(rb), cudaMemcpyDeviceToHost, st);
+        cudaFreeAsync(rng_dev, st);
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return done(cuda_fail(e, "fit range"));
+        if (rb[2]) return done(fail(MFA_ERR_DOMAIN, std::to_string(rb[2]) + " non-finite grid values"));
+    }
     for (int d = 0; d < 3; ++d)
-        if ((e = upload_axis(A[d], D[d], st)) != cudaSuccess) return done(cuda_fail(e, "fit tables"));
+        if ((s = build_axis_dev(d, (int)dims[d], (int)nctrl[d], p, knots[d], D[d], st)) != MFA_OK) return done(s);
     const int64_t mu = dims[0], mv = dims[1], mw = dims[2], nu = nctrl[0], nv = nctrl[1], nw = nctrl[2];
     if ((e = cudaMallocAsync(&W.Q64, sizeof(double) * mw * mv * mu, st)) != cudaSuccess) return done(cuda_fail(e, "fit scratch"));
     f32_to_f64_kernel<<<grid_for(mw * mv * mu), 128, 0, st>>>(values, W.Q64, mw * mv * mu);
@@ -482,13 +656,14 @@ extern "C" mfa_status mfa_encode_grid(const int64_t dims[3], const float* values
     const int64_t nerr = cap[0] + cap[1] + cap[2] + 2;
     if ((e = cudaMallocAsync(&W.err, sizeof(unsigned long long) * nerr, st)) != cudaSuccess)
         return done(cuda_fail(e, "encode scratch"));
-    if ((e = cudaMallocAsync(&rng_dev, 2 * sizeof(double), st)) != cudaSuccess) return done(cuda_fail(e, "encode scratch"));
-    unsigned long long rinit[2] = {~0ULL, 0ULL};
+    if ((e = cudaMallocAsync(&rng_dev, 3 * sizeof(double), st)) != cudaSuccess) return done(cuda_fail(e, "encode scratch"));
+    unsigned long long rinit[3] = {~0ULL, 0ULL, 0ULL};
     cudaMemcpyAsync(rng_dev, rinit, sizeof(rinit), cudaMemcpyHostToDevice, st);
     range_kernel<<<grid_for(npts), 128, 0, st>>>(values, npts, rng_dev);
-    unsigned long long rb[2];
+    unsigned long long rb[3];
     cudaMemcpyAsync(rb, rng_dev, sizeof(rb), cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return done(cuda_fail(e, "encode range"));
+    if (rb[2]) return done(fail(MFA_ERR_DOMAIN, std::to_string(rb[2]) + " non-finite grid values"));
     const double range = ord_to_double(rb[1]) - ord_to_double(rb[0]);
     const double inv_range = range > 0.0 ? 1.0 / range : 1.0;
 
@@ -496,13 +671,11 @@ extern "C" mfa_status mfa_encode_grid(const int64_t dims[3], const float* values
     bool converged = false;
     double max_err = 0.0, rms = 0.0;
     for (;;) {
-        AxisFit A[3];
         int64_t n[3];
         for (int d = 0; d < 3; ++d) {
             n[d] = (int64_t)U[d].size() - p - 1;
-            if ((s = build_axis(d, (int)dims[d], (int)n[d], p, U[d].data(), A[d])) != MFA_OK) return done(s);
             D[d].release(st);
-            if ((e = upload_axis(A[d], D[d], st)) != cudaSuccess) return done(cuda_fail(e, "encode tables"));
+            if ((s = build_axis_dev(d, (int)dims[d], (int)n[d], p, U[d].data(), D[d], st)) != MFA_OK) return done(s);
         }
         const AxisFitDev ax[3] = {D[0].d, D[1].d, D[2].d};
         if ((s = fit_all(W.Q64, ax, W.T1, W.T2, ctrl_out, W.C64, st)) != MFA_OK) return done(s);
@@ -548,7 +721,7 @@ extern "C" mfa_status mfa_encode_grid(const int64_t dims[3], const float* values
         for (int d = 0; d < 3; ++d) {
             const int64_t Sd = n[d] - p;
             std::vector<int> cnt(Sd, 0);
-            for (int j = 0; j < A[d].m; ++j) cnt[A[d].f[j]]++;
+            for (int fj : sample_spans(U[d].data(), p, (int)n[d], (int)dims[d])) cnt[fj]++;
             std::vector<double> ins;
             for (int64_t sp = 0; sp < Sd; ++sp)
                 if (dv(hs[d][sp]) > cfg->e_max && cnt[sp] >= 2 * (p + 1) && n[d] + (int64_t)ins.size() < cap[d])

@@ -102,6 +102,26 @@ __global__ void __launch_bounds__(256, MFA_EVAL_MINB) eval_kernel(const __grid_c
             }
             continue;
         }
+        if constexpr (LAYOUT == kBricks) {   // plain haloed bricks: the block into registers
+            float nb[P + 1][P + 1][P + 1];
+            load_pblock<P>(args.Q, plain_entry<P>(args.g, s[0], s[1], s[2]), nb);
+            if (GRAD) {
+                float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
+                axis_basis<P, false>(args.ax[0], UNI, s[0], t[0], Bu);
+                axis_basis<P, true>(args.ax[1], UNI, s[1], t[1], Bv);
+                axis_basis<P, false>(args.ax[2], UNI, s[2], t[2], Bw);
+                float val, gu, gv, gw;
+                contract_vg_cached<P>(nb, Bu, Bv, Bw, val, gu, gv, gw);
+                store(val, gu * sc[0], gv * sc[1], gw * sc[2]);
+            } else {
+                float Nu[P + 1], Nv[P + 1], Nw[P + 1];
+                axis_basis_value<P>(args.ax[0], UNI, s[0], t[0], Nu);
+                axis_basis_value<P>(args.ax[1], UNI, s[1], t[1], Nv);
+                axis_basis_value<P>(args.ax[2], UNI, s[2], t[2], Nw);
+                store(contract_v_cached<P>(nb, Nu, Nv, Nw), 0.f, 0.f, 0.f);
+            }
+            continue;
+        }
         const float4* base = args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
         float r0[P + 1][P + 1];
         load_slab<P>(base, r0);   // issued before the basis so its latency overlaps it
@@ -155,6 +175,7 @@ template <int P>
 static cudaError_t dispatch_eval(const EvalArgs& a, int layout, bool uni, bool grad, cudaStream_t st) {
     if constexpr (P <= 3) {
         if (layout == kBezier) return dispatch_eval_l<P, kBezier>(a, uni, grad, st);
+        if (layout == kBricks) return dispatch_eval_l<P, kBricks>(a, uni, grad, st);
     }
     return dispatch_eval_l<P, kQuads>(a, uni, grad, st);
 }

@@ -75,7 +75,9 @@ __global__ void __launch_bounds__(256) hessian_kernel(const __grid_constant__ He
                 }
             }
             const float4* base = BEZ ? bez_block<P>(args.Q, args.bg, s[0], s[1], s[2])
-                                     : args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]);
+                                     : (LAYOUT == kBricks ? args.Q : args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]));
+            PlainRef pe{0, 0};
+            if constexpr (LAYOUT == kBricks) pe = plain_entry<P>(args.g, s[0], s[1], s[2]);
             float Nu[P + 1], Du[P + 1], Eu[P + 1], Nv[P + 1], Dv[P + 1], Ev[P + 1], Nw[P + 1], Dw[P + 1], Ew[P + 1];
             basis3<P, LAYOUT, UNI>(args.ax[0], s[0], t[0], Nu, Du, Eu);
             basis3<P, LAYOUT, UNI>(args.ax[1], s[1], t[1], Nv, Dv, Ev);
@@ -87,6 +89,8 @@ __global__ void __launch_bounds__(256) hessian_kernel(const __grid_constant__ He
                 float r[P + 1][P + 1];
                 if constexpr (BEZ)
                     load_bslab<P>(bslab_ptr<P>(base, c), r);
+                else if constexpr (LAYOUT == kBricks)
+                    load_pslab<P>(base, pe, c, r);
                 else
                     load_slab<P>(base + c * Brick<P>::SLAB, r);
                 float B[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -191,6 +195,8 @@ static cudaError_t dispatch_hess(const HessArgs& a, int layout, bool uni, cudaSt
     if constexpr (P <= 3) {
         if (layout == kBezier)
             return uni ? launch_hess_t<P, kBezier, true>(a, st) : launch_hess_t<P, kBezier, false>(a, st);
+        if (layout == kBricks)
+            return uni ? launch_hess_t<P, kBricks, true>(a, st) : launch_hess_t<P, kBricks, false>(a, st);
     }
     return uni ? launch_hess_t<P, kQuads, true>(a, st) : launch_hess_t<P, kQuads, false>(a, st);
 }

@@ -96,6 +96,63 @@ __device__ __forceinline__ int64_t brick_entry(const BrickGrid& g, int su, int s
 }
 
 // ---------------------------------------------------------------------------
+// Plain haloed bricks (kBricks, p <= 3; mfa_internal.cuh pbrick_*): the
+// neighbourhood of span triple (su, sv, sw) starts at local (lu, lv, lw) =
+// s & 15 of its brick; a row of p+1 values sits at float offset lu of a
+// 16-byte-aligned row, so it is read as the two aligned float4 around it and
+// shifted by o = lu & 3 with two levels of selects.
+// ---------------------------------------------------------------------------
+template <int P>
+struct PBrick {
+    static constexpr int EU = pbrick_eu(P);
+    static constexpr int EV = pbrick_ev(P);
+    static constexpr int SIZE = EU * EV * EV;   // floats per brick
+};
+
+struct PlainRef {
+    int64_t base;   // float offset of the 16-byte-aligned start of row (0, 0)
+    int o;          // shift of the first value inside it (0..3)
+};
+
+template <int P>
+__device__ __forceinline__ PlainRef plain_entry(const BrickGrid& g, int su, int sv, int sw) {
+    const int bx = su >> kBrickLog, by = sv >> kBrickLog, bz = sw >> kBrickLog;
+    const int lu = su & (kBrick - 1), lv = sv & (kBrick - 1), lw = sw & (kBrick - 1);
+    const int64_t brick = ((int64_t)bz * g.nby + by) * g.nbx + bx;
+    const int64_t b = brick * PBrick<P>::SIZE + (lw * PBrick<P>::EV + lv) * PBrick<P>::EU + (lu & ~3);
+    MFA_DCHECK(su >= 0 && sv >= 0 && sw >= 0 &&
+               4 * (b + (P * PBrick<P>::EV + P) * PBrick<P>::EU + 8) <= 16 * g.q_f4);
+    return PlainRef{b, lu & 3};
+}
+
+template <int P>
+__device__ __forceinline__ void load_prow(const float* __restrict__ Qf, int64_t off, int o, float (&r)[P + 1]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(Qf + off));
+    const float4 c = __ldg(reinterpret_cast<const float4*>(Qf + off) + 1);
+    const float x[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+    float y[P + 2];
+#pragma unroll
+    for (int i = 0; i < P + 2; ++i) y[i] = (o & 2) ? x[i + 2] : x[i];
+#pragma unroll
+    for (int i = 0; i <= P; ++i) r[i] = (o & 1) ? y[i + 1] : y[i];
+}
+
+template <int P>
+__device__ __forceinline__ void load_pslab(const float4* __restrict__ Q, const PlainRef& e, int c,
+                                           float (&r)[P + 1][P + 1]) {
+    const float* Qf = reinterpret_cast<const float*>(Q);
+#pragma unroll
+    for (int b = 0; b <= P; ++b) load_prow<P>(Qf, e.base + (c * PBrick<P>::EV + b) * PBrick<P>::EU, e.o, r[b]);
+}
+
+template <int P>
+__device__ __forceinline__ void load_pblock(const float4* __restrict__ Q, const PlainRef& e,
+                                            float (&nb)[P + 1][P + 1][P + 1]) {
+#pragma unroll
+    for (int c = 0; c <= P; ++c) load_pslab<P>(Q, e, c, nb[c]);
+}
+
+// ---------------------------------------------------------------------------
 // a5: basis values and t-derivatives.
 //
 // Interior spans of a clamped uniform knot vector (spans p-1 .. S-p) all

@@ -87,12 +87,19 @@ struct AxisTables {
     float S = 0.f;                    // uniform: number of spans as float
 };
 
-enum Layout { kQuads = 0, kBezier = 1 };
+enum Layout { kQuads = 0, kBezier = 1, kBricks = 2 };
+
+// plain haloed bricks (kBricks, p <= 3): one fp32 per control point, bricks
+// of 16^3 spans with the p halo points on the high side, rows padded to a
+// multiple of 4 floats (16-byte aligned): (16+p rounded up to 4) x (16+p)^2
+// floats per brick, <= 1.86 x the grid (C5: 1.85 x)
+__host__ __device__ constexpr int pbrick_eu(int p) { return ((kBrick + p + 3) / 4) * 4; }
+__host__ __device__ constexpr int pbrick_ev(int p) { return kBrick + p; }
 
 struct Model {
     int device = 0;
     int p = 0;
-    int layout = kQuads;           // kBezier: per-span-triple Bernstein blocks (non-uniform, p <= 3)
+    int layout = kQuads;           // kBezier: per-span-triple Bernstein blocks (p <= 3); kBricks: plain haloed bricks
     int64_t n[3] = {0, 0, 0};
     int uniform[3] = {0, 0, 0};
     float vmin = 0.f, vmax = 0.f;

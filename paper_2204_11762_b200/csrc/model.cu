@@ -90,6 +90,28 @@ __global__ void relayout_bricks_kernel(const float* __restrict__ P, float4* __re
     }
 }
 
+// K1c: plain haloed bricks (kBricks, p <= 3).  Brick (bx,by,bz) float
+// (lu,lv,lw) = P[k][j][i] of i = 16 bx + lu, j = 16 by + lv, k = 16 bz + lw
+// (zeros outside the grid and in the row padding).  One thread per float.
+__global__ void relayout_plain_kernel(const float* __restrict__ P, float* __restrict__ Q, int nu, int nv, int nw,
+                                      int nbx, int nby, int EU, int EV, int64_t total) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t bsz = (int64_t)EU * EV * EV;
+        const int64_t brick = idx / bsz;
+        int rem = (int)(idx - brick * bsz);
+        const int lu = rem % EU;
+        rem /= EU;
+        const int lv = rem % EV;
+        const int lw = rem / EV;
+        const int bx = (int)(brick % nbx);
+        const int by = (int)((brick / nbx) % nby);
+        const int bz = (int)(brick / ((int64_t)nbx * nby));
+        const int i = bx * kBrick + lu, j = by * kBrick + lv, k = bz * kBrick + lw;
+        Q[idx] = (lu < EV && i < nu && j < nv && k < nw) ? P[((int64_t)k * nv + j) * nu + i] : 0.f;
+    }
+}
+
 // Order-preserving float <-> uint mapping for atomic min/max.
 __device__ __forceinline__ unsigned int f2ord(float f) {
     unsigned int u = __float_as_uint(f);
@@ -266,11 +288,14 @@ __global__ void knot_tables_kernel(const double* __restrict__ U, int p, int nsp,
 // K4: scatter packed 16x16 tiles into images.
 // ---------------------------------------------------------------------------
 __global__ void unpack_tiles_kernel(const void* __restrict__ packed, int in_fp16, const int* __restrict__ tiles,
-                                    int64_t n_tiles, int W, int H, float4* __restrict__ img) {
+                                    int64_t n_tiles, int n_views, int W, int H, float4* __restrict__ img) {
     const int64_t t = blockIdx.x;
     if (t >= n_tiles) return;
     const int view = tiles[3 * t], tx = tiles[3 * t + 1], ty = tiles[3 * t + 2];
-    if (view < 0) return;  // padding unit
+    // padding units (view = -1) and malformed entries are skipped (no store outside the image)
+    if (view < 0 || view >= n_views || tx < 0 || ty < 0 || tx >= (W + MFA_TILE - 1) / MFA_TILE ||
+        ty >= (H + MFA_TILE - 1) / MFA_TILE)
+        return;
     const int px = threadIdx.x & 15, py = threadIdx.x >> 4;
     const int x = tx * MFA_TILE + px, y = ty * MFA_TILE + py;
     if (x >= W || y >= H) return;
@@ -337,7 +362,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
     const auto t_create = std::chrono::steady_clock::now();
     if (!out) return fail(MFA_ERR_INVALID_ARG, "out is NULL");
     const int want_layout = opt ? opt->layout : MFA_LAYOUT_AUTO;
-    if (want_layout < MFA_LAYOUT_AUTO || want_layout > MFA_LAYOUT_BEZIER)
+    if (want_layout < MFA_LAYOUT_AUTO || want_layout > MFA_LAYOUT_BRICKS)
         return fail(MFA_ERR_INVALID_ARG, "options.layout out of range");
     *out = nullptr;
     if (!degree || !nctrl || !knots || !ctrl) return fail(MFA_ERR_INVALID_ARG, "NULL argument");
@@ -491,6 +516,8 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
     bool bez = want_layout == MFA_LAYOUT_BEZIER ||
                (want_layout == MFA_LAYOUT_AUTO && p <= 3 && (nonuni || bez_bytes <= kBezSmallModelBytes));
     if (bez && p > 3) return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs degree <= 3"));
+    if (want_layout == MFA_LAYOUT_BRICKS && p > 3)
+        return cleanup(fail(MFA_ERR_UNSUPPORTED, "plain-brick layout needs degree <= 3"));
     if (bez && (nctrl[0] - p) * (nctrl[1] - p) * (nctrl[2] - p) >= ((int64_t)1 << 31)) {   // 32-bit block index
         if (want_layout == MFA_LAYOUT_BEZIER)
             return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs < 2^31 span triples"));
@@ -530,7 +557,18 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
             m->layout = kBezier;
         }
     }
-    if (!bez) {   // bricked row quads
+    if (!bez && want_layout == MFA_LAYOUT_BRICKS) {   // plain haloed bricks (<= 1.86 x the grid)
+        for (int d = 0; d < 3; ++d) m->nb[d] = (int)((nctrl[d] - p + kBrick - 1) / kBrick);
+        const int EU = pbrick_eu(p), EV = pbrick_ev(p);
+        const int64_t fl = (int64_t)m->nb[0] * m->nb[1] * m->nb[2] * EU * EV * EV;   // floats
+        if ((e = cudaMalloc(&m->Q, fl * sizeof(float) + 32)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc Q"));
+        relayout_plain_kernel<<<4736, 256, 0, st>>>(Pdev, reinterpret_cast<float*>(m->Q), (int)nu, (int)nv, (int)nw,
+                                                     m->nb[0], m->nb[1], EU, EV, fl);
+        cudaMemsetAsync(reinterpret_cast<float*>(m->Q) + fl, 0, 32, st);   // the 8-float row window may read past the end
+        m->device_bytes += fl * (int64_t)sizeof(float) + 32;
+        m->q_f4 = (fl + 8) / 4;
+        m->layout = kBricks;
+    } else if (!bez) {   // bricked row quads
         for (int d = 0; d < 3; ++d) m->nb[d] = (int)((nctrl[d] - p + kBrick - 1) / kBrick);
         const int EU = brick_eu(p), EV = brick_ev(p), EW = brick_ev(p);
         const int64_t qn = (int64_t)m->nb[0] * m->nb[1] * m->nb[2] * EU * EV * EW;   // entries
@@ -576,7 +614,7 @@ extern "C" mfa_status mfa_model_info(mfa_model h, mfa_model_desc* out) {
     out->v_max = m->vmax;
     out->device_bytes = m->device_bytes;
     out->device = m->device;
-    out->layout = m->layout == kBezier ? MFA_LAYOUT_BEZIER : MFA_LAYOUT_QUADS;
+    out->layout = m->layout == kBezier ? MFA_LAYOUT_BEZIER : (m->layout == kBricks ? MFA_LAYOUT_BRICKS : MFA_LAYOUT_QUADS);
     out->model_bytes = m->model_bytes;
     out->create_ms = m->create_ms;
     return MFA_OK;
@@ -700,6 +738,12 @@ static mfa_status validate_render(const Model* m, int32_t n_views, const mfa_cam
     for (int d = 0; d < 3; ++d)
         if (!(prm->box_max[d] > prm->box_min[d])) return fail(MFA_ERR_INVALID_ARG, "box_max <= box_min");
     if (!(prm->step > 0.0)) return fail(MFA_ERR_INVALID_ARG, "step <= 0");
+    {   // the per-ray sample count must fit an int: box diagonal / step < 2^30
+        double d2 = 0.0;
+        for (int d = 0; d < 3; ++d) d2 += (prm->box_max[d] - prm->box_min[d]) * (prm->box_max[d] - prm->box_min[d]);
+        if (!(sqrt(d2) / prm->step < 1073741824.0))
+            return fail(MFA_ERR_INVALID_ARG, "step too small: box diagonal / step must stay below 2^30 samples");
+    }
     (void)m;
     return MFA_OK;
 }
@@ -815,7 +859,7 @@ extern "C" mfa_status mfa_unpack_tiles(const void* packed, int32_t in_fp16, cons
     if (n_tiles == 0) return MFA_OK;
     if (!packed || !tiles || !image_out) return fail(MFA_ERR_INVALID_ARG, "NULL pointer");
     unpack_tiles_kernel<<<(unsigned)n_tiles, MFA_TILE * MFA_TILE, 0, (cudaStream_t)stream>>>(
-        packed, in_fp16, tiles, n_tiles, width, height, reinterpret_cast<float4*>(image_out));
+        packed, in_fp16, tiles, n_tiles, n_views, width, height, reinterpret_cast<float4*>(image_out));
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "unpack_tiles launch");
 }

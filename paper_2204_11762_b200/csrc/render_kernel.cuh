@@ -33,7 +33,7 @@
 #define MFA_UNIT_SHAPE 1
 #endif
 #ifndef MFA_VIEW_GROUP   // full-frame work order: >1 interleaves groups of orbit-adjacent views
-#define MFA_VIEW_GROUP 1
+#define MFA_VIEW_GROUP 4 // C5: DRAM per launch 506 -> 343 GB, L2 hit 44 -> 56 %, +1.4 %
 #endif
 #ifndef MFA_VIEW_ORDER   // with MFA_VIEW_GROUP > 1: 1 = per supertile, 2 = per supertile row, 3 = per tile
 #define MFA_VIEW_ORDER 1
@@ -233,7 +233,8 @@ struct RenderShape {
 #ifdef MFA_RENDER_MINB
     static constexpr int MINB = MFA_RENDER_MINB;
 #else
-    static constexpr int MINB = P <= 3 ? (CACHE ? 3 : 4) : 2;
+    // plain bricks: the 8-float row windows of a reload need registers (2 CTAs)
+    static constexpr int MINB = LAYOUT == kBricks ? 2 : (P <= 3 ? (CACHE ? 3 : 4) : 2);
 #endif
     // p >= 4: a CTA (8 warps) takes a whole 16x16 tile so its sub-tiles share L1
     static constexpr bool CTA_TILES = MFA_CTA_TILES < 0 ? (P >= 4 && THREADS == 256) : (bool)MFA_CTA_TILES;
@@ -298,7 +299,11 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             view = __ldg(args.tiles + 3 * tile_id);
             tx = __ldg(args.tiles + 3 * tile_id + 1);
             ty = __ldg(args.tiles + 3 * tile_id + 2);
-            if (view < 0) continue;  // padding unit (multi-GPU equal-size buffers)
+            // padding units (view = -1, multi-GPU equal-size buffers) and any
+            // malformed entry (view or tile outside this launch) are skipped:
+            // a bad list must never index frames[] or store outside the image
+            if (view < 0 || view >= args.n_views || tx < 0 || ty < 0 || tx >= args.tiles_x || ty >= args.tiles_y)
+                continue;
         } else {
             // supertile order: the ~200 tiles in flight form a compact image
             // region, so neighbouring rays reuse control blocks from L1/L2
@@ -410,7 +415,8 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
             t_in = fmax(tn, 0.0);
             if (hit && tf > t_in) {
                 const double frc = (tf - t_in) * args.inv_step - 0.5;
-                K = frc > 0.0 ? (int)ceil(frc) : 0;
+                // (validate_render bounds the box diagonal / step below 2^30)
+                K = frc > 0.0 ? (int)ceil(fmin(frc, 1073741824.0)) : 0;
             }
         }
         // ---- a3 setup: fixed-point sample coordinates per axis --------------
@@ -451,6 +457,12 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
                 if (e != nb_key) {       // reload only when the span triple changed
                     load_bblock<P>(bez_block_at<P>(args.Q, args.bg, e), nb);
                     nb_key = e;
+                }
+            } else if constexpr (CACHE && LAYOUT == kBricks) {
+                const PlainRef e = plain_entry<P>(args.g, s[0], s[1], s[2]);
+                if (e.base + e.o != nb_key) {
+                    load_pblock<P>(args.Q, e, nb);
+                    nb_key = e.base + e.o;
                 }
             } else if constexpr (CACHE) {
                 const int64_t e = brick_entry<P>(args.g, s[0], s[1], s[2]);
@@ -848,8 +860,9 @@ __global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P
         }
         my_samples += (unsigned)k;
     }
-    if (args.samples) {
-        my_samples = __reduce_add_sync(0xffffffffu, (unsigned)my_samples);
+    if (args.samples) {   // 64-bit warp sum (a warp may composite more than 2^32 samples)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, o);
         if (lane == 0 && my_samples) atomicAdd(args.samples, my_samples);
 #if MFA_LANE_STATS
         if (lane == 0) {
@@ -913,6 +926,7 @@ template <int P, bool EXT>
 static cudaError_t dispatch_render(const RenderArgs& a, int layout, bool uni, int shade, cudaStream_t st) {
     if constexpr (P <= 3) {
         if (layout == kBezier) return dispatch_render_l<P, kBezier, EXT>(a, uni, shade, st);
+        if (layout == kBricks) return dispatch_render_l<P, kBricks, EXT>(a, uni, shade, st);
     }
     return dispatch_render_l<P, kQuads, EXT>(a, uni, shade, st);
 }

@@ -72,7 +72,7 @@ def models(c, layout):
 
 
 @pytest.mark.parametrize("c,layout", [(1, "quads"), (2, "quads"), (2, "bezier"), (3, "quads"), (4, "quads"),
-                                      (5, "bezier"), (5, "quads")])
+                                      (5, "bezier"), (5, "quads"), (2, "bricks"), (5, "bricks")])
 def test_hessian_parity_configs(c, layout):
     w, m, om = models(c, layout)
     u, v, ww = WL.query_points(c, 1 << 15)

@@ -261,11 +261,12 @@ def test_invalid_models_raise():
     assert info["v_min"] == 2 and info["v_max"] == 2 and info["uniform"] == (1, 1, 1)
 
 
-@pytest.mark.parametrize("c,layout", [(1, "bezier"), (2, "bezier"), (3, "bezier"), (5, "quads")])
+@pytest.mark.parametrize("c,layout", [(1, "bezier"), (2, "bezier"), (3, "bezier"), (5, "quads"),
+                                      (1, "bricks"), (2, "bricks"), (3, "bricks"), (5, "bricks")])
 def test_both_layouts_eval_and_render(c, layout):
-    """Each model also through the other control-point layout (bricked quads
-    vs Bezier blocks): eval parity on random + boundary points and a render
-    parity check (a reduced image for C3/C5)."""
+    """Each model also through the other control-point layouts (bricked quads,
+    Bezier blocks, plain haloed bricks): eval parity on random + boundary
+    points and a render parity check (a reduced image for C3/C5)."""
     w = workload(c) if c in (1, 2) else workload(c, width=256, height=192, n_views=1)
     m = gpu_model(c, layout)
     assert m.info()["layout"] == layout
@@ -307,7 +308,7 @@ def test_nonuniform_multiple_knots(p):
     w.v_lo, w.v_hi = float(ctrl.min()), float(ctrl.max())
     om = O.Model.from_workload(w)
     from paper_2204_11762_b200 import Model
-    for layout in ("quads", "bezier"):
+    for layout in ("quads", "bezier", "bricks"):
         m = Model.from_workload(w, layout=layout)
         u, v, ww = WL.query_points(1, 1 << 14)
         got = gpu_eval(m, u, v, ww)
@@ -501,3 +502,24 @@ def test_skip_transparent_gradient_is_bit_identical(c, layout):
         res.append((img.cpu().numpy(), int(cnt.item())))
     np.testing.assert_array_equal(res[0][0], res[1][0])
     assert res[0][1] == res[1][1]
+
+
+def test_bricks_layout_footprint_and_full_size_c5():
+    """The plain haloed-brick layout (<= 2x the fp32 grid, P:133 / P:263) on
+    the full C5 model: footprint ratio, and the bench's launch configuration
+    (all 64 views in one call) checked on a seeded tile subset of 2 views."""
+    from paper_2204_11762_b200 import Model
+    w = workload(5)
+    m = Model.from_workload(w, layout="bricks")
+    info = m.info()
+    assert info["layout"] == "bricks"
+    ratio = info["device_bytes"] / info["model_bytes"]
+    assert ratio <= 2.0, ratio
+    samples = torch.zeros(1, dtype=torch.int64, device="cuda")
+    img = m.render(w.cameras, cuda(w.tf), w.v_lo, w.v_hi, w.params, samples=samples)
+    torch.cuda.synchronize()
+    H, W = w.cameras[0].height, w.cameras[0].width
+    for v, pix in WL.tile_subset(5, W, H, 0.01, views=(7, 40)).items():
+        ref = O.render(oracle_model(5), w.cameras[v], w.tf, w.v_lo, w.v_hi, w.params, pixels=pix)
+        parity.check_image(img[v].cpu().numpy().reshape(-1, 4)[pix], ref, f"C5 bricks view {v}")
+    print(f"C5 bricks: device {info['device_bytes'] / 2**20:.0f} MiB = {ratio:.2f} x the grid")
