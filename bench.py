@@ -143,74 +143,101 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_oracle_sample(w, seconds: float, cfg_idx: int, nthreads=None):
-    """Oracle (as it stands) on a bounded seeded tile sample of view 0; returns
-    (samples/s, cores, description).  Calibrated on a small sample first."""
-    import oracle as O
-    from paper_2204_11762_b200 import workloads as WL
-    om = O.Model.from_workload(w)
-    cam = w.cameras[0]
-    cores = nthreads or O.ncores()
-    frac = 0.002
-    t0 = time.perf_counter()
-    pix = WL.tile_subset(cfg_idx, cam.width, cam.height, frac)[0]
-    r = O.render(om, cam, w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
-    dt = max(time.perf_counter() - t0, 1e-3)
-    frac = min(1.0, frac * max(1.0, seconds / dt))
-    for _ in range(3):   # the calibration sample is small; re-size until the run lands near `seconds`
-        pix = WL.tile_subset(cfg_idx, cam.width, cam.height, frac)[0]
+def cpu_model_name() -> str:
+    """The host CPU model (lscpu's "Model name", read from /proc/cpuinfo)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.lower().startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+class OracleSampler:
+    """The ONE oracle sampling scheme of both CPU legs (the cpu_baseline of
+    the GPU line and the --impl reference arm): a seeded fraction of the
+    16x16 tiles of one view per call (workloads.tile_subset), views rotating
+    over 4 evenly spaced views of the batch, the fraction calibrated once so
+    a call takes about `seconds` on the host cores (all of them)."""
+
+    def __init__(self, w, c, seconds):
+        import oracle as O
+        from paper_2204_11762_b200 import workloads as WL
+        self.O, self.WL, self.w, self.c = O, WL, w, c
+        self.om = O.Model.from_workload(w)
+        self.cores = O.ncores()
+        V = len(w.cameras)
+        self.views = [(i * V) // 4 for i in range(4)]
+        cam = w.cameras[0]
+        frac = 0.002
+        for _ in range(4):   # calibrate on view 0: grow the fraction until a call lands near `seconds`
+            n, dt = self._run(0, frac)
+            if dt >= 0.6 * seconds or frac >= 1.0:
+                break
+            frac = min(1.0, frac * seconds / max(dt, 1e-3))
+        self.frac = frac
+        tx, ty = (cam.width + 15) // 16, (cam.height + 15) // 16
+        self.tiles = max(1, int(round(frac * tx * ty)))
+
+    def _run(self, view, frac):
+        cam = self.w.cameras[view]
+        pix = self.WL.tile_subset(self.c, cam.width, cam.height, frac, views=(view,))[view]
         t0 = time.perf_counter()
-        r = O.render(om, cam, w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
-        dt = time.perf_counter() - t0
-        if dt >= 0.6 * seconds or frac >= 1.0:
-            break
-        frac = min(1.0, frac * seconds / max(dt, 1e-3))
-    ns = int(r["count"].sum())
-    desc = (f"{len(pix)} pixels ({frac * 100:.2f}% of the 16x16 tiles, seeded) of view 0 of {w.name}; "
-            f"{ns} composited samples in {dt:.2f} s")
-    return ns / dt, cores, desc, dt
+        r = self.O.render(self.om, cam, self.w.tf, self.w.v_lo, self.w.v_hi, self.w.params, pixels=pix,
+                          nthreads=self.cores)
+        return int(r["count"].sum()), time.perf_counter() - t0
+
+    def call(self, i):
+        """Call i: (composited samples, seconds) on view views[i % 4]."""
+        return self._run(self.views[i % 4], self.frac)
+
+    def describe(self, calls):
+        return (f"per call a seeded {self.frac * 100:.3f}% of the 16x16 tiles ({self.tiles} tiles) of one view of "
+                f"{self.w.name}, views {self.views} in rotation, {calls} calls; fp64 oracle on {self.cores} threads "
+                f"({cpu_model_name()})")
+
+
+def cpu_oracle_sample(w, seconds: float, cfg_idx: int):
+    """cpu_baseline: 4 sampler calls (one per rotation view), ~seconds in total."""
+    smp = OracleSampler(w, cfg_idx, seconds / 4)
+    ns, dt = 0, 0.0
+    for i in range(4):
+        n, t = smp.call(i)
+        ns += n
+        dt += t
+    return ns / dt, smp.cores, smp.describe(4) + f"; {ns} composited samples in {dt:.2f} s", dt
 
 
 def run_reference(args):
-    """Reference arm: the fp64 oracle on host cores, each step a bounded sample."""
+    """Reference arm: the fp64 oracle on host cores, each step one call of the
+    same sampler as the cpu_baseline leg."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import oracle as O
     from paper_2204_11762_b200 import workloads as WL
     c = int(args.workload[1:])
     kw = {"n_views": args.views} if args.views else {}
     w = WL.make_config(c, **kw)
-    om = O.Model.from_workload(w)
-    cores = O.ncores()
-    cam = w.cameras[0]
-    # size each step to ~ (120 s / (steps + warmup)) of CPU work, at least 1 tile
     budget = min(20.0, 120.0 / max(1, args.steps + args.warmup))
-    frac = 0.001
-    t0 = time.perf_counter()
-    pix = WL.tile_subset(c, cam.width, cam.height, frac)[0]
-    O.render(om, cam, w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
-    dt = max(time.perf_counter() - t0, 1e-3)
-    frac = min(1.0, frac * max(1.0, budget / dt))
-    tot_s = 0
-    tot_t = 0.0
+    smp = OracleSampler(w, c, budget)
+    tot_s, tot_t = 0, 0.0
     for i in range(args.warmup + args.steps):
-        v = i % len(w.cameras)
-        pix = WL.tile_subset(c, cam.width, cam.height, frac, views=(v,))[v]
-        t0 = time.perf_counter()
-        r = O.render(om, w.cameras[v], w.tf, w.v_lo, w.v_hi, w.params, pixels=pix, nthreads=cores)
-        dt = time.perf_counter() - t0
+        n, dt = smp.call(i)
         if i >= args.warmup:
-            tot_s += int(r["count"].sum())
+            tot_s += n
             tot_t += dt
     val = tot_s / tot_t
-    desc = f"per step a seeded {frac * 100:.3f}% tile sample of one view of {w.name}"
+    desc = smp.describe(args.steps)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator)", "config": {"workload": w.name},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": smp.cores, "kind": "oracle", "sample": desc,
+                         "cpu": cpu_model_name()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
     return 0
@@ -437,7 +464,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, desc, _ = cpu_oracle_sample(w, args.cpu_seconds, c)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc, "cpu": cpu_model_name()}
 
     if rank == 0:
         res = {

@@ -133,24 +133,71 @@ __global__ void fit_normal_kernel(const int* __restrict__ f, const double* __res
 }
 
 // ---- K_fc: banded Cholesky A = L L^T, L[i][k] = L(i, i - k) -----------------
-// status[0] = -1 on success, else the first control point whose pivot failed
-__global__ void fit_cholesky_kernel(const double* __restrict__ Ab, int p, int n, double* __restrict__ L,
-                                    int* __restrict__ status) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    status[0] = -1;
+// one thread per axis (blockIdx.x = axis: the three factorisations run
+// concurrently); the last P rows of L stay in a register window and each row
+// takes one reciprocal and one square root, so a row costs a few hundred
+// cycles of dependent fp64 latency instead of a chain of global loads.
+// status[axis] = -1 on success, else the first control point whose pivot failed
+struct CholArgs {
+    const double* Ab[3];
+    double* L[3];
+    int n[3];
+    int* status;
+};
+
+template <int P>
+__global__ void fit_cholesky_kernel(const CholArgs a) {
+    if (threadIdx.x != 0) return;
+    const int ax = blockIdx.x;
+    const double* __restrict__ Ab = a.Ab[ax];
+    double* __restrict__ L = a.L[ax];
+    const int n = a.n[ax];
+    // win[q][k] = L(i-1-q, i-1-q-k) for the previous P rows (q = 0 is row i-1);
+    // inv[q] = 1 / L(i-1-q, i-1-q)
+    double win[P][P + 1], inv[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        inv[q] = 0.0;
+#pragma unroll
+        for (int k = 0; k <= P; ++k) win[q][k] = 0.0;
+    }
+    a.status[ax] = -1;
     for (int i = 0; i < n; ++i) {
-        for (int c = max(0, i - p); c < i; ++c) {
-            double sum = Ab[(size_t)i * (p + 1) + (i - c)];
-            for (int l = max(0, i - p); l < c; ++l) sum -= L[(size_t)i * (p + 1) + (i - l)] * L[(size_t)c * (p + 1) + (c - l)];
-            L[(size_t)i * (p + 1) + (i - c)] = sum / L[(size_t)c * (p + 1)];
+        double row[P + 1];   // row[k] = L(i, i - k)
+        // off-diagonal entries c = i - k, k = P .. 1 (ascending c)
+#pragma unroll
+        for (int k = P; k >= 1; --k) {
+            row[k] = 0.0;
+            if (i - k < 0) continue;
+            double sum = Ab[(size_t)i * (P + 1) + k];
+            const int q = k - 1;   // row c = i - k is window entry q
+            // l = c - kk .. for l in [max(0, i - P), c - 1]: L(i, l) = row[i - l], L(c, l) = win[q][c - l]
+#pragma unroll
+            for (int j = P; j > k; --j) {   // l = i - j (ascending l), needs l >= 0 and l < c
+                if (i - j >= 0) sum -= row[j] * win[q][j - k];
+            }
+            row[k] = sum * inv[q];
         }
-        double sum = Ab[(size_t)i * (p + 1)];
-        for (int l = max(0, i - p); l < i; ++l) sum -= L[(size_t)i * (p + 1) + (i - l)] * L[(size_t)i * (p + 1) + (i - l)];
-        if (!(sum > 1e-14 * fmax(1.0, Ab[(size_t)i * (p + 1)]))) {
-            status[0] = i;
+        double d = Ab[(size_t)i * (P + 1)];
+#pragma unroll
+        for (int k = P; k >= 1; --k)
+            if (i - k >= 0) d -= row[k] * row[k];
+        if (!(d > 1e-14 * fmax(1.0, Ab[(size_t)i * (P + 1)]))) {
+            a.status[ax] = i;
             return;
         }
-        L[(size_t)i * (p + 1)] = sqrt(sum);
+        row[0] = sqrt(d);
+#pragma unroll
+        for (int k = 0; k <= P; ++k) L[(size_t)i * (P + 1) + k] = row[k];
+#pragma unroll
+        for (int q = P - 1; q > 0; --q) {
+            inv[q] = inv[q - 1];
+#pragma unroll
+            for (int k = 0; k <= P; ++k) win[q][k] = win[q - 1][k];
+        }
+        inv[0] = 1.0 / row[0];
+#pragma unroll
+        for (int k = 0; k <= P; ++k) win[0][k] = row[k];
     }
 }
 
@@ -325,43 +372,68 @@ struct AxisDevMem {
     }
 };
 
-// the operator of axis d on the device: samples, normal matrix, Cholesky,
-// N^+ (K_fs, K_fn, K_fc, K_fm); synchronises once to report a singular fit
-static mfa_status build_axis_dev(int d, int m, int n, int p, const double* U_host, AxisDevMem& D, cudaStream_t st) {
+// the operators of the three axes on the device: samples, normal matrix,
+// Cholesky (one launch for all axes), N^+ (K_fs, K_fn, K_fc, K_fm);
+// synchronises once to report a singular fit
+static mfa_status build_axes_dev(const int m[3], const int n[3], int p, const double* const U_host[3],
+                                 AxisDevMem (&D)[3], cudaStream_t st) {
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    const size_t nu = sizeof(double) * (n + p + 1), nf = sizeof(int) * m, nb = sizeof(double) * (size_t)m * (p + 1),
-                 nab = sizeof(double) * (size_t)n * (p + 1), nm = sizeof(double) * (size_t)n * m;
-    cudaError_t e = cudaMallocAsync(&D.mem, up(nu) + up(nf) + up(nb) + 2 * up(nab) + up(nm) + 256, st);
-    if (e != cudaSuccess) return cuda_fail(e, "fit tables");
-    char* b = (char*)D.mem;
-    double* U = (double*)b;
-    int* f = (int*)(b + up(nu));
-    double* B = (double*)(b + up(nu) + up(nf));
-    double* Ab = (double*)(b + up(nu) + up(nf) + up(nb));
-    double* L = (double*)(b + up(nu) + up(nf) + up(nb) + up(nab));
-    double* M = (double*)(b + up(nu) + up(nf) + up(nb) + 2 * up(nab));
-    int* status = (int*)(b + up(nu) + up(nf) + up(nb) + 2 * up(nab) + up(nm));
-    cudaMemcpyAsync(U, U_host, nu, cudaMemcpyHostToDevice, st);
-    fit_samples_kernel<<<(m + 127) / 128, 128, 0, st>>>(U, p, n, m, f, B);
-    fit_normal_kernel<<<(n + 127) / 128, 128, 0, st>>>(f, B, p, n, m, Ab);
-    fit_cholesky_kernel<<<1, 32, 0, st>>>(Ab, p, n, L, status);
-    const unsigned g = (unsigned)((m + 127) / 128);
-    switch (p) {
-        case 1: fit_pinv_kernel<1><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
-        case 2: fit_pinv_kernel<2><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
-        case 3: fit_pinv_kernel<3><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
-        case 4: fit_pinv_kernel<4><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
-        default: fit_pinv_kernel<5><<<g, 128, 0, st>>>(f, B, L, n, m, M); break;
+    CholArgs ca;
+    int* status = nullptr;
+    cudaError_t e;
+    int* f[3];
+    double* B[3];
+    double* M[3];
+    for (int d = 0; d < 3; ++d) {
+        const size_t nu = sizeof(double) * (n[d] + p + 1), nf = sizeof(int) * m[d],
+                     nb = sizeof(double) * (size_t)m[d] * (p + 1), nab = sizeof(double) * (size_t)n[d] * (p + 1),
+                     nm = sizeof(double) * (size_t)n[d] * m[d];
+        if ((e = cudaMallocAsync(&D[d].mem, up(nu) + up(nf) + up(nb) + 2 * up(nab) + up(nm) + 256, st)) != cudaSuccess)
+            return cuda_fail(e, "fit tables");
+        char* b = (char*)D[d].mem;
+        double* U = (double*)b;
+        f[d] = (int*)(b + up(nu));
+        B[d] = (double*)(b + up(nu) + up(nf));
+        double* Ab = (double*)(b + up(nu) + up(nf) + up(nb));
+        double* L = (double*)(b + up(nu) + up(nf) + up(nb) + up(nab));
+        M[d] = (double*)(b + up(nu) + up(nf) + up(nb) + 2 * up(nab));
+        if (d == 0) status = (int*)(b + up(nu) + up(nf) + up(nb) + 2 * up(nab) + up(nm));
+        cudaMemcpyAsync(U, U_host[d], nu, cudaMemcpyHostToDevice, st);
+        fit_samples_kernel<<<(m[d] + 127) / 128, 128, 0, st>>>(U, p, n[d], m[d], f[d], B[d]);
+        fit_normal_kernel<<<(n[d] + 127) / 128, 128, 0, st>>>(f[d], B[d], p, n[d], m[d], Ab);
+        ca.Ab[d] = Ab;
+        ca.L[d] = L;
+        ca.n[d] = n[d];
     }
-    int hs = -1;
-    cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, st);
+    ca.status = status;
+    switch (p) {
+        case 1: fit_cholesky_kernel<1><<<3, 32, 0, st>>>(ca); break;
+        case 2: fit_cholesky_kernel<2><<<3, 32, 0, st>>>(ca); break;
+        case 3: fit_cholesky_kernel<3><<<3, 32, 0, st>>>(ca); break;
+        case 4: fit_cholesky_kernel<4><<<3, 32, 0, st>>>(ca); break;
+        default: fit_cholesky_kernel<5><<<3, 32, 0, st>>>(ca); break;
+    }
+    for (int d = 0; d < 3; ++d) {
+        const unsigned g = (unsigned)((m[d] + 127) / 128);
+        switch (p) {
+            case 1: fit_pinv_kernel<1><<<g, 128, 0, st>>>(f[d], B[d], ca.L[d], n[d], m[d], M[d]); break;
+            case 2: fit_pinv_kernel<2><<<g, 128, 0, st>>>(f[d], B[d], ca.L[d], n[d], m[d], M[d]); break;
+            case 3: fit_pinv_kernel<3><<<g, 128, 0, st>>>(f[d], B[d], ca.L[d], n[d], m[d], M[d]); break;
+            case 4: fit_pinv_kernel<4><<<g, 128, 0, st>>>(f[d], B[d], ca.L[d], n[d], m[d], M[d]); break;
+            default: fit_pinv_kernel<5><<<g, 128, 0, st>>>(f[d], B[d], ca.L[d], n[d], m[d], M[d]); break;
+        }
+    }
+    int hs[3] = {-1, -1, -1};
+    cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "fit operator");
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "fit operator kernels");
-    if (hs >= 0)
-        return fail(MFA_ERR_INVALID_ARG, std::string("fit: normal equations singular on axis ") + "uvw"[d] +
-                                             " at control point " + std::to_string(hs) +
-                                             " (a basis function without samples: too many control points for the grid)");
-    D.d = AxisFitDev{m, n, f, B, M};
+    for (int d = 0; d < 3; ++d) {
+        if (hs[d] >= 0)
+            return fail(MFA_ERR_INVALID_ARG, std::string("fit: normal equations singular on axis ") + "uvw"[d] +
+                                                 " at control point " + std::to_string(hs[d]) +
+                                                 " (a basis function without samples: too many control points for the grid)");
+        D[d].d = AxisFitDev{m[d], n[d], f[d], B[d], M[d]};
+    }
     return MFA_OK;
 }
 
@@ -392,56 +464,64 @@ static unsigned grid_for(int64_t work) {
 
 // ---- K_gemm: C[z][M][N] = A[z][M][K] . op(B)[z][K][N], fp64, row-major -----
 // op(B) = B[K][N] (BT = false) or B^T with B stored [N][K] (BT = true).
-// 64 x 64 tile per 256-thread CTA, each thread a 4 x 4 register tile; k-slabs
-// of 16 staged through shared memory (double-buffered: the next slab's global
-// loads are in flight while the current one is multiplied).  Batch z via
-// blockIdx.z with element strides sa, sb, sc (0 = shared operand).
-constexpr int kGM = 64, kGN = 64, kGK = 16;
+// 128 x 64 tile per 256-thread CTA, each thread an 8 x 4 register tile (32
+// DFMA per 6 shared-memory 16-byte loads); k-slabs of 16 staged through
+// shared memory, double-buffered (the next slab's global loads are in flight
+// while the current one is multiplied).  Batch z via blockIdx.z with element
+// strides sa, sb, sc (0 = shared operand).
+constexpr int kGM = 128, kGN = 64, kGK = 16;
 
 template <bool BT>
 __global__ void __launch_bounds__(256) dgemm_kernel(const double* __restrict__ A, const double* __restrict__ B,
                                                     double* __restrict__ C, int M, int N, int K, int64_t sa,
                                                     int64_t sb, int64_t sc) {
-    __shared__ double As[2][kGK][kGM + 2];   // As[k][m]
-    __shared__ double Bs[2][kGK][kGN + 2];   // Bs[k][n]
+    extern __shared__ __align__(16) double gsm[];             // dynamic: 50 KB (opt-in above 48 KB)
+    double (*As)[kGK][kGM + 2] = reinterpret_cast<double (*)[kGK][kGM + 2]>(gsm);                   // As[b][k][m]
+    double (*Bs)[kGK][kGN + 2] = reinterpret_cast<double (*)[kGK][kGN + 2]>(gsm + 2 * kGK * (kGM + 2));   // Bs[b][k][n]
     const int z = blockIdx.z;
     A += z * sa;
     B += z * sb;
     C += z * sc;
     const int m0 = blockIdx.y * kGM, n0 = blockIdx.x * kGN;
     const int tid = threadIdx.x;
-    const int tm = (tid / 16) * 4, tn = (tid % 16) * 4;
-    double acc[4][4];
+    const int tm = (tid / 16) * 8, tn = (tid % 16) * 4;
+    double acc[8][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    // each thread stages 4 elements of A and 4 of B per slab
-    double ra[4], rb[4];
+    double ra[8], rb[4];
     auto load = [&](int k0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = tid + 256 * q;              // 0..1023
-            // A tile 64 (m) x 16 (k): k fastest in memory (row-major A)
+        for (int q = 0; q < 8; ++q) {   // A tile 128 (m) x 16 (k), k fastest in memory
+            const int e = tid + 256 * q;
             const int am = e / kGK, ak = e % kGK;
             const int gm = m0 + am, gk = k0 + ak;
-            ra[q] = (gm < M && gk < K) ? A[(int64_t)gm * K + gk] : 0.0;
+            ra[q] = (gm < M && gk < K) ? __ldg(A + (int64_t)gm * K + gk) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + 256 * q;
             if (BT) {   // B stored [N][K]: k fastest
                 const int bn = e / kGK, bk = e % kGK;
-                const int gn = n0 + bn, gk2 = k0 + bk;
-                rb[q] = (gn < N && gk2 < K) ? B[(int64_t)gn * K + gk2] : 0.0;
+                const int gn = n0 + bn, gk = k0 + bk;
+                rb[q] = (gn < N && gk < K) ? __ldg(B + (int64_t)gn * K + gk) : 0.0;
             } else {    // B stored [K][N]: n fastest
                 const int bk = e / kGN, bn = e % kGN;
-                const int gn = n0 + bn, gk2 = k0 + bk;
-                rb[q] = (gn < N && gk2 < K) ? B[(int64_t)gk2 * N + gn] : 0.0;
+                const int gn = n0 + bn, gk = k0 + bk;
+                rb[q] = (gn < N && gk < K) ? __ldg(B + (int64_t)gk * N + gn) : 0.0;
             }
         }
     };
     auto stash = [&](int buf) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
             const int e = tid + 256 * q;
             As[buf][e % kGK][e / kGK] = ra[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + 256 * q;
             if (BT) Bs[buf][e % kGK][e / kGK] = rb[q];
             else Bs[buf][e / kGN][e % kGN] = rb[q];
         }
@@ -455,13 +535,21 @@ __global__ void __launch_bounds__(256) dgemm_kernel(const double* __restrict__ A
         if (more) load(k0 + kGK);
 #pragma unroll
         for (int k = 0; k < kGK; ++k) {
-            double a[4], b[4];
+            double a[8], b[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[buf][k][tm + i];
+            for (int i = 0; i < 8; i += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(&As[buf][k][tm + i]);
+                a[i] = t.x;
+                a[i + 1] = t.y;
+            }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[buf][k][tn + j];
+            for (int j = 0; j < 4; j += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(&Bs[buf][k][tn + j]);
+                b[j] = t.x;
+                b[j + 1] = t.y;
+            }
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
@@ -472,7 +560,7 @@ __global__ void __launch_bounds__(256) dgemm_kernel(const double* __restrict__ A
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {
         const int gm = m0 + tm + i;
         if (gm >= M) continue;
 #pragma unroll
@@ -486,8 +574,14 @@ __global__ void __launch_bounds__(256) dgemm_kernel(const double* __restrict__ A
 static cudaError_t dgemm(bool bt, const double* A, const double* B, double* C, int M, int N, int K, int batch,
                          int64_t sa, int64_t sb, int64_t sc, cudaStream_t st) {
     const dim3 grid((unsigned)((N + kGN - 1) / kGN), (unsigned)((M + kGM - 1) / kGM), (unsigned)batch);
-    if (bt) dgemm_kernel<true><<<grid, 256, 0, st>>>(A, B, C, M, N, K, sa, sb, sc);
-    else dgemm_kernel<false><<<grid, 256, 0, st>>>(A, B, C, M, N, K, sa, sb, sc);
+    const int smem = (int)(sizeof(double) * 2 * kGK * ((kGM + 2) + (kGN + 2)));
+    if (bt) {
+        cudaFuncSetAttribute(dgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        dgemm_kernel<true><<<grid, 256, smem, st>>>(A, B, C, M, N, K, sa, sb, sc);
+    } else {
+        cudaFuncSetAttribute(dgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        dgemm_kernel<false><<<grid, 256, smem, st>>>(A, B, C, M, N, K, sa, sb, sc);
+    }
     return cudaGetLastError();
 }
 
@@ -591,8 +685,10 @@ extern "C" mfa_status mfa_fit_grid(const int64_t dims[3], const float* values, i
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return done(cuda_fail(e, "fit range"));
         if (rb[2]) return done(fail(MFA_ERR_DOMAIN, std::to_string(rb[2]) + " non-finite grid values"));
     }
-    for (int d = 0; d < 3; ++d)
-        if ((s = build_axis_dev(d, (int)dims[d], (int)nctrl[d], p, knots[d], D[d], st)) != MFA_OK) return done(s);
+    {
+        const int mm[3] = {(int)dims[0], (int)dims[1], (int)dims[2]}, nn[3] = {(int)nctrl[0], (int)nctrl[1], (int)nctrl[2]};
+        if ((s = build_axes_dev(mm, nn, p, knots, D, st)) != MFA_OK) return done(s);
+    }
     const int64_t mu = dims[0], mv = dims[1], mw = dims[2], nu = nctrl[0], nv = nctrl[1], nw = nctrl[2];
     if ((e = cudaMallocAsync(&W.Q64, sizeof(double) * mw * mv * mu, st)) != cudaSuccess) return done(cuda_fail(e, "fit scratch"));
     f32_to_f64_kernel<<<grid_for(mw * mv * mu), 128, 0, st>>>(values, W.Q64, mw * mv * mu);
@@ -675,7 +771,11 @@ extern "C" mfa_status mfa_encode_grid(const int64_t dims[3], const float* values
         for (int d = 0; d < 3; ++d) {
             n[d] = (int64_t)U[d].size() - p - 1;
             D[d].release(st);
-            if ((s = build_axis_dev(d, (int)dims[d], (int)n[d], p, U[d].data(), D[d], st)) != MFA_OK) return done(s);
+        }
+        {
+            const int mm[3] = {(int)dims[0], (int)dims[1], (int)dims[2]}, nn[3] = {(int)n[0], (int)n[1], (int)n[2]};
+            const double* const uu[3] = {U[0].data(), U[1].data(), U[2].data()};
+            if ((s = build_axes_dev(mm, nn, p, uu, D, st)) != MFA_OK) return done(s);
         }
         const AxisFitDev ax[3] = {D[0].d, D[1].d, D[2].d};
         if ((s = fit_all(W.Q64, ax, W.T1, W.T2, ctrl_out, W.C64, st)) != MFA_OK) return done(s);

@@ -56,6 +56,19 @@ def test_fit_square_interpolates_and_errors():
     bad[5] = 2.0
     with pytest.raises(MfaError, match="KNOTS"):
         fit_grid(cuda(q), p, [bad] + knots[1:])
+    # a knot layout leaving a basis function without samples: the device
+    # Cholesky reports the singular pivot (axis and control point)
+    sparse = np.concatenate([np.zeros(p + 1), [0.05, 0.06, 0.07], np.ones(p + 1)])   # 7 ctrl, 9 samples
+    with pytest.raises(MfaError, match="singular on axis u"):
+        fit_grid(cuda(q), p, [sparse] + knots[1:])
+    # non-finite input values: MFA_ERR_DOMAIN before any fit (fit and encoder)
+    from paper_2204_11762_b200 import encode_grid
+    qn = q.copy()
+    qn[3, 2, 1] = np.nan
+    with pytest.raises(MfaError, match="DOMAIN"):
+        fit_grid(cuda(qn), p, knots)
+    with pytest.raises(MfaError, match="DOMAIN"):
+        encode_grid(cuda(qn), p, (4, 4, 4), 1e-3, 2, dims)
 
 
 @pytest.mark.parametrize("kind,p,e_max", [("gb", 2, 0.01), ("gb", 3, 0.003), ("ml", 2, 0.05)])

@@ -523,3 +523,26 @@ def test_bricks_layout_footprint_and_full_size_c5():
         ref = O.render(oracle_model(5), w.cameras[v], w.tf, w.v_lo, w.v_hi, w.params, pixels=pix)
         parity.check_image(img[v].cpu().numpy().reshape(-1, 4)[pix], ref, f"C5 bricks view {v}")
     print(f"C5 bricks: device {info['device_bytes'] / 2**20:.0f} MiB = {ratio:.2f} x the grid")
+
+
+def test_malformed_tile_entries_are_skipped():
+    """Tile entries outside the call's views or the image (view >= n_views,
+    negative or too-large tile coordinates) are skipped by the render and
+    unpack kernels: no store outside the image, valid tiles unaffected."""
+    from paper_2204_11762_b200 import dist as D, unpack_tiles
+    w = workload(2, width=100, height=75, n_views=2)
+    m = gpu_model(2)
+    tf = cuda(w.tf)
+    full = m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params)
+    good = D.all_units(2, 100, 75)
+    bad = np.array([[2, 0, 0], [7, 1, 1], [0, -1, 0], [1, 0, -3], [0, 7, 0], [1, 0, 5], [-1, 0, 0]], np.int32)
+    tl = np.ascontiguousarray(np.concatenate([good[:5], bad, good[5:]]), dtype=np.int32)
+    guard = torch.full((4, 75, 100, 4), -7.0, device="cuda")   # 2 extra views past the call's 2
+    m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=cuda(tl), out=guard, scatter=True)
+    packed = m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=cuda(tl))
+    img = torch.full((4, 75, 100, 4), -7.0, device="cuda")
+    unpack_tiles(packed, cuda(tl), 2, 100, 75, out=img)
+    torch.cuda.synchronize()
+    for out in (guard, img):
+        assert torch.equal(out[:2], full)
+        assert (out[2:] == -7.0).all()
