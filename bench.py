@@ -60,6 +60,9 @@ def parse():
                     help="control-point layout (default: the library's choice)")
     ap.add_argument("--assign", default="auto", choices=["auto", "views", "rows", "diagonal"],
                     help="N > 1: how (view, tile) units are dealt to ranks (dist.assign_units)")
+    ap.add_argument("--all-configs", action="store_true",
+                    help="one device-timed JSON line per BASELINE.json config (C1..C5), same fields as the main "
+                         "line's render part (no e2e / CPU legs); for the results table, not the driver's line")
     ap.add_argument("--emulate", type=int, default=0, metavar="G",
                     help="one GPU: render each of G ranks' unit lists alone (every assignment mode) and "
                          "report the projected G-GPU time = the slowest rank's")
@@ -730,6 +733,67 @@ def shared_host_image(V, H, W, el, rank, world):
     return t, cleanup
 
 
+def run_all_configs(args):
+    """One device-timed line per config C1..C5 (the main line's render
+    measurement: W warm-up launches, K timed with CUDA events on the launch
+    stream, composited samples counted on the device, clocks sampled)."""
+    import torch
+
+    from paper_2204_11762_b200 import Model, roofline as RL, workloads as WL
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+    for c in (1, 2, 3, 4, 5):
+        w = WL.make_config(c)
+        m = Model.from_workload(w, layout=args.layout)
+        info = m.info()
+        tf = torch.from_numpy(w.tf).cuda()
+        V = len(w.cameras)
+        W, H = w.cameras[0].width, w.cameras[0].height
+        img = torch.empty((V, H, W, 4), device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        # small frames: K launches per timed step so each step lasts >= ~20 ms
+        reps = max(1, int(round(0.02 / max(1e-6, 1e-3 * {1: 0.01, 2: 0.25, 3: 0.9, 4: 17.0, 5: 700.0}[c]))))
+
+        def step():
+            for _ in range(reps):
+                m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, out=img, samples=cnt)
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        cnt.zero_()
+        clk = ClockSampler(0)
+        clk.start()
+        time.sleep(0.3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        clocks = clk.stop()
+        ms = e0.elapsed_time(e1)
+        samples = int(cnt.item())
+        F = RL.flops_per_sample(w.degree, True)
+        peak, src = RL.fp32_peak_tflops()
+        launches = args.steps * reps * ((V + 63) // 64)
+        ach = F * samples / (ms / 1e3) / 1e12
+        print(json.dumps({
+            "metric": METRIC, "value": samples / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "dtype": "f32",
+            "data": "synthetic (seeded generator of the BASELINE.json config recipe; no dataset)",
+            "config": {"workload": w.name, "views": V, "width": W, "height": H, "degree": w.degree,
+                       "layout": info["layout"], "launches_per_step": reps * ((V + 63) // 64),
+                       "model_bytes": info["model_bytes"], "device_bytes": info["device_bytes"],
+                       "footprint_ratio": info["device_bytes"] / info["model_bytes"], "create_ms": info["create_ms"]},
+            "frames_per_s": V * reps * args.steps / (ms / 1e3),
+            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                         "flops_per_sample": F, "launch_ms": ms / launches, "peak_source": src},
+            "gpu_launches": launches, "clocks": clocks}), flush=True)
+        del m, img
+        torch.cuda.empty_cache()
+    return 0
+
+
 def run_emulate(args):
     """One GPU, G emulated ranks: for each assignment mode render every
     rank's unit list alone (tiles, stored at their image positions) and time
@@ -806,6 +870,8 @@ def main():
         return run_reference(args)
     if args.emulate:
         return run_emulate(args)
+    if args.all_configs:
+        return run_all_configs(args)
     return run_ours(args)
 
 

@@ -244,9 +244,13 @@ struct RenderShape {
 // + gradient for every sample, R-20), 2 = NEXT-1's measured variant: the
 // gradient contraction and Phong are skipped for a sample whose TF opacity is
 // 0 (it composites with weight 0, so the image is bit-identical to SHADE = 1)
+#ifdef MFA_RENDER_MAXNREG   // experiment: an explicit register cap instead of the launch-bounds occupancy
+#define MFA_RENDER_BOUNDS __maxnreg__(MFA_RENDER_MAXNREG)
+#else
+#define MFA_RENDER_BOUNDS __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P, LAYOUT>::MINB)
+#endif
 template <int P, int LAYOUT, bool UNI, int SHADE, bool EXT>
-__global__ void __launch_bounds__(RenderShape<P, LAYOUT>::THREADS, RenderShape<P, LAYOUT>::MINB)
-    render_kernel(const __grid_constant__ RenderArgs args) {
+__global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderArgs args) {
     constexpr bool BEZ = LAYOUT == kBezier;
     constexpr bool CACHE = RenderShape<P, LAYOUT>::CACHE;
     extern __shared__ float4 s_tf[];
