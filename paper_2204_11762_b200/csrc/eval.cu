@@ -22,8 +22,8 @@ struct EvalArgs {
     unsigned long long* n_err;
     int64_t n;
     const float4* rec;     // SORTED: points as (u, v, w, index bits), grouped by spatial bin
-    float4* out4;          // SORTED: (value, du, dv, dw) of point i at out4[i] (original order, AoS)
-    const int* pos;        // (unused by eval: kept for the Hessian's gather)
+    float4* out4;          // SORTED: (value, du, dv, dw) at the sorted position (in place over rec)
+    const int* pos;        // SORTED: sorted position of point i
 };
 
 #ifndef MFA_EVAL_MINB     // resident 256-thread CTAs per SM the register budget is sized for
@@ -49,13 +49,10 @@ __global__ void __launch_bounds__(256, MFA_EVAL_MINB) eval_kernel(const __grid_c
             q[1] = __ldg(args.v + i);
             q[2] = __ldg(args.w + i);
         }
-        // direct: SoA outputs at i; SORTED: one 16-byte store at the point's
-        // original index (AoS), transposed to the caller's SoA arrays by one
-        // coalesced pass (aos_to_soa_kernel) -- cheaper than a random-read
-        // gather from the sorted order (round 1: 1.04 GB of DRAM reads)
+        // direct: SoA outputs at i; SORTED: one coalesced float4 at the sorted position
         auto store = [&](float val, float gu, float gv, float gw) {
             if constexpr (SORTED) {
-                args.out4[i] = make_float4(val, gu, gv, gw);
+                args.out4[it] = make_float4(val, gu, gv, gw);
             } else {
                 args.value[i] = val;
                 if (GRAD) {
@@ -296,26 +293,26 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(const unsigned* __restri
 __global__ void __launch_bounds__(256) bin_scatter_kernel(const float* __restrict__ u, const float* __restrict__ v,
                                                           const float* __restrict__ w, int64_t n,
                                                           int* __restrict__ bins, unsigned* __restrict__ cursor,
-                                                          float4* __restrict__ rec, int want_pos) {
+                                                          float4* __restrict__ rec) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const unsigned pos = atomicAdd(cursor + (size_t)bins[i] * MFA_CURSOR_STRIDE, 1u);
         rec[pos] = make_float4(__ldg(u + i), __ldg(v + i), __ldg(w + i), __int_as_float((int)i));
-        if (want_pos) bins[i] = (int)pos;
+        bins[i] = (int)pos;
     }
 }
 
-// eval results (AoS at the original index) to the caller's SoA arrays:
-// coalesced 16-byte reads, coalesced 4-byte writes
-__global__ void __launch_bounds__(256) aos_to_soa_kernel(const float4* __restrict__ out4, int64_t n,
-                                                         float* __restrict__ value, float* __restrict__ du,
+// results back to the caller's SoA arrays: coalesced writes at i, one 16-byte
+// gather from the sorted position
+__global__ void __launch_bounds__(256) bin_gather_kernel(const float4* __restrict__ out4, const int* __restrict__ pos,
+                                                         int64_t n, float* __restrict__ value, float* __restrict__ du,
                                                          float* __restrict__ dv, float* __restrict__ dw) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float4 r = __ldcs(out4 + i);
-        __stcs(value + i, r.x);
+        const float4 r = __ldg(out4 + __ldg(pos + i));
+        value[i] = r.x;
         if (du) {
-            __stcs(du + i, r.y);
-            __stcs(dv + i, r.z);
-            __stcs(dw + i, r.w);
+            du[i] = r.y;
+            dv[i] = r.z;
+            dw[i] = r.w;
         }
     }
 }
@@ -354,12 +351,10 @@ size_t bin_workspace_bytes(const Model* m, int64_t n) {
            up(sizeof(unsigned) * (g.nbins + 1) * MFA_CURSOR_STRIDE);
 }
 
-size_t eval_workspace_bytes(const Model* m, int64_t n) {
-    return bin_workspace_bytes(m, n) + ((sizeof(float4) * (size_t)n + 255) & ~(size_t)255);   // + AoS results
-}
+size_t eval_workspace_bytes(const Model* m, int64_t n) { return bin_workspace_bytes(m, n); }
 
 BinnedPoints bin_points(const Model* m, int64_t n, const float* u, const float* v, const float* w, void* ws,
-                        cudaStream_t st, bool want_pos) {
+                        cudaStream_t st) {
     const BinGrid g = make_bins(m);
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
     char* b = (char*)ws;
@@ -380,7 +375,7 @@ BinnedPoints bin_points(const Model* m, int64_t n, const float* u, const float* 
     }
     bin_count_kernel<<<cgrid, smem > 48 * 1024 ? 1024 : 256, smem, st>>>(u, v, w, n, g, bins, counts);
     bin_scan_kernel<<<1, 1024, 0, st>>>(counts, g.nbins + 1, cursor);
-    bin_scatter_kernel<<<grid, 256, 0, st>>>(u, v, w, n, bins, cursor, rec, want_pos ? 1 : 0);
+    bin_scatter_kernel<<<grid, 256, 0, st>>>(u, v, w, n, bins, cursor, rec);
     return BinnedPoints{rec, bins};
 }
 
@@ -392,9 +387,9 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
     a.out4 = nullptr;
     a.pos = nullptr;
     if (ws && n >= (int64_t)1 << 16 && n < ((int64_t)1 << 31) && ws_bytes >= eval_workspace_bytes(m, n)) {
-        const BinnedPoints bp = bin_points(m, n, u, v, w, ws, st, false);
+        const BinnedPoints bp = bin_points(m, n, u, v, w, ws, st);
         a.rec = bp.rec;
-        a.out4 = reinterpret_cast<float4*>((char*)ws + bin_workspace_bytes(m, n));
+        a.out4 = bp.rec;   // results overwrite the record a thread has just read
         a.pos = bp.pos;
     }
     a.Q = m->Q;
@@ -429,7 +424,7 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
-        aos_to_soa_kernel<<<grid, 256, 0, st>>>(a.out4, n, value, du, dv, dw);
+        bin_gather_kernel<<<grid, 256, 0, st>>>(a.out4, a.pos, n, value, du, dv, dw);
         e = cudaGetLastError();
     }
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "eval launch");

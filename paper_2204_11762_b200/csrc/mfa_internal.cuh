@@ -203,7 +203,7 @@ struct BinnedPoints {
 };
 size_t bin_workspace_bytes(const Model* m, int64_t n);
 BinnedPoints bin_points(const Model* m, int64_t n, const float* u, const float* v, const float* w, void* ws,
-                        cudaStream_t st, bool want_pos = true);   // want_pos: pos[i] = sorted position (Hessian gather)
+                        cudaStream_t st);
 mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                          const mfa_render_params* prm, const mfa_tiles* tiles, void* out,
                          unsigned long long* samples, cudaStream_t st, const mfa_render_ext* ext = nullptr);
