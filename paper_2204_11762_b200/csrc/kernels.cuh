@@ -347,8 +347,17 @@ __device__ __forceinline__ void nonuni_span_f32(const AxisArgs& A, float u, int&
 // them (spans are monotone along a ray) is the knot table read.  The offset
 // F - lo (< h * 2^62) is shifted to < 2^23 and converted exactly with the
 // 2^23 magic number, so t costs no int64 -> float conversion.
+#ifndef MFA_NU_SHIFTCMP   // 1: span crossings tested on the shifted 32-bit offset d = (F - lo) >> dshift
+#define MFA_NU_SHIFTCMP 0    //    against the span width in the same units (wsh, from the record)
+#endif
+
 struct NUAxis {
-    long long lo, hi;   // knot bounds of span s (2^62 fixed point)
+    long long lo;       // left knot of span s (2^62 fixed point)
+#if MFA_NU_SHIFTCMP
+    int wsh;            // ceil(width / 2^dshift): forward crossing iff (F - lo) >> dshift >= wsh
+#else
+    long long hi;       // right knot of span s
+#endif
     float tsc;          // 2^(dshift-62) / h_s
     float invh;         // 1 / h_s
     int s;
@@ -370,10 +379,15 @@ __device__ __forceinline__ void nu_load(const AxisArgs& A, NUAxis& st) {
                  : "=l"(r0), "=l"(r1), "=l"(r2), "=l"(r3)
                  : "l"(A.srec + st.s));
     st.lo = r0;
+#if MFA_NU_SHIFTCMP
+    st.wsh = (int)r1;
+#else
     st.hi = r1;
+#endif
     st.invh = __int_as_float((int)r2);
     st.tsc = __int_as_float((int)r3);
 #else
+    static_assert(!MFA_NU_SHIFTCMP, "MFA_NU_SHIFTCMP needs the span records");
     st.lo = __ldg(A.kfx + st.s);
     st.hi = (st.s + 1 < A.nsp) ? __ldg(A.kfx + st.s + 1) : 0x7fffffffffffffffLL;
     st.invh = __ldg(A.invh + st.s);
@@ -392,6 +406,7 @@ __device__ __forceinline__ void nu_init(const AxisArgs& A, long long F, NUAxis& 
     nu_load(A, st);
 }
 
+#if !MFA_NU_SHIFTCMP
 __device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis& st) {
     // F may leave [0, 2^62] by rounding at the entry/exit faces only; the span
     // index is kept in range and the local offset is clamped below instead of
@@ -416,14 +431,26 @@ __device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis&
     const float fd = __int_as_float(0x4b000000 | d) - 8388608.0f;
     return fd * st.tsc;
 }
+#endif
 
 // nu_span in two phases (MFA_NU_SPLIT, the render default): first every axis
 // moves into its neighbouring span and issues the record load (predicated, no
 // branch), then every axis consumes its record, so the crossings of the three
 // axes wait for one load round trip instead of three (C5 +6 %).
+// the span-local offset in units of 2^dshift (negative before the span)
+__device__ __forceinline__ int nu_offset(const AxisArgs& A, long long F, const NUAxis& st) {
+    return (int)((F - st.lo) >> A.dshift);
+}
+
 __device__ __forceinline__ void nu_cross(const AxisArgs& A, long long F, NUAxis& st) {
+#if MFA_NU_SHIFTCMP
+    const int d = nu_offset(A, F, st);
+    const bool fwd = d >= st.wsh;
+    const bool bwd = d < 0 && st.s > 0;
+#else
     const bool fwd = F >= st.hi;
     const bool bwd = F < st.lo && st.s > 0;
+#endif
     if (fwd || bwd) {
         st.s += fwd ? 1 : -1;
         nu_load(A, st);
@@ -435,6 +462,17 @@ __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxi
     // rare: crossed more than one span this step; impossible when every span is
     // wider than the largest step (A.multi = 0; the render compiles a loop
     // without the check, MULTI = false, for launches where no axis needs it)
+#if MFA_NU_SHIFTCMP
+    int d = nu_offset(A, F, st);
+    if (MULTI && A.multi && (d >= st.wsh || (d < 0 && st.s > 0))) {
+        int s = st.s;
+        while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
+        while (s > 0 && F < __ldg(A.kfx + s)) --s;
+        st.s = s;
+        nu_load(A, st);
+        d = nu_offset(A, F, st);
+    }
+#else
     if (MULTI && A.multi && (F >= st.hi || (F < st.lo && st.s > 0))) {
         int s = st.s;
         while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
@@ -443,6 +481,7 @@ __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxi
         nu_load(A, st);
     }
     int d = (int)((F - st.lo) >> A.dshift);
+#endif
     d = min(max(d, 0), 8388607);
     const float fd = __int_as_float(0x4b000000 | d) - 8388608.0f;
     return fd * st.tsc;

@@ -177,11 +177,17 @@ __global__ void span_tables_kernel(const double* __restrict__ U, int p, int nsp,
 // 1/h and the offset scale 2^(dshift-62)/h, so a span crossing is one sector
 // load (kernels.cuh nu_load).
 __global__ void span_rec_kernel(const long long* __restrict__ kfx, const float* __restrict__ invh, int nsp,
-                                float dscale, longlong4* __restrict__ rec) {
+                                float dscale, int dshift, longlong4* __restrict__ rec) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nsp) return;
     const float ih = invh[s];
-    rec[s] = make_longlong4(kfx[s], s + 1 < nsp ? kfx[s + 1] : 0x7fffffffffffffffLL,
+#if MFA_NU_SHIFTCMP   // {lo, ceil(width / 2^dshift) (INT_MAX for the last span), bits(1/h), bits(tsc)}
+    const long long w = s + 1 < nsp ? kfx[s + 1] - kfx[s] : -1;
+    const long long second = w < 0 ? 0x7fffffffLL : (w + (1LL << dshift) - 1) >> dshift;
+#else
+    const long long second = s + 1 < nsp ? kfx[s + 1] : 0x7fffffffffffffffLL;
+#endif
+    rec[s] = make_longlong4(kfx[s], second,
                             (long long)(unsigned)__float_as_int(ih),
                             (long long)(unsigned)__float_as_int(ih * dscale));
 }
@@ -493,7 +499,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
                                                              (long long*)A.kfx, Mb[d], (int*)A.bucket);
         A.srec = (longlong4*)(base + off[d][6]);
         span_rec_kernel<<<(nsp + 127) / 128, 128, 0, st>>>((const long long*)A.kfx, (const float*)A.invh, nsp,
-                                                           ldexpf(1.0f, A.dshift - kNonUniFracBits),
+                                                           ldexpf(1.0f, A.dshift - kNonUniFracBits), A.dshift,
                                                            (longlong4*)A.srec);
         // uniform interior spans [p-1, S-p] share one polynomial set
         A.ic_lo = p - 1;

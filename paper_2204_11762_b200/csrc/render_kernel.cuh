@@ -38,6 +38,9 @@
 #ifndef MFA_VIEW_ORDER   // with MFA_VIEW_GROUP > 1: 1 = per supertile, 2 = per supertile row, 3 = per tile
 #define MFA_VIEW_ORDER 1
 #endif
+#ifndef MFA_PREFETCH_NEXT   // experiment: 1 / 2 = prefetch the predicted next block into L1 / L2
+#define MFA_PREFETCH_NEXT 0
+#endif
 #ifndef MFA_FLAT_LOOP
 #define MFA_FLAT_LOOP 1
 #endif
@@ -494,13 +497,17 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 #endif
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
-                if (UNI) {
+                if constexpr (UNI) {
                     uni_span_fx(F[i], args.ax[i].nsp, s[i], t[i]);
                     gs[i] = args.gsc[i];
                 } else {
+#if MFA_NU_SPLIT
+                    __builtin_unreachable();   // handled above
+#else
                     t[i] = nu_span(args.ax[i], F[i], nu[i]);
                     s[i] = nu[i].s;
                     gs[i] = nu[i].invh * args.gsc[i];
+#endif
                 }
             }
         };
@@ -777,6 +784,35 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 float t[3], gs1[3];
                 locate(s, t, gs1, multi_tag);
                 fetch(s);
+#if MFA_PREFETCH_NEXT
+                if constexpr (BEZ && !UNI) {
+                    // predict the span triple of the sample after this one from the
+                    // current span bounds (one crossing per axis at most) and pull
+                    // its block towards the SM a whole iteration before its load
+                    int s2[3];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+#if MFA_NU_SHIFTCMP
+                        const int d2 = nu_offset(args.ax[i], F[i] + DF[i], nu[i]);
+                        s2[i] = s[i] + (d2 >= nu[i].wsh ? 1 : 0) - (d2 < 0 && s[i] > 0 ? 1 : 0);
+#else
+                        const long long F2 = F[i] + DF[i];
+                        s2[i] = s[i] + (F2 >= nu[i].hi ? 1 : 0) - (F2 < nu[i].lo && s[i] > 0 ? 1 : 0);
+#endif
+                    }
+                    const int e2 = (s2[2] * args.bg.S1 + s2[1]) * args.bg.S0 + s2[0];
+                    if (e2 != nb_key && live) {
+                        const char* q = reinterpret_cast<const char*>(bez_block_at<P>(args.Q, args.bg, e2));
+#if MFA_PREFETCH_NEXT == 2
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(q + 128));
+#else
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(q + 128));
+#endif
+                    }
+                }
+#endif
                 comp_on = live;
                 shade_composite(val, gu, gv, gw, gs, 0.f, 0.f);
 #if MFA_ORDER
