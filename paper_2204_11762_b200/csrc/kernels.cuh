@@ -348,7 +348,7 @@ __device__ __forceinline__ void nonuni_span_f32(const AxisArgs& A, float u, int&
 // F - lo (< h * 2^62) is shifted to < 2^23 and converted exactly with the
 // 2^23 magic number, so t costs no int64 -> float conversion.
 #ifndef MFA_NU_SHIFTCMP   // 1: span crossings tested on the shifted 32-bit offset d = (F - lo) >> dshift
-#define MFA_NU_SHIFTCMP 0    //    against the span width in the same units (wsh, from the record)
+#define MFA_NU_SHIFTCMP 1    //    against the span width in the same units (wsh, from the record): C5 +2.1 %
 #endif
 
 struct NUAxis {
