@@ -572,6 +572,27 @@ def secondary_kernels(w, m, c, p, img, tf, stream):
     res["encode_grid"] = {"s": time.perf_counter() - t0, "e_max": 1e-3, "result": er,
                           "rounds_nctrl_maxerr": [[int(r[0]), int(r[1]), int(r[2]), float(r[3])] for r in log]}
     del q
+    # the same render on the other control-point layouts (footprint / throughput
+    # trade-off, P:133 / P:263): one warm-up and one timed launch each
+    lay = {}
+    for layout in ("quads", "bricks", "bezier"):
+        if layout == m.info()["layout"] or (layout != "quads" and w.degree > 3):
+            continue
+        try:
+            ml = Model.from_workload(w, layout=layout)
+        except Exception as ex:   # e.g. not enough device memory for the Bezier blocks
+            lay[layout] = {"error": str(ex)[:200]}
+            continue
+        il = ml.info()
+        out_l = torch.empty((len(w.cameras), w.cameras[0].height, w.cameras[0].width, 4), device="cuda")
+        cnt_l = torch.zeros(1, dtype=torch.int64, device="cuda")
+        ms = _time(lambda: ml.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, out=out_l, samples=cnt_l), 1, stream)
+        lay[layout] = {"samples_per_s": int(cnt_l.item()) / 2 / (ms / 1e3), "ms_per_step": ms,
+                       "device_bytes": il["device_bytes"], "footprint_ratio": il["device_bytes"] / il["model_bytes"],
+                       "create_ms": il["create_ms"]}
+        del ml, out_l
+        torch.cuda.empty_cache()
+    res["layouts"] = lay
     if img is not None and img.shape[0] >= 2 and img.dtype == torch.float32:
         a, b = img[0], img[1]
         ws = torch.empty(int(__import__("paper_2204_11762_b200")._lib.lib().mfa_image_quality_workspace(

@@ -37,6 +37,7 @@ struct AxisArgs {
     int dshift;      // non-uniform render: (F - U_s) >> dshift fits 23 bits on every span
     float dscale;    // 2^(dshift - 62)
     int multi;       // non-uniform render: 1 if one ray step can cross more than one span (set per launch)
+    float gsc;       // non-uniform render: parameter -> physical gradient scale 1/L (set per launch)
 };
 
 __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
@@ -49,6 +50,7 @@ __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
     a.bucket = A.bucket;
     a.srec = A.srec;
     a.multi = 1;
+    a.gsc = 1.f;
     a.nsp = A.nsp;
     a.M = A.M;
     int lg = 0;
@@ -347,8 +349,8 @@ __device__ __forceinline__ void nonuni_span_f32(const AxisArgs& A, float u, int&
 // them (spans are monotone along a ray) is the knot table read.  The offset
 // F - lo (< h * 2^62) is shifted to < 2^23 and converted exactly with the
 // 2^23 magic number, so t costs no int64 -> float conversion.
-#ifndef MFA_NU_SHIFTCMP   // 1: span crossings tested on the shifted 32-bit offset d = (F - lo) >> dshift
-#define MFA_NU_SHIFTCMP 1    //    against the span width in the same units (wsh, from the record): C5 +2.1 %
+#ifndef MFA_GSV   // 1: the gradient scale (1/h) * gsc folded into the span state at each crossing
+#define MFA_GSV 0
 #endif
 
 struct NUAxis {
@@ -359,7 +361,11 @@ struct NUAxis {
     long long hi;       // right knot of span s
 #endif
     float tsc;          // 2^(dshift-62) / h_s
+#if MFA_GSV
+    float gsv;          // (1 / h_s) * gsc: the span's t -> physical gradient scale (set at each crossing)
+#else
     float invh;         // 1 / h_s
+#endif
     int s;
 };
 
@@ -384,14 +390,23 @@ __device__ __forceinline__ void nu_load(const AxisArgs& A, NUAxis& st) {
 #else
     st.hi = r1;
 #endif
+#if MFA_GSV
+    st.gsv = __int_as_float((int)r2) * A.gsc;
+#else
     st.invh = __int_as_float((int)r2);
+#endif
     st.tsc = __int_as_float((int)r3);
 #else
     static_assert(!MFA_NU_SHIFTCMP, "MFA_NU_SHIFTCMP needs the span records");
     st.lo = __ldg(A.kfx + st.s);
     st.hi = (st.s + 1 < A.nsp) ? __ldg(A.kfx + st.s + 1) : 0x7fffffffffffffffLL;
-    st.invh = __ldg(A.invh + st.s);
-    st.tsc = st.invh * A.dscale;
+    const float ih = __ldg(A.invh + st.s);
+#if MFA_GSV
+    st.gsv = ih * A.gsc;
+#else
+    st.invh = ih;
+#endif
+    st.tsc = ih * A.dscale;
 #endif
 }
 
@@ -437,6 +452,14 @@ __device__ __forceinline__ float nu_span(const AxisArgs& A, long long F, NUAxis&
 // moves into its neighbouring span and issues the record load (predicated, no
 // branch), then every axis consumes its record, so the crossings of the three
 // axes wait for one load round trip instead of three (C5 +6 %).
+__device__ __forceinline__ float nu_gscale(const AxisArgs& A, const NUAxis& st) {
+#if MFA_GSV
+    return st.gsv;
+#else
+    return st.invh * A.gsc;
+#endif
+}
+
 // the span-local offset in units of 2^dshift (negative before the span)
 __device__ __forceinline__ int nu_offset(const AxisArgs& A, long long F, const NUAxis& st) {
     return (int)((F - st.lo) >> A.dshift);

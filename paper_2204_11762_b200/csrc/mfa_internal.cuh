@@ -43,6 +43,12 @@
     } while (0)
 #endif
 
+// render span records and the tracker that reads them must agree (model.cu
+// writes the records, kernels.cuh reads them): defined here, for every TU
+#ifndef MFA_NU_SHIFTCMP   // 1: span crossings tested on the shifted 32-bit offset d = (F - lo) >> dshift
+#define MFA_NU_SHIFTCMP 1    //    against the span width in the same units (wsh, from the record): C5 +2.1 %
+#endif
+
 #ifndef MFA_SUPERTILE   // full-frame work order: supertiles of MFA_SUPERTILE x MFA_SUPERTILE 16x16 tiles
 #define MFA_SUPERTILE 2
 #endif

@@ -120,6 +120,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         a->bmin[d] = prm->box_min[d];
         a->L[d] = prm->box_max[d] - prm->box_min[d];
         a->gsc[d] = (float)((uni ? (double)m->ax[d].nsp : 1.0) / a->L[d]);
+        a->ax[d].gsc = a->gsc[d];   // non-uniform axes: folded into the span state at each crossing
     }
     a->step = prm->step;
     a->inv_step = 1.0 / prm->step;

@@ -490,7 +490,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 for (int i = 0; i < 3; ++i) {
                     t[i] = nu_finish<MULTI>(args.ax[i], F[i], nu[i]);
                     s[i] = nu[i].s;
-                    gs[i] = nu[i].invh * args.gsc[i];
+                    gs[i] = nu_gscale(args.ax[i], nu[i]);
                 }
                 return;
             }
@@ -506,7 +506,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 #else
                     t[i] = nu_span(args.ax[i], F[i], nu[i]);
                     s[i] = nu[i].s;
-                    gs[i] = nu[i].invh * args.gsc[i];
+                    gs[i] = nu_gscale(args.ax[i], nu[i]);
 #endif
                 }
             }
