@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--skip-transparent-gradient", action="store_true",
                     help="NEXT-1 variant: shading = 2 (no gradient / Phong for samples with TF opacity 0; "
                          "identical image)")
+    ap.add_argument("--skip-transparent-blocks", action="store_true",
+                    help="NEXT-1 variant: shading = 3 (samples in macro blocks whose value range maps to TF "
+                         "opacity 0 are skipped entirely; identical image)")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: direct NVLink stores into rank 0's image (p2p) or packed tiles + NCCL all-gather")
     ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier", "bricks"],
@@ -277,9 +280,10 @@ def run_ours(args):
     c = int(args.workload[1:])
     kw = {"n_views": args.views} if args.views else {}
     w = WL.make_config(c, **kw)
-    if args.no_shading or args.skip_transparent_gradient:
+    if args.no_shading or args.skip_transparent_gradient or args.skip_transparent_blocks:
         import dataclasses
-        w.params = dataclasses.replace(w.params, shading=0 if args.no_shading else 2)
+        w.params = dataclasses.replace(w.params, shading=0 if args.no_shading else
+                                       (2 if args.skip_transparent_gradient else 3))
     V = len(w.cameras)
     W, H = w.cameras[0].width, w.cameras[0].height
     stream = torch.cuda.current_stream()
@@ -397,9 +401,10 @@ def run_ours(args):
             "launch_ms": launch_ms, "peak_source": peak_src,
             "counted_bytes_per_sample": Bs,
             "l2_counted_GBps": Bs * per_launch_samples / (launch_ms / 1e3) / 1e9}
-    if int(w.params.shading) == 2:
-        roof["note"] = ("NEXT-1 variant (shading = 2): samples with TF opacity 0 skip the gradient contraction and "
-                        "Phong, so F(p) overstates the work done; not a roofline claim")
+    if int(w.params.shading) in (2, 3):
+        roof["note"] = (f"NEXT-1 variant (shading = {int(w.params.shading)}): samples with TF opacity 0 skip the "
+                        "gradient contraction and Phong (2) or all of their work (3), so F(p) overstates the work "
+                        "done; not a roofline claim")
     if clocks.get("sm_mhz"):
         pk_clk, _ = RL.fp32_peak_tflops(clocks["sm_mhz"])
         roof["frac_at_observed_clock"] = achieved_tf / pk_clk

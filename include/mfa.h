@@ -236,7 +236,12 @@ typedef struct {
                                         Phong skipped for samples whose TF opacity is 0 (NEXT-1's
                                         variant: they composite with weight 0, so the image and the
                                         sample count equal shading = 1's; degree <= 3 models, other
-                                        layouts run shading = 1) */
+                                        layouts run shading = 1), 3 on with whole samples skipped
+                                        (no block fetch, value, gradient or Phong) where the TF opacity
+                                        is 0 over the value range of the sample's 2^3-span macro block
+                                        (Bezier layout: the convex hull of its Bernstein coefficients;
+                                        image and sample count again equal shading = 1's; other layouts
+                                        run shading = 1) */
     double ka, kd, ks, shininess;    /* Phong constants */
     double grad_eps;                 /* |physical gradient| <= grad_eps -> ambient only (R-11) */
     int32_t out_fp16;                /* 0: fp32 RGBA (16 B/px); 1: fp16 RGBA (8 B/px) */

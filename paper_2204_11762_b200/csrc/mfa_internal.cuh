@@ -62,6 +62,10 @@ constexpr int kNonUniFracBits = 62; // non-uniform axes: parameter fixed point, 
 constexpr int kBrickLog = 4;        // bricks of 16x16x16 spans
 constexpr int kBrick = 1 << kBrickLog;
 constexpr int kQueueSlots = 256;    // persistent-kernel work counters (one per in-flight launch)
+#ifndef MFA_MACRO_LOG
+#define MFA_MACRO_LOG 1
+#endif
+constexpr int kMacroLog = MFA_MACRO_LOG;   // macro blocks of 2^3 span triples (transparent-block skip; 4^3: -3 %, 8^3: -9 %)
 __host__ __device__ constexpr int bez_row(int p) { return p == 1 ? 2 : 4; }  // floats per stored block row
 
 // float4 per brick entry: p <= 3 stores row PAIRS (rows j and j+1 of a quad
@@ -116,6 +120,11 @@ struct Model {
     AxisTables ax[3];
     void* table_mem = nullptr;   // one allocation for all axis tables
     int64_t device_bytes = 0;
+    // Bezier layout: value bounds per macro block of kMacro^3 span triples (the
+    // Bernstein convex hull: min / max coefficient, order-preserving uint
+    // encoding), for NEXT-1's transparent-block skip (shading = 3)
+    unsigned int* mmx = nullptr;   // [n_macro][2]
+    int mm[3] = {0, 0, 0};         // macro blocks per axis
     int64_t model_bytes = 0;       // the fp32 control grid the caller passed (n_u n_v n_w * 4)
     double create_ms = 0.0;        // wall time of mfa_model_create (validation, upload, relayout, tables)
 

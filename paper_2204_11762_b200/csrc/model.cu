@@ -222,10 +222,18 @@ __global__ void bezier_tables_kernel(const double* __restrict__ U, int p, int ns
 // coefficients of the spline on that span triple:
 //   Z[l][k][j] = sum_{c,b,a} Dw[c][l] Dv[b][k] Du[a][j] P[sw+c][sv+b][su+a]
 // (sum-factorised, fp64), stored as rows of bez_row(p) floats, j fastest.
+__global__ void init_minmax_kernel(unsigned* __restrict__ mmx, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        mmx[2 * i] = 0xffffffffu;   // ordered min: starts at the largest key
+        mmx[2 * i + 1] = 0u;
+    }
+}
+
 template <int P>
 __global__ void bezier_blocks_kernel(const float* __restrict__ Pg, int nu, int nv, const double* __restrict__ Du,
                                      const double* __restrict__ Dv, const double* __restrict__ Dw, int Su, int Sv,
-                                     int64_t nblocks, float* __restrict__ out) {
+                                     int64_t nblocks, float* __restrict__ out, unsigned* __restrict__ mmx, int mm0,
+                                     int mm1) {
     constexpr int Q = P + 1, R = bez_row(P);
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < nblocks;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -255,15 +263,24 @@ __global__ void bezier_blocks_kernel(const float* __restrict__ Pg, int nu, int n
                     Y[c][k][j] = acc;
                 }
         float* o = out + idx * (Q * Q * R);
+        float lo = INFINITY, hi = -INFINITY;
         for (int l = 0; l < Q; ++l)
             for (int k = 0; k < Q; ++k) {
                 for (int j = 0; j < Q; ++j) {
                     double acc = 0.0;
                     for (int c = 0; c < Q; ++c) acc += dw[c * Q + l] * Y[c][k][j];
-                    o[(l * Q + k) * R + j] = (float)acc;
+                    const float f = (float)acc;
+                    o[(l * Q + k) * R + j] = f;
+                    lo = fminf(lo, f);
+                    hi = fmaxf(hi, f);
                 }
                 for (int j = Q; j < R; ++j) o[(l * Q + k) * R + j] = 0.f;
             }
+        // macro-block value bounds (the spline on a span triple lies in the
+        // convex hull of its Bernstein coefficients)
+        const int64_t mi = ((int64_t)(sw >> kMacroLog) * mm1 + (sv >> kMacroLog)) * mm0 + (su >> kMacroLog);
+        atomicMin(mmx + 2 * mi, f2ord(lo));
+        atomicMax(mmx + 2 * mi + 1, f2ord(hi));
     }
 }
 
@@ -410,6 +427,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
         if (Udev) cudaFree(Udev);
         if (mm) cudaFree(mm);
         if (s != MFA_OK) {
+            if (m->mmx) cudaFree(m->mmx);
             if (m->Q) cudaFree(m->Q);
             if (m->queue) cudaFree(m->queue);
             if (m->table_mem) cudaFree(m->table_mem);
@@ -551,10 +569,17 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
                                                                        Dax[d]);
             }
             float* out = reinterpret_cast<float*>(m->Q);
+            const int64_t Sd[3] = {S0, S1, S2};
+            for (int d = 0; d < 3; ++d) m->mm[d] = (int)((Sd[d] + (1 << kMacroLog) - 1) >> kMacroLog);
+            const int64_t nmac = (int64_t)m->mm[0] * m->mm[1] * m->mm[2];
+            if ((e = cudaMalloc(&m->mmx, sizeof(unsigned) * 2 * nmac)) != cudaSuccess)
+                return cleanup(cuda_fail(e, "cudaMalloc macro bounds"));
+            init_minmax_kernel<<<(unsigned)std::min<int64_t>((nmac + 255) / 256, 4096), 256, 0, st>>>(m->mmx, nmac);
+            m->device_bytes += sizeof(unsigned) * 2 * nmac;
             switch (p) {
-                case 1: bezier_blocks_kernel<1><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out); break;
-                case 2: bezier_blocks_kernel<2><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out); break;
-                default: bezier_blocks_kernel<3><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out); break;
+                case 1: bezier_blocks_kernel<1><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out, m->mmx, m->mm[0], m->mm[1]); break;
+                case 2: bezier_blocks_kernel<2><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out, m->mmx, m->mm[0], m->mm[1]); break;
+                default: bezier_blocks_kernel<3><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out, m->mmx, m->mm[0], m->mm[1]); break;
             }
             cudaStreamSynchronize(st);
             cudaFree(D);
@@ -634,6 +659,7 @@ extern "C" mfa_status mfa_model_destroy(mfa_model h) {
     if (cur != m->device) cudaSetDevice(m->device);
     free_model_resources(m);
     if (m->Q) cudaFree(m->Q);
+    if (m->mmx) cudaFree(m->mmx);
     if (m->queue) cudaFree(m->queue);
     if (m->table_mem) cudaFree(m->table_mem);
     if (cur != m->device && cur >= 0) cudaSetDevice(cur);

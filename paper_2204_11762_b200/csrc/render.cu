@@ -54,6 +54,48 @@ void free_model_resources(Model* m) {
     h = Model::HostRes{};
 }
 
+// NEXT-1 transparent-block skip (shading = 3): one bit per macro block of
+// kMacro^3 span triples, set when the transfer function's opacity is 0 over
+// the block's whole value range [min, max] of its Bernstein coefficients (the
+// spline lies in their convex hull).  The test covers every table entry a
+// value in the range can touch in the kernel's lookup (f = (v - v_lo) s,
+// entries floor(f) .. floor(f) + 1) with two entries of margin for fp32
+// rounding of the sample value; a prefix count of the non-zero-opacity
+// entries makes it O(1) per block.
+__global__ void macro_transparent_kernel(const unsigned* __restrict__ mmx, int64_t nmac, const float4* __restrict__ tf,
+                                         int tf_n, float v_lo, float s_scale, unsigned* __restrict__ bits) {
+    __shared__ int pre[1025];
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int i = 0; i < tf_n; ++i) {
+            pre[i] = c;
+            c += tf[i].w != 0.f;
+        }
+        pre[tf_n] = c;
+    }
+    __syncthreads();
+    const int64_t nw = (nmac + 31) / 32;
+    for (int64_t wi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; wi < nw; wi += (int64_t)gridDim.x * blockDim.x) {
+        unsigned word = 0;
+        for (int bit = 0; bit < 32; ++bit) {
+            const int64_t mi = wi * 32 + bit;
+            if (mi >= nmac) break;
+            const unsigned klo = mmx[2 * mi], khi = mmx[2 * mi + 1];
+            if (klo == 0xffffffffu) {   // no span triple in this macro block (past the grid): never sampled
+                word |= 1u << bit;
+                continue;
+            }
+            const float lo = __uint_as_float((klo & 0x80000000u) ? (klo & 0x7fffffffu) : ~klo);
+            const float hi = __uint_as_float((khi & 0x80000000u) ? (khi & 0x7fffffffu) : ~khi);
+            const float flo = fminf(fmaxf((lo - v_lo) * s_scale, 0.f), (float)(tf_n - 1));
+            const float fhi = fminf(fmaxf((hi - v_lo) * s_scale, 0.f), (float)(tf_n - 1));
+            const int i0 = max(0, (int)floorf(flo) - 2), i1 = min(tf_n - 1, (int)floorf(fhi) + 3);
+            if (pre[i1 + 1] - pre[i0] == 0) word |= 1u << bit;
+        }
+        bits[wi] = word;
+    }
+}
+
 cudaError_t dispatch_render_main(const RenderArgs& a, int p, int layout, bool uni, int shade, cudaStream_t st) {
     switch (p) {
         case 1: return dispatch_render<1, false>(a, layout, uni, shade, st);
@@ -149,7 +191,22 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->out = out;
     a->out_fp16 = prm->out_fp16;
     a->samples = samples;
-    const int shade = prm->shading == 2 ? 2 : (prm->shading != 0);   // 2: NEXT-1 skip variant
+    // 2 / 3: NEXT-1 variants (gradient skip / transparent-block skip)
+    const int shade = (prm->shading == 2 || prm->shading == 3) ? prm->shading : (prm->shading != 0);
+    a->tbits = nullptr;
+    a->mm0 = m->mm[0];
+    a->mm1 = m->mm[1];
+    void* tscratch = nullptr;
+    if (shade == 3 && m->layout == kBezier && m->mmx && !(field || lights || curv)) {
+        const int64_t nmac = (int64_t)m->mm[0] * m->mm[1] * m->mm[2];
+        tscratch = scratch_alloc(sizeof(unsigned) * ((nmac + 31) / 32), st);
+        if (tscratch) {
+            const int64_t nw = (nmac + 31) / 32;
+            macro_transparent_kernel<<<(unsigned)std::min<int64_t>((nw + 255) / 256, 2048), 256, 0, st>>>(
+                m->mmx, nmac, a->tf, a->tf_n, a->v_lo, a->s_scale, (unsigned*)tscratch);
+            a->tbits = (const unsigned*)tscratch;
+        }
+    }
     cudaError_t e = cudaSuccess;
     bool exhausted = false;
     auto run = [&]() -> cudaError_t {
@@ -171,6 +228,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     if (tiles) {
         if (n_views > kMaxViewsPerLaunch) {
             delete a;
+            if (tscratch) cudaFreeAsync(tscratch, st);
             return fail(MFA_ERR_UNSUPPORTED, "tiled render supports at most 64 views per call");
         }
         for (int v = 0; v < n_views; ++v) compute_frame(cams[v], a->frames[v]);
@@ -195,6 +253,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         }
     }
     delete a;
+    if (tscratch) cudaFreeAsync(tscratch, st);
     if (exhausted)
         return fail(MFA_ERR_UNSUPPORTED, "render: more than 256 renders in flight on distinct streams for one model");
     return e == cudaSuccess ? MFA_OK : cuda_fail(e, "render launch");

@@ -21,6 +21,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "kernels.cuh"
 
@@ -108,6 +109,8 @@ struct RenderArgs {
         int n;                    // 0: off
         float scale, range;       // index = (kappa + range) * scale, scale = (n - 1) / (2 range)
     } curv;
+    const unsigned* tbits;        // SHADE == 3: bit per macro block, 1 = the TF is transparent over its value range
+    int mm0, mm1;                 // SHADE == 3: macro blocks along u, v
     ViewFrame frames[kMaxViewsPerLaunch];   // per view, computed on the host (compute_frame)
 };
 
@@ -246,7 +249,10 @@ struct RenderShape {
 // SHADE: 0 = ShadingOn false (value only, Alg. 1 l.8), 1 = the ★ path (value
 // + gradient for every sample, R-20), 2 = NEXT-1's measured variant: the
 // gradient contraction and Phong are skipped for a sample whose TF opacity is
-// 0 (it composites with weight 0, so the image is bit-identical to SHADE = 1)
+// 0 (it composites with weight 0, so the image is bit-identical to SHADE = 1);
+// 3 = the transparent-block skip: a sample whose macro block's value range
+// (Bernstein convex hull) maps to TF opacity 0 is neither fetched nor queried
+// (it too composites with weight 0: bit-identical to SHADE = 1)
 #ifdef MFA_RENDER_MAXNREG   // experiment: an explicit register cap instead of the launch-bounds occupancy
 #define MFA_RENDER_BOUNDS __maxnreg__(MFA_RENDER_MAXNREG)
 #else
@@ -477,6 +483,15 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                     load_block<P>(args.Q + e, nb);
                     nb_key = e;
                 }
+            }
+        };
+        // SHADE == 3: is the sample's macro block transparent under this TF?
+        auto transparent = [&](const int (&s)[3]) -> bool {
+            if constexpr (SHADE == 3) {
+                const int mi = ((s[2] >> kMacroLog) * args.mm1 + (s[1] >> kMacroLog)) * args.mm0 + (s[0] >> kMacroLog);
+                return (__ldg(args.tbits + (mi >> 5)) >> (mi & 31)) & 1u;
+            } else {
+                return false;
             }
         };
         // a4: span + local coordinate per axis of the sample at F
@@ -759,6 +774,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         // two-stage pipeline: iteration k queries sample k+1 while it shades
         // and composites sample k; the ERT test (l.14-15; R-13) follows.
         float val = 0.f, gu = 0.f, gv = 0.f, gw = 0.f, gs[3] = {0.f, 0.f, 0.f};
+        bool tr_cur = false;   // SHADE == 3: the sample being shaded lies in a transparent macro block
         float ck1 = 0.f, ck2 = 0.f;   // curvatures of the sample being shaded (EXT curvature TF)
         if (live) {
             int s[3];
@@ -768,8 +784,11 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 if (args.curv.n > 0) curv_query(s, t, gs, ck1, ck2);
                 sample_field(s, t, val, gu, gv, gw, gs);
             } else {
-                fetch(s);
-                query(s, t, val, gu, gv, gw);
+                tr_cur = transparent(s);
+                if (!tr_cur) {
+                    fetch(s);
+                    query(s, t, val, gu, gv, gw);
+                }
             }
 #pragma unroll
             for (int i = 0; i < 3; ++i) F[i] += (!kFlat || K > 1) ? DF[i] : 0;
@@ -783,7 +802,8 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 int s[3];
                 float t[3], gs1[3];
                 locate(s, t, gs1, multi_tag);
-                fetch(s);
+                const bool tr_next = transparent(s);
+                if (!tr_next) fetch(s);
 #if MFA_PREFETCH_NEXT
                 if constexpr (BEZ && !UNI) {
                     // predict the span triple of the sample after this one from the
@@ -813,12 +833,13 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                     }
                 }
 #endif
-                comp_on = live;
+                comp_on = live && !tr_cur;   // a transparent sample composites with weight 0
                 shade_composite(val, gu, gv, gw, gs, 0.f, 0.f);
 #if MFA_ORDER
                 t[0] = fmaf(order_dep, 0.f, t[0]);   // exact: t[0] + 0 (A is finite)
 #endif
-                query(s, t, val, gu, gv, gw);
+                if (!tr_next) query(s, t, val, gu, gv, gw);
+                tr_cur = tr_next;
                 const bool adv = live && k + 2 < K;
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
@@ -917,11 +938,28 @@ template <int P, int LAYOUT, bool UNI, int SHADE, bool EXT>
 static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(float4) * a.tf_n;
     auto kern = render_kernel<P, LAYOUT, UNI, SHADE, EXT>;
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     constexpr int kThreads = RenderShape<P, LAYOUT>::THREADS;
-    {   // shared-memory carveout: enough for MINB resident CTAs but at least
+    // launch shape per (device, TF size): the carveout and the occupancy query
+    // cost several driver calls, which dominated a tiny frame's launch (C1:
+    // 64 x 64 pixels); cached here, computed on first use
+    struct Shape {
+        int sms = 0, occ = 0;
+        size_t smem = (size_t)-1;
+    };
+    static Shape cache[64];
+    static std::mutex mu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Shape sh;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev < 64) sh = cache[dev];
+    }
+    if (sh.smem != smem) {
+        sh.smem = smem;
+        sh.sms = 148;
+        cudaDeviceGetAttribute(&sh.sms, cudaDevAttrMultiProcessorCount, dev);
+        // shared-memory carveout: enough for MINB resident CTAs but at least
         // MFA_CARVE_FLOOR (8 %), the rest of the unified 256 KB is L1 (the block
         // caches live there).  The driver's default (more shared memory) measured
         // C5 -15%, C4 -37%; a 25 % floor: C5 -1 %, C4 -1.4 %
@@ -936,10 +974,13 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
             }
         }
         if (pct >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        sh.occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sh.occ, kern, kThreads, smem);
+        if (sh.occ < 1) sh.occ = 1;
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev < 64) cache[dev] = sh;
     }
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
-    if (occ < 1) occ = 1;
-    int64_t grid = (int64_t)sms * occ;
+    int64_t grid = (int64_t)sh.sms * sh.occ;
     const int64_t need = (a.n_units + kThreads / 32 - 1) / (kThreads / 32);
     if (grid > need) grid = need > 0 ? need : 1;
     kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
@@ -949,16 +990,22 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
 template <int P, int LAYOUT, bool EXT>
 static cudaError_t dispatch_render_l(const RenderArgs& a, bool uni, int shade, cudaStream_t st) {
     constexpr bool kSkip = !EXT && RenderShape<P, LAYOUT>::CACHE;   // SHADE = 2 is built for the hot path only
+    constexpr bool kSkipBlk = kSkip && LAYOUT == kBezier;             // SHADE = 3 needs the macro-block bounds
     if (shade == 2 && !kSkip) shade = 1;
+    if (shade == 3 && !(kSkipBlk && a.tbits)) shade = 1;
     if (uni) {
         if (shade == 0) return launch_render_t<P, LAYOUT, true, 0, EXT>(a, st);
         if constexpr (kSkip)
             if (shade == 2) return launch_render_t<P, LAYOUT, true, 2, EXT>(a, st);
+        if constexpr (kSkipBlk)
+            if (shade == 3) return launch_render_t<P, LAYOUT, true, 3, EXT>(a, st);
         return launch_render_t<P, LAYOUT, true, 1, EXT>(a, st);
     }
     if (shade == 0) return launch_render_t<P, LAYOUT, false, 0, EXT>(a, st);
     if constexpr (kSkip)
         if (shade == 2) return launch_render_t<P, LAYOUT, false, 2, EXT>(a, st);
+    if constexpr (kSkipBlk)
+        if (shade == 3) return launch_render_t<P, LAYOUT, false, 3, EXT>(a, st);
     return launch_render_t<P, LAYOUT, false, 1, EXT>(a, st);
 }
 

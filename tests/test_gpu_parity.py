@@ -484,24 +484,27 @@ def test_many_renders_in_flight_on_distinct_streams():
 
 @pytest.mark.parametrize("c,layout", [(2, "auto"), (3, "auto"), (5, "auto"), (5, "quads"), (1, "auto")])
 def test_skip_transparent_gradient_is_bit_identical(c, layout):
-    """NEXT-1 variant (shading = 2): the gradient contraction and Phong are
-    skipped where the TF opacity is 0; those samples composite with weight 0,
-    so the image and the composited-sample count equal the shaded render's
-    bit for bit (C5 on a reduced 4-view batch, both layouts)."""
+    """NEXT-1 variants: shading = 2 skips the gradient contraction and Phong
+    where the TF opacity is 0; shading = 3 skips whole samples in macro blocks
+    whose value range maps to opacity 0 (Bezier layout).  Those samples
+    composite with weight 0, so the image and the composited-sample count
+    equal the shaded render's bit for bit (C5 on a reduced 4-view batch, both
+    layouts)."""
     import dataclasses
     kw = {"n_views": 4, "width": 640, "height": 360} if c == 5 else {}
     w = workload(c, **kw)
     m = gpu_model(c, layout) if not kw else __import__("paper_2204_11762_b200").Model.from_workload(w, layout=layout)
     tf = cuda(w.tf)
     res = []
-    for sh in (1, 2):
+    for sh in (1, 2, 3):
         prm = dataclasses.replace(w.params, shading=sh)
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         img = m.render(w.cameras, tf, w.v_lo, w.v_hi, prm, samples=cnt)
         torch.cuda.synchronize()
         res.append((img.cpu().numpy(), int(cnt.item())))
-    np.testing.assert_array_equal(res[0][0], res[1][0])
-    assert res[0][1] == res[1][1]
+    for other in res[1:]:
+        np.testing.assert_array_equal(res[0][0], other[0])
+        assert res[0][1] == other[1]
 
 
 def test_bricks_layout_footprint_and_full_size_c5():
