@@ -598,6 +598,20 @@ def secondary_kernels(w, m, c, p, img, tf, stream):
         del ml, out_l
         torch.cuda.empty_cache()
     res["layouts"] = lay
+    # NEXT-1 variant on the bench workload: whole samples skipped where the TF
+    # opacity is provably 0 (shading = 3; bit-identical image) -- frames/s
+    if int(w.params.shading) == 1 and m.info()["layout"] == "bezier":
+        import dataclasses
+        p3 = dataclasses.replace(w.params, shading=3)
+        out3 = torch.empty((len(w.cameras), w.cameras[0].height, w.cameras[0].width, 4), device="cuda")
+        cnt3 = torch.zeros(1, dtype=torch.int64, device="cuda")
+        ms = _time(lambda: m.render(w.cameras, tf, w.v_lo, w.v_hi, p3, out=out3, samples=cnt3), 2, stream)
+        res["skip_transparent_blocks"] = {
+            "ms_per_step": ms, "frames_per_s": len(w.cameras) / (ms / 1e3),
+            "composited_samples_per_s": int(cnt3.item()) / 3 / (ms / 1e3),
+            "note": "shading = 3: samples whose 2^3-span group maps to TF opacity 0 are not queried (empty-space "
+                    "skip); image bit-identical to the headline's; not value+gradient samples, so not the metric"}
+        del out3
     if img is not None and img.shape[0] >= 2 and img.dtype == torch.float32:
         a, b = img[0], img[1]
         ws = torch.empty(int(__import__("paper_2204_11762_b200")._lib.lib().mfa_image_quality_workspace(
