@@ -149,7 +149,9 @@ mfa_status mfa_model_destroy(mfa_model m);
  *             by the number of points outside [0,1]^3 or NaN.  Those points
  *             get NaN outputs (batched form of S:74's domain error, R-18).
  * n == 0 is valid and enqueues nothing.
- * For n >= 2^16 the call takes the binned path of mfa_eval_batch_ws with
+ * For n >= 2^16 on a model larger than 64 MiB (one that does not stay in
+ * L2; smaller models are gathered directly in input order, which is faster
+ * for them) the call takes the binned path of mfa_eval_batch_ws with
  * STREAM-ORDERED scratch (cudaMallocAsync / cudaFreeAsync on `stream` from
  * the device's default memory pool, ~20 B per point; the pool's release
  * threshold is raised once so the blocks stay cached between calls); if the
@@ -162,7 +164,7 @@ mfa_status mfa_eval_batch(mfa_model m, int64_t n, const float* u, const float* v
 /*
  * mfa_eval_batch_ws -- mfa_eval_batch with a caller-owned device workspace of
  * at least mfa_eval_workspace_bytes(m, n) bytes (~20 B per point).  For
- * n >= 2^16 the points are first grouped by a coarse parameter-space bin
+ * n >= 2^16 (and a model larger than 64 MiB) the points are first grouped by a coarse parameter-space bin
  * (~8^3 knot spans per bin; a counting sort into (u, v, w, index) records)
  * and evaluated in bin order, results written at their original indices:
  * neighbouring points then share control-point neighbourhoods in L1/L2

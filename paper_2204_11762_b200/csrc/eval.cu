@@ -386,7 +386,7 @@ mfa_status launch_eval(const Model* m, int64_t n, const float* u, const float* v
     a.rec = nullptr;
     a.out4 = nullptr;
     a.pos = nullptr;
-    if (ws && n >= (int64_t)1 << 16 && n < ((int64_t)1 << 31) && ws_bytes >= eval_workspace_bytes(m, n)) {
+    if (ws && bin_worthwhile(m, n) && ws_bytes >= eval_workspace_bytes(m, n)) {
         const BinnedPoints bp = bin_points(m, n, u, v, w, ws, st);
         a.rec = bp.rec;
         a.out4 = bp.rec;   // results overwrite the record a thread has just read

@@ -213,8 +213,7 @@ extern "C" size_t mfa_hessian_workspace_bytes(mfa_model h, int64_t n) {
 extern "C" mfa_status mfa_eval_hessian(mfa_model h, int64_t n, const float* u, const float* v, const float* w,
                                        float* value, float* grad, float* hess, unsigned long long* n_domain_errors,
                                        mfa_stream stream) {
-    if (h && n >= ((int64_t)1 << 16) && n < ((int64_t)1 << 31) &&
-        check_device(reinterpret_cast<const Model*>(h)) == MFA_OK) {
+    if (h && check_device(reinterpret_cast<const Model*>(h)) == MFA_OK && bin_worthwhile(reinterpret_cast<const Model*>(h), n)) {
         // the binned path with stream-ordered scratch (no caller workspace)
         const size_t bytes = hessian_workspace_bytes(reinterpret_cast<const Model*>(h), n);
         void* ws = scratch_alloc(bytes, (cudaStream_t)stream);
@@ -263,7 +262,7 @@ extern "C" mfa_status mfa_eval_hessian_ws(mfa_model h, int64_t n, const float* u
     if (workspace && workspace_bytes < hessian_workspace_bytes(m, n))
         return fail(MFA_ERR_INVALID_ARG, "workspace smaller than mfa_hessian_workspace_bytes()");
     const int* pos = nullptr;
-    if (workspace && n >= (int64_t)1 << 16 && n < ((int64_t)1 << 31)) {
+    if (workspace && bin_worthwhile(m, n)) {
         const BinnedPoints bp = bin_points(m, n, u, v, w, workspace, st);
         a.rec = bp.rec;
         pos = bp.pos;

@@ -217,6 +217,13 @@ struct BinnedPoints {
     int* pos;
 };
 size_t bin_workspace_bytes(const Model* m, int64_t n);
+// binning pays only when the model does not stay in L2: a model of at most
+// kBinModelBytes is gathered directly in input order (C2, 56 MB of Bezier
+// blocks: 24 G vs 10 G points/s binned; C3 quads, 722 MB: 6.4 vs 13.1)
+constexpr int64_t kBinModelBytes = 64ll << 20;
+inline bool bin_worthwhile(const Model* m, int64_t n) {
+    return n >= ((int64_t)1 << 16) && n < ((int64_t)1 << 31) && m->device_bytes > kBinModelBytes;
+}
 BinnedPoints bin_points(const Model* m, int64_t n, const float* u, const float* v, const float* w, void* ws,
                         cudaStream_t st);
 mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,

@@ -680,7 +680,7 @@ extern "C" mfa_status mfa_eval_batch(mfa_model h, int64_t n, const float* u, con
     mfa_status s = check_device(m);
     if (s != MFA_OK) return s;
     cudaStream_t st = (cudaStream_t)stream;
-    if (n >= ((int64_t)1 << 16) && n < ((int64_t)1 << 31)) {
+    if (bin_worthwhile(m, n)) {
         // the binned path with stream-ordered scratch (no caller workspace)
         const size_t bytes = eval_workspace_bytes(m, n);
         void* ws = scratch_alloc(bytes, st);
