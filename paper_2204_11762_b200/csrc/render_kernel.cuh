@@ -39,6 +39,9 @@
 #ifndef MFA_VIEW_ORDER   // with MFA_VIEW_GROUP > 1: 1 = per supertile, 2 = per supertile row, 3 = per tile
 #define MFA_VIEW_ORDER 1
 #endif
+#ifndef MFA_BULK_PF   // experiment: bulk async prefetch of the block of the sample after next into shared memory
+#define MFA_BULK_PF 0
+#endif
 #ifndef MFA_PREFETCH_NEXT   // experiment: 1 / 2 = prefetch the predicted next block into L1 / L2
 #define MFA_PREFETCH_NEXT 0
 #endif
@@ -271,6 +274,39 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
     for (int v = threadIdx.x; v < args.n_views; v += blockDim.x) s_frame[v] = args.frames[v];
 #endif
     for (int i = threadIdx.x; i < args.tf_n; i += blockDim.x) s_tf[i] = __ldg(args.tf + i);
+#if MFA_BULK_PF
+    // experiment: the block of the sample after next is prefetched by a bulk
+    // async copy (cp.async.bulk, completion on a per-thread mbarrier) into a
+    // per-thread shared-memory slot a whole iteration before it is needed
+    constexpr bool kPF = BEZ && CACHE && !EXT && !UNI && P == 3;
+    constexpr int kPFT = kPF ? RenderShape<P, LAYOUT>::THREADS : 1;
+    __shared__ __align__(16) float s_pf[kPFT][kPF ? 68 : 4];   // 256 B + 16 B pad: conflict-free float4 reads
+    __shared__ __align__(8) unsigned long long s_mbar[kPFT];
+    if constexpr (kPF) {
+        const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar[threadIdx.x]);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    int pf_key = -1;
+    unsigned pf_phase = 0;
+    bool pf_pending = false;
+    auto pf_wait = [&]() {
+        if constexpr (kPF) {
+            const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar[threadIdx.x]);
+            asm volatile(
+                "{\n\t.reg .pred P1;\n\t"
+                "LAB_WAIT:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                "@P1 bra DONE;\n\t"
+                "bra LAB_WAIT;\n\t"
+                "DONE:\n\t}" ::"r"(mb),
+                "r"(pf_phase)
+                : "memory");
+            pf_phase ^= 1u;
+            pf_pending = false;
+        }
+    };
+#endif
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -803,6 +839,51 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 float t[3], gs1[3];
                 locate(s, t, gs1, multi_tag);
                 const bool tr_next = transparent(s);
+#if MFA_BULK_PF
+                if constexpr (kPF) {
+                    const int e = (s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
+                    if (!tr_next && e != nb_key) {
+                        if (pf_pending && pf_key == e) {   // prefetched one iteration ago
+                            pf_wait();
+                            const float4* sl = reinterpret_cast<const float4*>(&s_pf[threadIdx.x][0]);
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) {
+                                const float4 x = sl[q];
+                                nb[q >> 2][q & 3][0] = x.x;
+                                nb[q >> 2][q & 3][1] = x.y;
+                                nb[q >> 2][q & 3][2] = x.z;
+                                nb[q >> 2][q & 3][3] = x.w;
+                            }
+                        } else {
+                            load_bblock<P>(bez_block_at<P>(args.Q, args.bg, e), nb);
+                        }
+                        nb_key = e;
+                    }
+                    if (live) {   // predict the block of the sample after next (one crossing per axis)
+                        int s2[3];
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            const int d2 = nu_offset(args.ax[i], F[i] + DF[i], nu[i]);
+                            s2[i] = s[i] + (d2 >= nu[i].wsh ? 1 : 0) - (d2 < 0 && s[i] > 0 ? 1 : 0);
+                        }
+                        const int e2 = (s2[2] * args.bg.S1 + s2[1]) * args.bg.S0 + s2[0];
+                        if (e2 != nb_key && !(pf_pending && pf_key == e2)) {
+                            if (pf_pending) pf_wait();   // the slot is reused
+                            const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar[threadIdx.x]);
+                            const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_pf[threadIdx.x][0]);
+                            const float* src = reinterpret_cast<const float*>(bez_block_at<P>(args.Q, args.bg, e2));
+                            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(256)
+                                         : "memory");
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                                "l"(src), "r"(256), "r"(mb)
+                                : "memory");
+                            pf_key = e2;
+                            pf_pending = true;
+                        }
+                    }
+                } else
+#endif
                 if (!tr_next) fetch(s);
 #if MFA_PREFETCH_NEXT
                 if constexpr (BEZ && !UNI) {
@@ -921,6 +1002,9 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         }
         my_samples += (unsigned)k;
     }
+#if MFA_BULK_PF
+    if (pf_pending) pf_wait();   // no bulk copy may still be writing this CTA's shared memory at exit
+#endif
     if (args.samples) {   // 64-bit warp sum (a warp may composite more than 2^32 samples)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, o);
