@@ -756,7 +756,10 @@ def shared_host_image(V, H, W, el, rank, world):
     os.close(fd)
     t = torch.frombuffer(mm, dtype=torch.uint8)
     cr = torch.cuda.cudart()
-    reg = cr.cudaHostRegister(t.data_ptr(), nbytes, 0) == 0 if hasattr(cr, "cudaHostRegister") else False
+    try:   # page-lock the mapping so this rank's D2H copies run at PCIe speed (correct without it)
+        reg = int(cr.cudaHostRegister(t.data_ptr(), nbytes, 0)) == 0
+    except Exception:
+        reg = False
 
     def cleanup():
         nonlocal t

@@ -154,7 +154,7 @@ mfa_status mfa_model_destroy(mfa_model m);
  * for them) the call takes the binned path of mfa_eval_batch_ws with
  * STREAM-ORDERED scratch (cudaMallocAsync / cudaFreeAsync on `stream` from
  * the device's default memory pool, ~20 B per point; the pool's release
- * threshold is raised once so the blocks stay cached between calls); if the
+ * threshold is raised once to 8 GiB so the blocks stay cached between calls); if the
  * pool cannot serve it, the unbinned kernel runs instead (same outputs).
  * ---------------------------------------------------------------------- */
 mfa_status mfa_eval_batch(mfa_model m, int64_t n, const float* u, const float* v, const float* w,

@@ -695,9 +695,9 @@ extern "C" mfa_status mfa_eval_batch(mfa_model h, int64_t n, const float* u, con
 
 // Stream-ordered scratch for the calls without a caller workspace
 // (mfa_eval_batch, mfa_eval_hessian): cudaMallocAsync from the device's
-// default memory pool, whose release threshold is raised once per device so
-// freed blocks stay cached for the next call (no cudaMalloc / sync on the
-// hot path).  NULL if the pool cannot serve it (the caller then runs the
+// default memory pool, whose release threshold is raised once per device (to
+// 8 GiB, as the encoder's) so freed blocks stay cached for the next call (no
+// cudaMalloc / sync on the hot path).  NULL if the pool cannot serve it (the caller then runs the
 // unbinned kernels).
 void* mfa::scratch_alloc(size_t bytes, cudaStream_t st) {
     static std::mutex mu;
@@ -709,7 +709,7 @@ void* mfa::scratch_alloc(size_t bytes, cudaStream_t st) {
         if (dev < 64 && !(warmed >> dev & 1)) {
             cudaMemPool_t pool;
             if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t thr = UINT64_MAX;
+                uint64_t thr = 8ULL << 30;   // keep up to 8 GiB cached (the encoder's keep_pool uses the same)
                 cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
             }
             warmed |= (uint64_t)1 << dev;
