@@ -785,8 +785,9 @@ def run_all_configs(args):
     from paper_2204_11762_b200 import Model, roofline as RL, workloads as WL
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream()
-    for c in (1, 2, 3, 4, 5):
-        w = WL.make_config(c)
+    runs = [(c, None) for c in (1, 2, 3, 4, 5)] + [(1, 64), (2, 64)]   # + small frames batched 64 per launch
+    for c, nv in runs:
+        w = WL.make_config(c, n_views=nv) if nv else WL.make_config(c)
         m = Model.from_workload(w, layout=args.layout)
         info = m.info()
         tf = torch.from_numpy(w.tf).cuda()
@@ -795,7 +796,7 @@ def run_all_configs(args):
         img = torch.empty((V, H, W, 4), device="cuda")
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         # small frames: K launches per timed step so each step lasts >= ~20 ms
-        reps = max(1, int(round(0.02 / max(1e-6, 1e-3 * {1: 0.01, 2: 0.25, 3: 0.9, 4: 17.0, 5: 700.0}[c]))))
+        reps = max(1, int(round(0.02 / max(1e-6, 1e-3 * {1: 0.01, 2: 0.25, 3: 0.9, 4: 17.0, 5: 700.0}[c] * (nv or 1)))))
 
         def step():
             for _ in range(reps):
@@ -824,7 +825,10 @@ def run_all_configs(args):
             "metric": METRIC, "value": samples / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "dtype": "f32",
             "data": "synthetic (seeded generator of the BASELINE.json config recipe; no dataset)",
-            "config": {"workload": w.name, "views": V, "width": W, "height": H, "degree": w.degree,
+            "config": {"workload": w.name + (f" x{nv} views per launch" if nv else ""), "views": V, "width": W,
+                       "height": H, "degree": w.degree,
+                       "batch": (None if not nv else ("64 copies of the same orthographic view" if c == 1 else
+                                                      "64 seeded orbit views of the config's camera model")),
                        "layout": info["layout"], "launches_per_step": reps * ((V + 63) // 64),
                        "model_bytes": info["model_bytes"], "device_bytes": info["device_bytes"],
                        "footprint_ratio": info["device_bytes"] / info["model_bytes"], "create_ms": info["create_ms"]},
