@@ -460,13 +460,28 @@ __device__ __forceinline__ float nu_gscale(const AxisArgs& A, const NUAxis& st) 
 #endif
 }
 
+#ifndef MFA_NU_UCMP   // 1: crossings in both directions by one unsigned compare (with MFA_NU_SHIFTCMP): C5 +1.6 %
+#define MFA_NU_UCMP 1
+#endif
+
 // the span-local offset in units of 2^dshift (negative before the span)
 __device__ __forceinline__ int nu_offset(const AxisArgs& A, long long F, const NUAxis& st) {
     return (int)((F - st.lo) >> A.dshift);
 }
 
 __device__ __forceinline__ void nu_cross(const AxisArgs& A, long long F, NUAxis& st) {
-#if MFA_NU_SHIFTCMP
+#if MFA_NU_SHIFTCMP && MFA_NU_UCMP
+    // one unsigned compare catches both directions: d < 0 wraps above every
+    // wsh (a backward crossing), d >= wsh is a forward one; the direction is
+    // the sign of d; span 0 never steps below 0 (a negative d there is exit-face
+    // rounding: the same record is reloaded and t clamps to 0)
+    const int d = nu_offset(A, F, st);
+    if ((unsigned)d >= (unsigned)st.wsh) {
+        st.s = max(st.s + ((d >> 31) | 1), 0);
+        nu_load(A, st);
+    }
+    return;
+#elif MFA_NU_SHIFTCMP
     const int d = nu_offset(A, F, st);
     const bool fwd = d >= st.wsh;
     const bool bwd = d < 0 && st.s > 0;
@@ -474,10 +489,12 @@ __device__ __forceinline__ void nu_cross(const AxisArgs& A, long long F, NUAxis&
     const bool fwd = F >= st.hi;
     const bool bwd = F < st.lo && st.s > 0;
 #endif
+#if !(MFA_NU_SHIFTCMP && MFA_NU_UCMP)
     if (fwd || bwd) {
         st.s += fwd ? 1 : -1;
         nu_load(A, st);
     }
+#endif
 }
 
 template <bool MULTI = true>
@@ -487,7 +504,11 @@ __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxi
     // without the check, MULTI = false, for launches where no axis needs it)
 #if MFA_NU_SHIFTCMP
     int d = nu_offset(A, F, st);
+#if MFA_NU_UCMP
+    if (MULTI && A.multi && (unsigned)d >= (unsigned)st.wsh) {
+#else
     if (MULTI && A.multi && (d >= st.wsh || (d < 0 && st.s > 0))) {
+#endif
         int s = st.s;
         while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
         while (s > 0 && F < __ldg(A.kfx + s)) --s;
@@ -505,8 +526,14 @@ __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxi
     }
     int d = (int)((F - st.lo) >> A.dshift);
 #endif
+#if MFA_NU_SHIFTCMP
+    // d < wsh <= 2^23 - 1 inside the span; negative only for exit-face rounding
+    // on span 0; the mask keeps the exponent intact whatever happens
+    const float fd = __int_as_float(0x4b000000 | (max(d, 0) & 0x7fffff)) - 8388608.0f;
+#else
     d = min(max(d, 0), 8388607);
     const float fd = __int_as_float(0x4b000000 | d) - 8388608.0f;
+#endif
     return fd * st.tsc;
 }
 

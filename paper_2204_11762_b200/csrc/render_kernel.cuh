@@ -39,6 +39,9 @@
 #ifndef MFA_VIEW_ORDER   // with MFA_VIEW_GROUP > 1: 1 = per supertile, 2 = per supertile row, 3 = per tile
 #define MFA_VIEW_ORDER 1
 #endif
+#ifndef MFA_PRED_ADV   // experiment: the sample advance as a predicated add instead of a select
+#define MFA_PRED_ADV 0
+#endif
 #ifndef MFA_BULK_PF   // experiment: bulk async prefetch of the block of the sample after next into shared memory
 #define MFA_BULK_PF 0
 #endif
@@ -925,7 +928,11 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
                     gs[i] = gs1[i];
+#if MFA_PRED_ADV
+                    if (adv) F[i] += DF[i];   // predicated 64-bit add
+#else
                     F[i] += adv ? DF[i] : 0;
+#endif
                 }
                 k += live ? 1 : 0;
                 live = live && !(A > args.o_max) && k < K;
