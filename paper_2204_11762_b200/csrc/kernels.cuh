@@ -505,7 +505,9 @@ __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxi
 #if MFA_NU_SHIFTCMP
     int d = nu_offset(A, F, st);
 #if MFA_NU_UCMP
-    if (MULTI && A.multi && (unsigned)d >= (unsigned)st.wsh) {
+    // (no A.multi test: on an axis whose spans are all wider than a step the
+    // compare is simply never true)
+    if (MULTI && (unsigned)d >= (unsigned)st.wsh) {
 #else
     if (MULTI && A.multi && (d >= st.wsh || (d < 0 && st.s > 0))) {
 #endif
@@ -529,7 +531,9 @@ __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxi
 #if MFA_NU_SHIFTCMP
     // d < wsh <= 2^23 - 1 inside the span; negative only for exit-face rounding
     // on span 0; the mask keeps the exponent intact whatever happens
-    const float fd = __int_as_float(0x4b000000 | (max(d, 0) & 0x7fffff)) - 8388608.0f;
+    unsigned bits;   // (max(d, 0) & 0x7fffff) | 0x4b000000 in one LOP3
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(bits) : "r"(max(d, 0)), "r"(0x7fffff), "r"(0x4b000000));
+    const float fd = __uint_as_float(bits) - 8388608.0f;
 #else
     d = min(max(d, 0), 8388607);
     const float fd = __int_as_float(0x4b000000 | d) - 8388608.0f;
