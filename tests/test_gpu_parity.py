@@ -549,3 +549,62 @@ def test_malformed_tile_entries_are_skipped():
     for out in (guard, img):
         assert torch.equal(out[:2], full)
         assert (out[2:] == -7.0).all()
+
+
+def test_render_host_views_and_reuse():
+    """mfa_render_host_views writes each view to its own host buffer (any
+    order, e.g. a rank's views into a shared host image); repeated host
+    renders reuse the model-owned staging, and a larger image after a smaller
+    one grows it -- every result equals the device render."""
+    from paper_2204_11762_b200 import Model
+    w = workload(2, width=96, height=64, n_views=5)
+    m = Model.from_workload(w)
+    tf = cuda(w.tf)
+    dev = m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params).cpu().numpy()
+    order = [3, 0, 4]
+    bufs = [torch.empty((64, 96, 4), dtype=torch.float32).pin_memory() for _ in order]
+    for _ in range(2):   # the second call reuses the staging buffers
+        m.render_host_views([w.cameras[v] for v in order], w.tf, w.v_lo, w.v_hi, w.params,
+                            [b.data_ptr() for b in bufs])
+        for v, b in zip(order, bufs):
+            np.testing.assert_array_equal(b.numpy(), dev[v])
+    w2 = workload(2, width=200, height=150, n_views=2)   # larger views: the staging grows
+    dev2 = m.render(w2.cameras, tf, w2.v_lo, w2.v_hi, w2.params).cpu().numpy()
+    host2 = torch.empty((2, 150, 200, 4), dtype=torch.float32).pin_memory()
+    m.render_host(w2.cameras, w2.tf, w2.v_lo, w2.v_hi, w2.params, host2)
+    np.testing.assert_array_equal(host2.numpy(), dev2)
+
+
+def test_transparent_skip_in_tiled_scatter_path():
+    """shading = 3 through the multi-GPU tile path (tiles stored at their image
+    positions): bit-identical to the full-frame shaded render."""
+    import dataclasses
+
+    from paper_2204_11762_b200 import Model, dist as D
+    w = workload(5, width=320, height=180, n_views=3)
+    m = Model.from_workload(w)
+    tf = cuda(w.tf)
+    full = m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params)
+    p3 = dataclasses.replace(w.params, shading=3)
+    img = torch.full_like(full, -1.0)
+    for lst in D.assign_units(3, 320, 180, 2, "views", pad=False):
+        m.render(w.cameras, tf, w.v_lo, w.v_hi, p3, tiles=cuda(lst), out=img, scatter=True)
+    torch.cuda.synchronize()
+    assert torch.equal(img, full)
+
+
+@pytest.mark.parametrize("layout", ["auto", "quads", "bricks", "bezier"])
+def test_model_info_footprint(layout):
+    """mfa_model_info reports the grid bytes, the device bytes of the chosen
+    layout (bricks <= 2x the grid) and the create time."""
+    from paper_2204_11762_b200 import Model
+    w = workload(2)
+    m = Model.from_workload(w, layout=layout)
+    info = m.info()
+    assert info["model_bytes"] == 4 * 64 ** 3
+    assert info["create_ms"] > 0
+    ratio = info["device_bytes"] / info["model_bytes"]
+    if info["layout"] == "bricks":
+        assert ratio <= 2.0
+    else:
+        assert ratio > 2.0
