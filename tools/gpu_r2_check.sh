@@ -1,8 +1,7 @@
 #!/bin/bash
-# round-2 GPU check: the -m gpu suite, the 1-GPU rank emulation (C5, 8 ranks),
-# bench --gpus 2 on one GPU (functional), the default bench line
-python -m pytest tests -m gpu -x -q > gpurun_out/r2_gputest.log 2>&1; tail -3 gpurun_out/r2_gputest.log
-timeout 900 python bench.py --emulate 8 --steps 1 > gpurun_out/r2_emulate_c5.json 2> gpurun_out/r2_emulate_c5.err; tail -c 3000 gpurun_out/r2_emulate_c5.json; tail -3 gpurun_out/r2_emulate_c5.err
-timeout 900 python bench.py --emulate 8 --steps 2 --workload c4 > gpurun_out/r2_emulate_c4.json 2> gpurun_out/r2_emulate_c4.err; tail -c 2000 gpurun_out/r2_emulate_c4.json
-timeout 900 python bench.py --gpus 2 --steps 2 --warmup 3 --no-eval --no-cpu-baseline > gpurun_out/r2_bench_g2.json 2> gpurun_out/r2_bench_g2.err; tail -c 1500 gpurun_out/r2_bench_g2.json; tail -5 gpurun_out/r2_bench_g2.err
-timeout 900 python bench.py --steps 3 --warmup 3 --cpu-seconds 10 > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err; tail -c 1200 gpurun_out/r2_bench.json; tail -3 gpurun_out/r2_bench.err
+# round-end check of the committed state: GPU suite, smoke, default bench line,
+# the reference (oracle) arm
+python -m pytest tests -m gpu -q > gpurun_out/r2c_gputest.log 2>&1; tail -2 gpurun_out/r2c_gputest.log
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/r2c_bench.json 2> gpurun_out/r2c_bench.err; cut -c1-300 gpurun_out/r2c_bench.json; echo
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r2c_ref.json 2> gpurun_out/r2c_ref.err; cut -c1-300 gpurun_out/r2c_ref.json
