@@ -196,6 +196,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->tbits = nullptr;
     a->mm0 = m->mm[0];
     a->mm1 = m->mm[1];
+    a->mm_n = m->mm[0] * m->mm[1] * m->mm[2];
     void* tscratch = nullptr;
     if (shade == 3 && m->layout == kBezier && m->mmx && !(field || lights || curv)) {
         const int64_t nmac = (int64_t)m->mm[0] * m->mm[1] * m->mm[2];

@@ -117,6 +117,7 @@ struct RenderArgs {
     } curv;
     const unsigned* tbits;        // SHADE == 3: bit per macro block, 1 = the TF is transparent over its value range
     int mm0, mm1;                 // SHADE == 3: macro blocks along u, v
+    int mm_n;                     // SHADE == 3: macro blocks in all (bounds checks)
     ViewFrame frames[kMaxViewsPerLaunch];   // per view, computed on the host (compute_frame)
 };
 
@@ -528,6 +529,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         auto transparent = [&](const int (&s)[3]) -> bool {
             if constexpr (SHADE == 3) {
                 const int mi = ((s[2] >> kMacroLog) * args.mm1 + (s[1] >> kMacroLog)) * args.mm0 + (s[0] >> kMacroLog);
+                MFA_DCHECK(mi >= 0 && mi < args.mm_n);
                 return (__ldg(args.tbits + (mi >> 5)) >> (mi & 31)) & 1u;
             } else {
                 return false;

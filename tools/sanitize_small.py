@@ -4,6 +4,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import dataclasses
+
 import numpy as np
 import torch
 
@@ -11,7 +13,7 @@ from paper_2204_11762_b200 import Model, unpack_tiles, workloads as WL
 
 for c, kw in ((1, {}), (2, dict(width=96, height=64)), (5, dict(width=64, height=48, n_views=2))):
     w = WL.make_config(c, **kw)
-    for layout in ("quads", "bezier"):
+    for layout in ("quads", "bezier", "bricks"):
         m = Model.from_workload(w, layout=layout)
         u, v, ww = (torch.from_numpy(x).cuda() for x in WL.query_points(c, 4096))
         m.eval(u, v, ww)
@@ -21,6 +23,9 @@ for c, kw in ((1, {}), (2, dict(width=96, height=64)), (5, dict(width=64, height
         tiles = torch.tensor([[0, 0, 0], [len(w.cameras) - 1, 1, 1], [-1, -1, -1]], dtype=torch.int32).cuda()
         packed = m.render(w.cameras, tf, w.v_lo, w.v_hi, w.params, tiles=tiles, out_fp16=True)
         unpack_tiles(packed, tiles, len(w.cameras), w.cameras[0].width, w.cameras[0].height)
+        torch.cuda.synchronize()
+        for shading in (0, 2, 3):   # value only, gradient skip, transparent-block skip
+            m.render(w.cameras, tf, w.v_lo, w.v_hi, dataclasses.replace(w.params, shading=shading))
         torch.cuda.synchronize()
         print(c, layout, "ok", float(img.sum()))
 
@@ -49,3 +54,18 @@ fit_grid(g, 3, [WL.clamped_uniform_knots(n, 3) for n in (12, 11, 10)])
 encode_grid(g, 2, (4, 4, 4), 1e-3, 3, (20, 20, 20))
 torch.cuda.synchronize()
 print("fit/encode ok")
+
+# host-buffer renders (model-owned staging) and the IPC image buffer
+from paper_2204_11762_b200._lib import IpcBuffer  # noqa: E402
+
+w = WL.make_config(2, width=80, height=48, n_views=3)
+m = Model.from_workload(w)
+H, W = w.cameras[0].height, w.cameras[0].width
+host = torch.empty((3, H, W, 4), dtype=torch.float32).pin_memory()
+m.render_host(w.cameras, w.tf, w.v_lo, w.v_hi, w.params, host)
+m.render_host_views(w.cameras, w.tf, w.v_lo, w.v_hi, w.params, [host[i].data_ptr() for i in range(3)])
+buf = IpcBuffer(3 * H * W * 16)
+m.render(w.cameras, torch.from_numpy(w.tf).cuda(), w.v_lo, w.v_hi, w.params, out=buf.tensor((3, H, W, 4), torch.float32))
+torch.cuda.synchronize()
+del buf
+print("host/ipc ok")
