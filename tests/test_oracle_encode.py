@@ -112,3 +112,52 @@ def test_gb_regression_pin():
     c = E.fit(q, knots, 2)
     err, _ = E.residual(q, c, knots, 2)
     assert err.max() < 0.05
+
+
+def test_residual_affine_invariance():
+    """S:208 (R-28): the relative error is |f - q| / (max q - min q), so it is
+    unchanged when data and control values are both scaled by a and shifted by
+    b (the B-spline basis sums to one, so the spline of a c + b is a f + b)."""
+    r = np.random.default_rng(11)
+    q = r.uniform(-1.0, 2.0, (9, 8, 10))
+    knots = [E.uniform_knots(n, 2) for n in (6, 5, 5)]
+    c = E.fit(q, knots, 2)
+    err, per = E.residual(q, c, knots, 2)
+    for a, b in ((1.0, 100.0), (3.5, -7.0), (0.01, 5.0)):
+        err2, per2 = E.residual(a * q + b, a * c + b, knots, 2)
+        np.testing.assert_allclose(err2, err, rtol=1e-9, atol=1e-12)
+        for (p1, c1), (p2, c2) in zip(per, per2):
+            np.testing.assert_allclose(p2, p1, rtol=1e-9, atol=1e-12)
+            np.testing.assert_array_equal(c2, c1)
+
+
+def test_adaptive_midpoint_split_is_exact():
+    """S:191 / S:209: an offending span is split at its parameter midpoint.
+    q = (u - 1/2)_+^3 is a cubic spline with one simple knot at 1/2: from one
+    span per axis (4 control points, p = 3), the first refinement inserts 1/2
+    on every axis (each axis sees the u error through its max over the other
+    axes) and the refit reproduces q to rounding, so round 2 converges."""
+    mu, mv, mw = 17, 9, 9
+    u = E.params(mu)
+    line = np.where(u > 0.5, (u - 0.5) ** 3, 0.0)
+    q = np.broadcast_to(line[None, None, :], (mw, mv, mu)).copy()
+    knots, c, rep = E.adaptive(q, 3, (4, 4, 4), 1e-9, 6, (20, 20, 20))
+    rounds = rep["rounds"]
+    assert rep["converged"] and len(rounds) == 2 and rounds[-1][1] <= 1e-10
+    for d in range(3):
+        np.testing.assert_array_equal(knots[d], [0, 0, 0, 0, 0.5, 1, 1, 1, 1])
+
+
+def test_adaptive_sample_count_guard():
+    """R-28: only spans holding >= 2(p+1) samples are split (each half keeps
+    >= p+1 samples).  |u - 0.37| is not a spline, so the error stays above
+    e_max; with 12 x 9 x 9 samples and p = 3 the first round splits every
+    axis at 1/2, after which no span holds 8 samples: the loop stops
+    unconverged with exactly one inserted knot per axis."""
+    mu, mv, mw = 12, 9, 9
+    line = np.abs(E.params(mu) - 0.37)
+    q = np.broadcast_to(line[None, None, :], (mw, mv, mu)).copy()
+    knots, c, rep = E.adaptive(q, 3, (4, 4, 4), 1e-6, 6, (40, 40, 40))
+    assert not rep["converged"] and len(rep["rounds"]) == 2
+    for d in range(3):
+        np.testing.assert_array_equal(knots[d], [0, 0, 0, 0, 0.5, 1, 1, 1, 1])

@@ -2,8 +2,9 @@
 undetected (samples at t_in + k*step, TF normalised by v_hi, sigma inflated
 100x, the exit-window alternative disabled, every pixel shading-sensitive)
 are applied one at a time to a scratch copy of oracle/oracle.c, and the CPU
-oracle suite must FAIL on each (tools/mutation_check.py runs all 16 slips).
-No GPU."""
+oracle suite must FAIL on each; so must one slip each in the basis
+derivatives, the Hessian, the curvature operator, the encoder's refinement
+and the SSIM luma (tools/mutation_check.py runs all 42 slips).  No GPU."""
 import os
 import sys
 
@@ -13,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 import mutation_check as MC   # noqa: E402
 
-REVIEW_SLIPS = ("A2", "B", "C", "D", "E")
+REVIEW_SLIPS = ("A2", "B", "C", "D", "E", "O2a", "H1b", "C1a", "E5a", "Q4")
 
 
 def test_unmutated_copy_passes():

@@ -214,3 +214,34 @@ def test_error_map():
     assert (QM.error_map(a, a) == 0).all()
     d = QM.quantize8(a) - QM.quantize8(b)
     assert e[2, 3] == pytest.approx(math.sqrt((d[2, 3] ** 2).sum()), rel=1e-15)
+
+
+def test_ssim_luma_weights_and_c1_closed_form():
+    """S:492 / S:514: SSIM on BT.601 luma 0.299 R + 0.587 G + 0.114 B with
+    C1 = (0.01 * 255)^2.  Constant images: SSIM = (2 ya yb + C1) / (ya^2 +
+    yb^2 + C1); against black, a pure red / green / blue level 200 image gives
+    C1 / ((w * 200)^2 + C1) with w its luma weight."""
+    c1 = (0.01 * 255.0) ** 2
+    blk = np.zeros((12, 12, 4))
+    for ch, wgt in enumerate((0.299, 0.587, 0.114)):
+        a = np.zeros((12, 12, 4))
+        a[..., ch] = 200 / 255.0
+        y = wgt * 200.0
+        assert QM.ssim(a, blk) == pytest.approx(c1 / (y * y + c1), rel=1e-12)
+
+
+def test_ssim_c2_single_window_closed_form():
+    """C2 = (0.03 * 255)^2, 11 x 11 Gaussian window, sigma = 1.5.  On
+    an 11 x 11 image (one window) whose only non-zero luma is the centre pixel
+    y, against black: mu_a = g0 y, var_a = g0 (1 - g0) y^2 (g0 = the
+    normalised centre weight), mu_b = var_b = cov = 0, so
+    SSIM = C1 / (mu_a^2 + C1) * C2 / (var_a + C2)."""
+    c1, c2 = (0.01 * 255.0) ** 2, (0.03 * 255.0) ** 2
+    k = np.arange(11) - 5
+    g0 = 1.0 / np.exp(-(k[:, None] ** 2 + k[None, :] ** 2) / (2 * 1.5 ** 2)).sum()
+    a = np.zeros((11, 11, 4))
+    a[5, 5, :3] = 1.0                          # white centre: luma 255
+    y = 255.0
+    mu, var = g0 * y, g0 * (1 - g0) * y * y
+    want = c1 / (mu * mu + c1) * c2 / (var + c2)
+    assert QM.ssim(a, np.zeros((11, 11, 4))) == pytest.approx(want, rel=1e-12)
