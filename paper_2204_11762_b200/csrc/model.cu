@@ -910,15 +910,29 @@ static mfa_status render_host_impl(const Model* m, int32_t n_views, const mfa_ca
     const size_t px = (size_t)cams[0].width * cams[0].height;
     const size_t view_bytes = px * (prm->out_fp16 ? 8 : 16);
     cudaError_t e;
-    if (!H.copy) {
-        if ((e = cudaStreamCreateWithFlags(&H.copy, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
-        for (int i = 0; i < 2; ++i) {
-            if ((e = cudaEventCreateWithFlags(&H.rendered[i], cudaEventDisableTiming)) != cudaSuccess ||
-                (e = cudaEventCreateWithFlags(&H.copied[i], cudaEventDisableTiming)) != cudaSuccess)
-                return cuda_fail(e, "event");
+    // each resource on its own: a call that failed half way (out of memory)
+    // leaves the rest to the next one
+    if (!H.copy && (e = cudaStreamCreateWithFlags(&H.copy, cudaStreamNonBlocking)) != cudaSuccess) {
+        H.copy = nullptr;
+        return cuda_fail(e, "stream");
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (!H.rendered[i] && (e = cudaEventCreateWithFlags(&H.rendered[i], cudaEventDisableTiming)) != cudaSuccess) {
+            H.rendered[i] = nullptr;
+            return cuda_fail(e, "event");
         }
-        if ((e = cudaMalloc((void**)&H.tf, sizeof(float) * 4 * 1024)) != cudaSuccess) return cuda_fail(e, "tf");
-        if ((e = cudaMalloc((void**)&H.cnt, sizeof(unsigned long long))) != cudaSuccess) return cuda_fail(e, "count");
+        if (!H.copied[i] && (e = cudaEventCreateWithFlags(&H.copied[i], cudaEventDisableTiming)) != cudaSuccess) {
+            H.copied[i] = nullptr;
+            return cuda_fail(e, "event");
+        }
+    }
+    if (!H.tf && (e = cudaMalloc((void**)&H.tf, sizeof(float) * 4 * 1024)) != cudaSuccess) {
+        H.tf = nullptr;
+        return cuda_fail(e, "tf");
+    }
+    if (!H.cnt && (e = cudaMalloc((void**)&H.cnt, sizeof(unsigned long long))) != cudaSuccess) {
+        H.cnt = nullptr;
+        return cuda_fail(e, "count");
     }
     if (H.stage_bytes < view_bytes) {
         cudaStreamSynchronize(H.copy);

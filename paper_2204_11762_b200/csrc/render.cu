@@ -220,10 +220,10 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
         }
         a->queue = m->queue + slot;
         cudaError_t r = cudaMemsetAsync(a->queue, 0, sizeof(unsigned int), st);
-        if (r != cudaSuccess) return r;
-        r = (field || lights || curv) ? dispatch_render_ext(*a, m->p, m->layout, uni, shade, st)
-                                      : dispatch_render_main(*a, m->p, m->layout, uni, shade, st);
-        release_queue_slot(m, slot, st);
+        if (r == cudaSuccess)
+            r = (field || lights || curv) ? dispatch_render_ext(*a, m->p, m->layout, uni, shade, st)
+                                          : dispatch_render_main(*a, m->p, m->layout, uni, shade, st);
+        release_queue_slot(m, slot, st);   // also on failure: the slot must not stay pending
         return r;
     };
     if (tiles) {
