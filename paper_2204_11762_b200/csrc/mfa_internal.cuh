@@ -215,6 +215,11 @@ size_t eval_workspace_bytes(const Model* m, int64_t n);
 struct BinnedPoints {
     float4* rec;
     int* pos;
+    const unsigned* counts;   // points per bin (nbins + 1: the last bin holds points outside [0,1]^3)
+    const unsigned* cursor;   // after the scatter: end of bin b at cursor[b * stride]
+    int stride;
+    int nb[3];
+    int nbins;
 };
 size_t bin_workspace_bytes(const Model* m, int64_t n);
 // binning pays only when the model does not stay in L2: a model of at most
