@@ -278,9 +278,16 @@ typedef struct {
  * samples_out optional device counter: += the number of composited samples
  *             (each sample up to and including the ERT sample).
  * Deterministic: a pixel's value does not depend on tiling, view batching or
- * launch configuration.  Each launch takes one of 256 work-counter slots of
- * the model in turn: at most 256 renders of one model may be in flight at a
- * time (across all streams).
+ * launch configuration.  Each launch owns one of the model's 256 work-counter
+ * slots until its completion event fires (launches on the same stream reuse
+ * one slot in stream order); a launch that finds every slot held by an
+ * unfinished launch on another stream fails with MFA_ERR_UNSUPPORTED and
+ * enqueues nothing.
+ * Stream capture: the call enqueues only a memset, the kernel and an event
+ * record, so it can be captured into a CUDA graph (tests/test_gpu_parity.py
+ * checks that a replay is bit-identical to the eager call).  A replayed graph reuses the slot it was captured
+ * with: do not replay it concurrently with other renders of the same model
+ * on other streams.
  */
 mfa_status mfa_render(mfa_model m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                       const mfa_render_params* prm, const mfa_tiles* tiles, void* rgba_out,
