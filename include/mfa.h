@@ -285,9 +285,9 @@ typedef struct {
  * enqueues nothing.
  * Stream capture: the call enqueues only a memset, the kernel and an event
  * record, so it can be captured into a CUDA graph (tests/test_gpu_parity.py
- * checks that a replay is bit-identical to the eager call).  A replayed graph reuses the slot it was captured
- * with: do not replay it concurrently with other renders of the same model
- * on other streams.
+ * checks that a replay is bit-identical to the eager call).  A replayed
+ * graph reuses the slot it was captured with: do not replay it concurrently
+ * with other renders of the same model on other streams.
  */
 mfa_status mfa_render(mfa_model m, int32_t n_views, const mfa_camera* cams, const mfa_tf* tf,
                       const mfa_render_params* prm, const mfa_tiles* tiles, void* rgba_out,
