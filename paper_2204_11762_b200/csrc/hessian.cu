@@ -165,24 +165,45 @@ static cudaError_t launch_hess_t(const HessArgs& a, cudaStream_t st) {
 }
 
 // results of the sorted evaluation back to the caller's SoA arrays
+#ifndef MFA_HESS_ILP
+#define MFA_HESS_ILP 4
+#endif
 __global__ void __launch_bounds__(256) hess_gather_kernel(const float4* __restrict__ out, const int* __restrict__ pos,
                                                           int64_t n, float* __restrict__ value,
                                                           float* __restrict__ grad, float* __restrict__ hess) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = __ldg(pos + i);
-        const float4 a = __ldg(out + 3 * p), b = __ldg(out + 3 * p + 1), c = __ldg(out + 3 * p + 2);
-        if (value) value[i] = a.x;
-        if (grad) {
-            grad[i] = a.y;
-            grad[n + i] = a.z;
-            grad[2 * n + i] = a.w;
+    // MFA_HESS_ILP points per thread per iteration: their random 48-byte reads
+    // are independent, so more of them are in flight
+    constexpr int U = MFA_HESS_ILP;
+    const int64_t S = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += U * S) {
+        int64_t p[U];
+        float4 a[U], b[U], c[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) p[k] = i0 + k * S < n ? __ldg(pos + i0 + k * S) : 0;
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+            if (i0 + k * S < n) {
+                a[k] = __ldg(out + 3 * p[k]);
+                b[k] = __ldg(out + 3 * p[k] + 1);
+                c[k] = __ldg(out + 3 * p[k] + 2);
+            }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int64_t i = i0 + k * S;
+            if (i >= n) continue;
+            if (value) value[i] = a[k].x;
+            if (grad) {
+                grad[i] = a[k].y;
+                grad[n + i] = a[k].z;
+                grad[2 * n + i] = a[k].w;
+            }
+            hess[i] = b[k].x;
+            hess[n + i] = b[k].y;
+            hess[2 * n + i] = b[k].z;
+            hess[3 * n + i] = b[k].w;
+            hess[4 * n + i] = c[k].x;
+            hess[5 * n + i] = c[k].y;
         }
-        hess[i] = b.x;
-        hess[n + i] = b.y;
-        hess[2 * n + i] = b.z;
-        hess[3 * n + i] = b.w;
-        hess[4 * n + i] = c.x;
-        hess[5 * n + i] = c.y;
     }
 }
 
