@@ -59,7 +59,7 @@ def parse():
                          "opacity 0 are skipped entirely; identical image)")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: direct NVLink stores into rank 0's image (p2p) or packed tiles + NCCL all-gather")
-    ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier", "bricks"],
+    ap.add_argument("--layout", default="auto", choices=["auto", "quads", "bezier", "bricks", "bezier_grouped"],
                     help="control-point layout (default: the library's choice)")
     ap.add_argument("--assign", default="auto", choices=["auto", "views", "rows", "diagonal"],
                     help="N > 1: how (view, tile) units are dealt to ranks (dist.assign_units)")
@@ -455,7 +455,7 @@ def run_ours(args):
         ev = {"metric": "mfa_eval_batch points/s (value + 3 partials)", "value": pts, "points": 1 << 24,
               "ms": ems, "flops_per_point": fe, "achieved_tflops": pts * fe / 1e12,
               "frac_fp32": pts * fe / 1e12 / peak_tf, "hbm_io_bytes_per_point": 28,
-              "hbm_io_gbps": pts * 28 / 1e9}
+              "hbm_io_gbps": pts * 28 / 1e9, "layout": m.info()["layout"]}
         del u, v_, w_, outs
 
     # ---- secondary: NEXT-4 Hessian eval, NEXT-2 ground truth + metrics -----
@@ -580,8 +580,9 @@ def secondary_kernels(w, m, c, p, img, tf, stream):
     # the same render on the other control-point layouts (footprint / throughput
     # trade-off, P:133 / P:263): one warm-up and one timed launch each
     lay = {}
-    for layout in ("quads", "bricks", "bezier"):
-        if layout == m.info()["layout"] or (layout != "quads" and w.degree > 3):
+    for layout in ("quads", "bricks", "bezier", "bezier_grouped"):
+        if layout == m.info()["layout"] or (layout != "quads" and w.degree > 3) or \
+                (layout == "bezier_grouped" and w.degree != 3):
             continue
         try:
             ml = Model.from_workload(w, layout=layout)
@@ -595,12 +596,18 @@ def secondary_kernels(w, m, c, p, img, tf, stream):
         lay[layout] = {"samples_per_s": int(cnt_l.item()) / 2 / (ms / 1e3), "ms_per_step": ms,
                        "device_bytes": il["device_bytes"], "footprint_ratio": il["device_bytes"] / il["model_bytes"],
                        "create_ms": il["create_ms"]}
-        del ml, out_l
+        del out_l
+        # mfa_eval_batch (2^24 random points, value + gradient) on this layout
+        u, v_, w_ = (torch.from_numpy(x).cuda() for x in WL.query_points(c, 1 << 24))
+        outs = ml.eval(u, v_, w_)
+        ms = _time(lambda: ml.eval(u, v_, w_, out=outs), 2, stream)
+        lay[layout]["eval_points_per_s"] = (1 << 24) / (ms / 1e3)
+        del ml, u, v_, w_, outs
         torch.cuda.empty_cache()
     res["layouts"] = lay
     # NEXT-1 variant on the bench workload: whole samples skipped where the TF
     # opacity is provably 0 (shading = 3; bit-identical image) -- frames/s
-    if int(w.params.shading) == 1 and m.info()["layout"] == "bezier":
+    if int(w.params.shading) == 1 and m.info()["layout"].startswith("bezier"):
         import dataclasses
         p3 = dataclasses.replace(w.params, shading=3)
         out3 = torch.empty((len(w.cameras), w.cameras[0].height, w.cameras[0].width, 4), device="cuda")

@@ -18,7 +18,7 @@ MFA_OK = 0
 STATUS = {0: "MFA_OK", 1: "MFA_ERR_INVALID_ARG", 2: "MFA_ERR_KNOTS", 3: "MFA_ERR_UNSUPPORTED",
           4: "MFA_ERR_DOMAIN", 5: "MFA_ERR_CUDA", 6: "MFA_ERR_OOM", 7: "MFA_ERR_DEVICE"}
 TILE = 16
-LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2, "bricks": 3}
+LAYOUTS = {"auto": 0, "quads": 1, "bezier": 2, "bricks": 3, "bezier_grouped": 4}
 
 # C-ABI symbols declared in include/mfa.h (checked by tests/test_abi.py)
 EXPORTS = ("mfa_model_create", "mfa_model_create_ex", "mfa_model_info", "mfa_model_destroy", "mfa_eval_batch", "mfa_render",
@@ -267,7 +267,7 @@ class Model:
         _check(lib().mfa_model_info(self._h, C.byref(d)))
         return dict(degree=tuple(d.degree), nctrl=tuple(d.nctrl), uniform=tuple(d.uniform),
                     v_min=d.v_min, v_max=d.v_max, device_bytes=d.device_bytes, device=d.device,
-                    layout={1: "quads", 2: "bezier", 3: "bricks"}.get(d.layout, d.layout), model_bytes=d.model_bytes,
+                    layout={1: "quads", 2: "bezier", 3: "bricks", 4: "bezier_grouped"}.get(d.layout, d.layout), model_bytes=d.model_bytes,
                     create_ms=d.create_ms)
 
     def close(self):

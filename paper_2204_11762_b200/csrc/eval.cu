@@ -40,7 +40,8 @@ struct EvalArgs {
 template <int P, int LAYOUT, bool UNI, bool GRAD>
 __device__ __forceinline__ bool eval_point(const EvalArgs& args, const float (&q)[3], float& val, float& gu, float& gv,
                                            float& gw) {
-    constexpr bool BEZ = LAYOUT == kBezier;
+    constexpr bool BEZ = is_bez(LAYOUT);
+    constexpr int SEC = bez_sec(LAYOUT == kBezierG);
     gu = gv = gw = 0.f;
     if (!(q[0] >= 0.f && q[0] <= 1.f && q[1] >= 0.f && q[1] <= 1.f && q[2] >= 0.f && q[2] <= 1.f)) {
         val = gu = gv = gw = __int_as_float(0x7fc00000);
@@ -58,18 +59,18 @@ __device__ __forceinline__ bool eval_point(const EvalArgs& args, const float (&q
         }
     }
     if constexpr (BEZ) {
-        const float4* base = bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]);
+        const float4* base = bez_block<P, SEC>(args.Q, args.bg, s[0], s[1], s[2]);
         if (GRAD) {
             float r0[P + 1][P + 1];
-            load_bslab<P>(base, r0);
+            load_bslab<P, SEC>(base, r0);
             float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
             bernstein<P, false>(t[0], Bu);
             bernstein<P, true>(t[1], Bv);
             bernstein<P, false>(t[2], Bw);
-            contract_vg_bez<P>(base, r0, Bu, Bv, Bw, val, gu, gv, gw);
+            contract_vg_bez<P, SEC>(base, r0, Bu, Bv, Bw, val, gu, gv, gw);
         } else {
             float nb[P + 1][P + 1][P + 1];
-            load_bblock<P>(base, nb);
+            load_bblock<P, SEC>(base, nb);
             float Nu[P + 1], Nv[P + 1], Nw[P + 1];
             bernstein_value<P>(t[0], Nu);
             bernstein_value<P>(t[1], Nv);
@@ -199,7 +200,8 @@ __global__ void __launch_bounds__(kCellThreads) eval_cells_kernel(const __grid_c
             if (b < args.nbins) {   // the point's cell in its bin (points outside [0,1]^3 sit in bin nbins)
                 const float q[3] = {r.x, r.y, r.z};
 #pragma unroll
-                for (int d = 2; d >= 0; --d) {   // u fastest
+                for (int i = 0; i < 3; ++i) {   // u fastest (grouped Bezier layout: w fastest, the group axis)
+                    const int d = LAYOUT == kBezierG ? i : 2 - i;
                     const int c = (int)((q[d] * (float)args.nb[d] - (float)bc[d]) * (float)kCellSub);
                     key = key * kCellSub + min(max(c, 0), kCellSub - 1);
                 }
@@ -264,7 +266,7 @@ static cudaError_t launch_eval_s(const EvalArgs& a, cudaStream_t st) {
 
 template <int P, int LAYOUT, bool UNI, bool GRAD>
 static cudaError_t launch_eval_t(const EvalArgs& a, cudaStream_t st) {
-    if (LAYOUT == kBezier && a.rec && a.bin_cnt) {
+    if (is_bez(LAYOUT) && a.rec && a.bin_cnt) {
         eval_cells_kernel<P, LAYOUT, UNI, GRAD><<<(unsigned)(a.nbins + 1), kCellThreads, 0, st>>>(a);
         return cudaGetLastError();
     }
@@ -283,6 +285,8 @@ template <int P>
 static cudaError_t dispatch_eval(const EvalArgs& a, int layout, bool uni, bool grad, cudaStream_t st) {
     if constexpr (P <= 3) {
         if (layout == kBezier) return dispatch_eval_l<P, kBezier>(a, uni, grad, st);
+        if constexpr (P == 3)
+            if (layout == kBezierG) return dispatch_eval_l<P, kBezierG>(a, uni, grad, st);
         if (layout == kBricks) return dispatch_eval_l<P, kBricks>(a, uni, grad, st);
     }
     return dispatch_eval_l<P, kQuads>(a, uni, grad, st);

@@ -41,7 +41,8 @@ struct HessArgs {
 
 template <int P, int LAYOUT, bool UNI, bool SORTED>
 __global__ void __launch_bounds__(256) hessian_kernel(const __grid_constant__ HessArgs args) {
-    constexpr bool BEZ = LAYOUT == kBezier;
+    constexpr bool BEZ = is_bez(LAYOUT);
+    constexpr int SEC = bez_sec(LAYOUT == kBezierG);
     const int64_t n = args.n;
     unsigned errs = 0;
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < n; it += (int64_t)gridDim.x * blockDim.x) {
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(256) hessian_kernel(const __grid_constant__ He
                     nonuni_span_f32(args.ax[d], q[d], s[d], t[d], sc[d]);
                 }
             }
-            const float4* base = BEZ ? bez_block<P>(args.Q, args.bg, s[0], s[1], s[2])
+            const float4* base = BEZ ? bez_block<P, SEC>(args.Q, args.bg, s[0], s[1], s[2])
                                      : (LAYOUT == kBricks ? args.Q : args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]));
             PlainRef pe{0, 0};
             if constexpr (LAYOUT == kBricks) pe = plain_entry<P>(args.g, s[0], s[1], s[2]);
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(256) hessian_kernel(const __grid_constant__ He
             for (int c = 0; c <= P; ++c) {
                 float r[P + 1][P + 1];
                 if constexpr (BEZ)
-                    load_bslab<P>(bslab_ptr<P>(base, c), r);
+                    load_bslab<P, SEC>(bslab_ptr<P, SEC>(base, c), r);
                 else if constexpr (LAYOUT == kBricks)
                     load_pslab<P>(base, pe, c, r);
                 else
@@ -216,6 +217,9 @@ static cudaError_t dispatch_hess(const HessArgs& a, int layout, bool uni, cudaSt
     if constexpr (P <= 3) {
         if (layout == kBezier)
             return uni ? launch_hess_t<P, kBezier, true>(a, st) : launch_hess_t<P, kBezier, false>(a, st);
+        if constexpr (P == 3)
+            if (layout == kBezierG)
+                return uni ? launch_hess_t<P, kBezierG, true>(a, st) : launch_hess_t<P, kBezierG, false>(a, st);
         if (layout == kBricks)
             return uni ? launch_hess_t<P, kBricks, true>(a, st) : launch_hess_t<P, kBricks, false>(a, st);
     }

@@ -497,6 +497,17 @@ __device__ __forceinline__ void nu_cross(const AxisArgs& A, long long F, NUAxis&
 #endif
 }
 
+#if MFA_NU_SHIFTCMP && MFA_NU_UCMP
+// nu_cross with the offset d = nu_offset(A, F, st) already computed (the
+// render's early block load computes it one iteration ahead)
+__device__ __forceinline__ void nu_cross_d(const AxisArgs& A, int d, NUAxis& st) {
+    if ((unsigned)d >= (unsigned)st.wsh) {
+        st.s = max(st.s + ((d >> 31) | 1), 0);
+        nu_load(A, st);
+    }
+}
+#endif
+
 template <bool MULTI = true>
 __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxis& st) {
     // rare: crossed more than one span this step; impossible when every span is
@@ -585,7 +596,7 @@ __device__ __forceinline__ void horner3(const float (&c)[P + 1], float t, float&
 template <int P, int LAYOUT, bool UNI>
 __device__ __forceinline__ void basis3(const AxisArgs& A, int s, float t, float (&N)[P + 1], float (&D1)[P + 1],
                                        float (&D2)[P + 1]) {
-    if constexpr (LAYOUT == kBezier) {
+    if constexpr (is_bez(LAYOUT)) {
         constexpr BernPower<P> BP = make_bern_power<P>();
 #pragma unroll
         for (int a = 0; a <= P; ++a) {
@@ -966,15 +977,18 @@ struct BezBlock {
     static constexpr int FLOATS = (P + 1) * (P + 1) * ROW;
 };
 
-template <int P>
+// SEC: floats between a block's 32-byte sectors (bez_sec: 8 for kBezier, 32
+// for the grouped kBezierG, p = 3)
+template <int P, int SEC = 8>
 __device__ __forceinline__ const float4* bez_block(const float4* Q, const BezGrid& g, int su, int sv, int sw) {
+    static_assert(SEC == 8 || (SEC == 32 && P == 3), "grouped Bezier blocks are p = 3");
     MFA_DCHECK(su >= 0 && su < g.S0 && sv >= 0 && sv < g.S1 && sw >= 0);
-    const int64_t b = ((int64_t)sw * g.S1 + sv) * g.S0 + su;
-    MFA_DCHECK((b + 1) * (BezBlock<P>::FLOATS / 4) <= g.q_f4);
-    return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Q) + b * BezBlock<P>::FLOATS);
+    const int64_t o = bez_block_offset(P, SEC == 32, g.S0, g.S1, su, sv, sw);
+    MFA_DCHECK((o + (SEC == 32 ? 7 * SEC + 8 : BezBlock<P>::FLOATS)) / 4 <= g.q_f4);
+    return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Q) + o);
 }
 
-// block b = (sw * S1 + sv) * S0 + su (< 2^31: mfa_model_create)
+// block b = (sw * S1 + sv) * S0 + su (< 2^31: mfa_model_create), linear layout only
 template <int P>
 __device__ __forceinline__ const float4* bez_block_at(const float4* Q, const BezGrid& g, int b) {
     MFA_DCHECK(b >= 0 && (int64_t)(b + 1) * (BezBlock<P>::FLOATS / 4) <= g.q_f4);
@@ -983,15 +997,16 @@ __device__ __forceinline__ const float4* bez_block_at(const float4* Q, const Bez
 
 // slab c of a Bezier block: rows b = 0..P at consecutive compile-time offsets
 
-template <int P>
+template <int P, int SEC = 8>
 __device__ __forceinline__ void load_bslab(const float4* __restrict__ q, float (&r)[P + 1][P + 1]) {
+    static_assert(MFA_LDG256 || SEC == 8, "the grouped Bezier layout is read by sector loads");
 #if MFA_LDG256
     if constexpr (P == 3) {   // 64 bytes = two sector loads
         const float* f = reinterpret_cast<const float*>(q);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             float x[8];
-            ldg256(f + 8 * k, x);
+            ldg256(f + SEC * k, x);
 #pragma unroll
             for (int e = 0; e < 8; ++e) r[2 * k + (e >> 2)][e & 3] = x[e];
         }
@@ -1011,20 +1026,22 @@ __device__ __forceinline__ void load_bslab(const float4* __restrict__ q, float (
     }
 }
 
-template <int P>
+template <int P, int SEC = 8>
 __device__ __forceinline__ const float4* bslab_ptr(const float4* q, int c) {
+    if constexpr (SEC != 8) return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + c * 2 * SEC);
     return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(q) + c * (P + 1) * BezBlock<P>::ROW);
 }
 
-template <int P>
+template <int P, int SEC = 8>
 __device__ __forceinline__ void load_bblock(const float4* __restrict__ q, float (&nb)[P + 1][P + 1][P + 1]) {
+    static_assert(MFA_LDG256 || SEC == 8, "the grouped Bezier layout is read by sector loads");
 #if MFA_LDG256
     if constexpr (P == 3) {   // the 256-byte block as 8 sector loads (two rows each)
         const float* f = reinterpret_cast<const float*>(q);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             float r[8];
-            ldg256(f + 8 * k, r);
+            ldg256(f + SEC * k, r);
 #pragma unroll
             for (int e = 0; e < 8; ++e) nb[k >> 1][2 * (k & 1) + (e >> 2)][e & 3] = r[e];
         }
@@ -1032,10 +1049,10 @@ __device__ __forceinline__ void load_bblock(const float4* __restrict__ q, float 
     }
 #endif
 #pragma unroll
-    for (int c = 0; c <= P; ++c) load_bslab<P>(bslab_ptr<P>(q, c), nb[c]);
+    for (int c = 0; c <= P; ++c) load_bslab<P, SEC>(bslab_ptr<P, SEC>(q, c), nb[c]);
 }
 
-template <int P>
+template <int P, int SEC = 8>
 __device__ __forceinline__ void contract_vg_bez(const float4* __restrict__ q, float (&r0)[P + 1][P + 1],
                                                 const float2 (&Bu)[P + 1], const float2 (&Bvs)[P + 1],
                                                 const float2 (&Bw)[P + 1], float& val, float& gu, float& gv,
@@ -1045,10 +1062,10 @@ __device__ __forceinline__ void contract_vg_bez(const float4* __restrict__ q, fl
 #pragma unroll
     for (int c = 0; c <= P; ++c) {
         if (c & 1) {
-            if (c < P) load_bslab<P>(bslab_ptr<P>(q, c + 1), r0);
+            if (c < P) load_bslab<P, SEC>(bslab_ptr<P, SEC>(q, c + 1), r0);
             contract_slab<P>(r1, Bu, Bvs, Bw[c], vw, gvu);
         } else {
-            if (c < P) load_bslab<P>(bslab_ptr<P>(q, c + 1), r1);
+            if (c < P) load_bslab<P, SEC>(bslab_ptr<P, SEC>(q, c + 1), r1);
             contract_slab<P>(r0, Bu, Bvs, Bw[c], vw, gvu);
         }
     }

@@ -67,6 +67,21 @@ constexpr int kQueueSlots = 256;    // persistent-kernel work counters (one per 
 #endif
 constexpr int kMacroLog = MFA_MACRO_LOG;   // macro blocks of 2^3 span triples (transparent-block skip; 4^3: -3 %, 8^3: -9 %)
 __host__ __device__ constexpr int bez_row(int p) { return p == 1 ? 2 : 4; }  // floats per stored block row
+// Grouped Bezier layout (kBezierG, p = 3): blocks of 4 consecutive w-spans
+// are interleaved by 32-byte sector -- group ((sw >> 2) * S1 + sv) * S0 + su is
+// 8 lines of 128 B, line j holding sector j (block rows 2j, 2j+1) of its 4
+// blocks -- so lanes of a warp that reload vertically neighbouring blocks in
+// the same instruction share L1 lines (wavefronts).  kBezier: one contiguous
+// block per span triple.
+// float offset of block (su, sv, sw) (its sector 0) in the block array
+__host__ __device__ inline long long bez_block_offset(int p, bool grouped, int S0, int S1, int su, int sv, int sw) {
+    if (grouped) return ((((long long)(sw >> 2) * S1 + sv) * S0 + su) << 8) + ((sw & 3) << 3);
+    return (((long long)sw * S1 + sv) * S0 + su) * (long long)((p + 1) * (p + 1) * bez_row(p));
+}
+// floats between consecutive 32-byte sectors of one p = 3 block
+__host__ __device__ constexpr int bez_sec(bool grouped) { return grouped ? 32 : 8; }
+// blocks to allocate along w for S2 w-spans (grouped: whole groups)
+__host__ __device__ inline long long bez_alloc_s2(bool grouped, long long S2) { return grouped ? (S2 + 3) / 4 * 4 : S2; }
 
 // float4 per brick entry: p <= 3 stores row PAIRS (rows j and j+1 of a quad
 // column, 32 bytes: one 256-bit load fetches two rows), p >= 4 single quads
@@ -97,7 +112,8 @@ struct AxisTables {
     float S = 0.f;                    // uniform: number of spans as float
 };
 
-enum Layout { kQuads = 0, kBezier = 1, kBricks = 2 };
+enum Layout { kQuads = 0, kBezier = 1, kBricks = 2, kBezierG = 3 };   // kBezierG: grouped Bezier blocks (p = 3)
+__host__ __device__ constexpr bool is_bez(int layout) { return layout == kBezier || layout == kBezierG; }
 
 // plain haloed bricks (kBricks, p <= 3): one fp32 per control point, bricks
 // of 16^3 spans with the p halo points on the high side, rows padded to a

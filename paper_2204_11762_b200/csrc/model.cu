@@ -229,7 +229,7 @@ __global__ void init_minmax_kernel(unsigned* __restrict__ mmx, int64_t n) {
     }
 }
 
-template <int P>
+template <int P, bool G = false>
 __global__ void bezier_blocks_kernel(const float* __restrict__ Pg, int nu, int nv, const double* __restrict__ Du,
                                      const double* __restrict__ Dv, const double* __restrict__ Dw, int Su, int Sv,
                                      int64_t nblocks, float* __restrict__ out, unsigned* __restrict__ mmx, int mm0,
@@ -262,19 +262,22 @@ __global__ void bezier_blocks_kernel(const float* __restrict__ Pg, int nu, int n
                     for (int b = 0; b < Q; ++b) acc += dv[b * Q + k] * X[c][b][j];
                     Y[c][k][j] = acc;
                 }
-        float* o = out + idx * (Q * Q * R);
+        float* o = out + bez_block_offset(P, G, Su, Sv, su, sv, sw);
         float lo = INFINITY, hi = -INFINITY;
         for (int l = 0; l < Q; ++l)
             for (int k = 0; k < Q; ++k) {
+                // row (l, k) = the (l * Q + k)-th R-float row; 32-byte sector = 8 / R rows
+                const int row = l * Q + k;
+                float* orow = G ? o + (row >> 1) * bez_sec(G) + (row & 1) * R : o + row * R;
                 for (int j = 0; j < Q; ++j) {
                     double acc = 0.0;
                     for (int c = 0; c < Q; ++c) acc += dw[c * Q + l] * Y[c][k][j];
                     const float f = (float)acc;
-                    o[(l * Q + k) * R + j] = f;
+                    orow[j] = f;
                     lo = fminf(lo, f);
                     hi = fmaxf(hi, f);
                 }
-                for (int j = Q; j < R; ++j) o[(l * Q + k) * R + j] = 0.f;
+                for (int j = Q; j < R; ++j) orow[j] = 0.f;
             }
         // macro-block value bounds (the spline on a span triple lies in the
         // convex hull of its Bernstein coefficients)
@@ -385,7 +388,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
     const auto t_create = std::chrono::steady_clock::now();
     if (!out) return fail(MFA_ERR_INVALID_ARG, "out is NULL");
     const int want_layout = opt ? opt->layout : MFA_LAYOUT_AUTO;
-    if (want_layout < MFA_LAYOUT_AUTO || want_layout > MFA_LAYOUT_BRICKS)
+    if (want_layout < MFA_LAYOUT_AUTO || want_layout > MFA_LAYOUT_BEZIER_GROUPED)
         return fail(MFA_ERR_INVALID_ARG, "options.layout out of range");
     *out = nullptr;
     if (!degree || !nctrl || !knots || !ctrl) return fail(MFA_ERR_INVALID_ARG, "NULL argument");
@@ -537,24 +540,31 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
     // AUTO: Bezier blocks for non-uniform models, and for uniform ones whose
     // blocks fit in a fraction of L2 (small models: every reload is an L2 hit)
     const double bez_bytes = 4.0 * (p + 1) * (p + 1) * (p + 1) * (double)(nctrl[0] - p) * (nctrl[1] - p) * (nctrl[2] - p);
-    bool bez = want_layout == MFA_LAYOUT_BEZIER ||
-               (want_layout == MFA_LAYOUT_AUTO && p <= 3 && (nonuni || bez_bytes <= kBezSmallModelBytes));
+    const bool want_bez = want_layout == MFA_LAYOUT_BEZIER || want_layout == MFA_LAYOUT_BEZIER_GROUPED;
+    bool bez = want_bez || (want_layout == MFA_LAYOUT_AUTO && p <= 3 && (nonuni || bez_bytes <= kBezSmallModelBytes));
     if (bez && p > 3) return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs degree <= 3"));
+    if (want_layout == MFA_LAYOUT_BEZIER_GROUPED && p != 3)
+        return cleanup(fail(MFA_ERR_UNSUPPORTED, "grouped Bezier layout needs degree 3"));
+    // AUTO takes the grouped blocks at p = 3 (render +4 %)
+    const bool grouped = bez && p == 3 && want_layout != MFA_LAYOUT_BEZIER;
     if (want_layout == MFA_LAYOUT_BRICKS && p > 3)
         return cleanup(fail(MFA_ERR_UNSUPPORTED, "plain-brick layout needs degree <= 3"));
-    if (bez && (nctrl[0] - p) * (nctrl[1] - p) * (nctrl[2] - p) >= ((int64_t)1 << 31)) {   // 32-bit block index
-        if (want_layout == MFA_LAYOUT_BEZIER)
+    // 32-bit block index (render cache key; grouped layout: the offset in 32-byte units)
+    if (bez && (nctrl[0] - p) * (nctrl[1] - p) * bez_alloc_s2(grouped, nctrl[2] - p) * (grouped ? 8 : 1) >=
+                   ((int64_t)1 << 31)) {
+        if (want_bez)
             return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs < 2^31 span triples"));
         bez = false;
     }
     if (bez) {
         const int64_t S0 = nctrl[0] - p, S1 = nctrl[1] - p, S2 = nctrl[2] - p;
         const int64_t nblk = S0 * S1 * S2;
+        const int64_t nblk_alloc = S0 * S1 * bez_alloc_s2(grouped, S2);   // grouped layout: whole groups
         const int64_t bfl = (int64_t)(p + 1) * (p + 1) * bez_row(p);      // floats per block
-        e = cudaMalloc(&m->Q, nblk * bfl * sizeof(float));
+        e = cudaMalloc(&m->Q, nblk_alloc * bfl * sizeof(float));
         if (e != cudaSuccess) {
             m->Q = nullptr;
-            if (want_layout == MFA_LAYOUT_BEZIER) return cleanup(cuda_fail(e, "cudaMalloc Bezier blocks"));
+            if (want_bez) return cleanup(cuda_fail(e, "cudaMalloc Bezier blocks"));
             cudaGetLastError();   // AUTO: fall back to the quad layout
             bez = false;
         } else {
@@ -579,13 +589,13 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
             switch (p) {
                 case 1: bezier_blocks_kernel<1><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out, m->mmx, m->mm[0], m->mm[1]); break;
                 case 2: bezier_blocks_kernel<2><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out, m->mmx, m->mm[0], m->mm[1]); break;
-                default: bezier_blocks_kernel<3><<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out, m->mmx, m->mm[0], m->mm[1]); break;
+                default: (grouped ? bezier_blocks_kernel<3, true> : bezier_blocks_kernel<3, false>)<<<4736, 128, 0, st>>>(Pdev, (int)nu, (int)nv, Dax[0], Dax[1], Dax[2], (int)S0, (int)S1, nblk, out, m->mmx, m->mm[0], m->mm[1]); break;
             }
             cudaStreamSynchronize(st);
             cudaFree(D);
-            m->device_bytes += nblk * bfl * (int64_t)sizeof(float);
-            m->q_f4 = nblk * bfl / 4;
-            m->layout = kBezier;
+            m->device_bytes += nblk_alloc * bfl * (int64_t)sizeof(float);
+            m->q_f4 = nblk_alloc * bfl / 4;
+            m->layout = grouped ? kBezierG : kBezier;
         }
     }
     if (!bez && want_layout == MFA_LAYOUT_BRICKS) {   // plain haloed bricks (<= 1.86 x the grid)
@@ -645,7 +655,10 @@ extern "C" mfa_status mfa_model_info(mfa_model h, mfa_model_desc* out) {
     out->v_max = m->vmax;
     out->device_bytes = m->device_bytes;
     out->device = m->device;
-    out->layout = m->layout == kBezier ? MFA_LAYOUT_BEZIER : (m->layout == kBricks ? MFA_LAYOUT_BRICKS : MFA_LAYOUT_QUADS);
+    out->layout = m->layout == kBezier    ? MFA_LAYOUT_BEZIER
+                  : m->layout == kBezierG ? MFA_LAYOUT_BEZIER_GROUPED
+                  : m->layout == kBricks  ? MFA_LAYOUT_BRICKS
+                                          : MFA_LAYOUT_QUADS;
     out->model_bytes = m->model_bytes;
     out->create_ms = m->create_ms;
     return MFA_OK;

@@ -198,7 +198,7 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->mm1 = m->mm[1];
     a->mm_n = m->mm[0] * m->mm[1] * m->mm[2];
     void* tscratch = nullptr;
-    if (shade == 3 && m->layout == kBezier && m->mmx && !(field || lights || curv)) {
+    if (shade == 3 && is_bez(m->layout) && m->mmx && !(field || lights || curv)) {
         const int64_t nmac = (int64_t)m->mm[0] * m->mm[1] * m->mm[2];
         tscratch = scratch_alloc(sizeof(unsigned) * ((nmac + 31) / 32), st);
         if (tscratch) {

@@ -48,6 +48,9 @@
 #ifndef MFA_PREFETCH_NEXT   // experiment: 1 / 2 = prefetch the predicted next block into L1 / L2
 #define MFA_PREFETCH_NEXT 0
 #endif
+#ifndef MFA_EARLY_LOAD   // experiment: issue the next sample's block load right after this sample's contraction
+#define MFA_EARLY_LOAD 0
+#endif
 #ifndef MFA_FLAT_LOOP
 #define MFA_FLAT_LOOP 1
 #endif
@@ -236,7 +239,7 @@ __device__ __forceinline__ float pow_spec(float x, float n) {
 
 template <int P, int LAYOUT>
 struct RenderShape {
-    static constexpr bool BEZ = LAYOUT == kBezier;
+    static constexpr bool BEZ = is_bez(LAYOUT);
     static constexpr bool CACHE = BEZ ? (bool)MFA_BEZ_CACHE : (MFA_RENDER_CACHE && P <= 3);
 #ifdef MFA_RENDER_THREADS
     static constexpr int THREADS = MFA_RENDER_THREADS;
@@ -267,7 +270,8 @@ struct RenderShape {
 #endif
 template <int P, int LAYOUT, bool UNI, int SHADE, bool EXT>
 __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderArgs args) {
-    constexpr bool BEZ = LAYOUT == kBezier;
+    constexpr bool BEZ = is_bez(LAYOUT);
+    constexpr int SEC = bez_sec(LAYOUT == kBezierG);
     constexpr bool CACHE = RenderShape<P, LAYOUT>::CACHE;
     extern __shared__ float4 s_tf[];
 #if MFA_SMEM_FRAMES
@@ -282,7 +286,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
     // experiment: the block of the sample after next is prefetched by a bulk
     // async copy (cp.async.bulk, completion on a per-thread mbarrier) into a
     // per-thread shared-memory slot a whole iteration before it is needed
-    constexpr bool kPF = BEZ && CACHE && !EXT && !UNI && P == 3;
+    constexpr bool kPF = LAYOUT == kBezier && CACHE && !EXT && !UNI && P == 3;
     constexpr int kPFT = kPF ? RenderShape<P, LAYOUT>::THREADS : 1;
     __shared__ __align__(16) float s_pf[kPFT][kPF ? 68 : 4];   // 256 B + 16 B pad: conflict-free float4 reads
     __shared__ __align__(8) unsigned long long s_mbar[kPFT];
@@ -505,10 +509,25 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 
         // a6: make the neighbourhood of span triple s resident (CACHE layouts)
         auto fetch = [&](const int (&s)[3]) {
-            if constexpr (BEZ && CACHE) {
+            if constexpr (BEZ && CACHE && LAYOUT == kBezierG) {
+                // key = the block's offset in 32-byte units (< 2^31: mfa_model_create)
+                const int e = ((((s[2] >> 2) * args.bg.S1 + s[1]) * args.bg.S0 + s[0]) << 5) | (s[2] & 3);
+                if (e != nb_key) {
+                    load_bblock<P, SEC>(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(args.Q) + (int64_t)e * 8), nb);
+                    nb_key = e;
+                }
+            } else if constexpr (BEZ && CACHE) {
                 const int e = (s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
+#if MFA_DIAG_NORELOAD   // diagnostic only (wrong images): a lane keeps its first block, no reloads
+                if (nb_key < 0) {
+#else
                 if (e != nb_key) {       // reload only when the span triple changed
+#endif
+#if MFA_DIAG_L1   // diagnostic only (wrong images): every reload reads one of 64 L1-resident blocks
+                    load_bblock<P>(bez_block_at<P>(args.Q, args.bg, e & 63), nb);
+#else
                     load_bblock<P>(bez_block_at<P>(args.Q, args.bg, e), nb);
+#endif
                     nb_key = e;
                 }
             } else if constexpr (CACHE && LAYOUT == kBricks) {
@@ -590,18 +609,18 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         auto query = [&](const int (&s)[3], const float (&t)[3], float& val, float& gu, float& gv, float& gw) {
             gu = gv = gw = 0.f;
             if constexpr (BEZ && !CACHE) {   // stream the block slab by slab
-                const float4* q = bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]);
+                const float4* q = bez_block<P, SEC>(args.Q, args.bg, s[0], s[1], s[2]);
                 float r0[P + 1][P + 1];
-                load_bslab<P>(q, r0);
+                load_bslab<P, SEC>(q, r0);
                 if (SHADE) {
                     float2 Bu[P + 1], Bv[P + 1], Bw[P + 1];
                     bernstein<P, false>(t[0], Bu);
                     bernstein<P, true>(t[1], Bv);
                     bernstein<P, false>(t[2], Bw);
-                    contract_vg_bez<P>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
+                    contract_vg_bez<P, SEC>(q, r0, Bu, Bv, Bw, val, gu, gv, gw);
                 } else {
                     float nbv[P + 1][P + 1][P + 1];
-                    load_bblock<P>(q, nbv);
+                    load_bblock<P, SEC>(q, nbv);
                     float Nu[P + 1], Nv[P + 1], Nw[P + 1];
                     bernstein_value<P>(t[0], Nu);
                     bernstein_value<P>(t[1], Nv);
@@ -774,7 +793,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 for (int c = 0; c <= P; ++c) {
                     float r[P + 1][P + 1];
                     if constexpr (BEZ)
-                        load_bslab<P>(bslab_ptr<P>(bez_block<P>(args.Q, args.bg, s[0], s[1], s[2]), c), r);
+                        load_bslab<P, SEC>(bslab_ptr<P, SEC>(bez_block<P, SEC>(args.Q, args.bg, s[0], s[1], s[2]), c), r);
                     else
                         load_slab<P>(args.Q + brick_entry<P>(args.g, s[0], s[1], s[2]) + c * Brick<P>::SLAB, r);
                     contract_vgh_slab<P>(r, Nu, Du, Eu, Nv, Dv, Ev, Nw[c], Dw[c], Ew[c], o);
@@ -839,9 +858,32 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         // position is frozen (no reloads) and its compositing weight is 0.
         // Iteration k composites sample k and queries sample min(k+1, K-1).
         auto flat_loop = [&](auto multi_tag) {
+#if MFA_EARLY_LOAD
+            constexpr bool kEarly = BEZ && SHADE != 3;
+            constexpr bool kEarlyNU = kEarly && !UNI;
+            static_assert(!kEarlyNU || (MFA_NU_SHIFTCMP && MFA_NU_UCMP), "the early load predicts the UCMP rule");
+            int dn[3] = {0, 0, 0};   // kEarlyNU: span offsets of the next sample, computed one iteration ahead
+            if constexpr (kEarlyNU) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) dn[i] = nu_offset(args.ax[i], F[i], nu[i]);
+            }
+#endif
             while (__any_sync(0xffffffffu, live)) {
                 int s[3];
                 float t[3], gs1[3];
+#if MFA_EARLY_LOAD
+                if constexpr (kEarlyNU) {
+                    constexpr bool MULTI = decltype(multi_tag)::value;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) nu_cross_d(args.ax[i], dn[i], nu[i]);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        t[i] = nu_finish<MULTI>(args.ax[i], F[i], nu[i]);
+                        s[i] = nu[i].s;
+                        gs1[i] = nu_gscale(args.ax[i], nu[i]);
+                    }
+                } else
+#endif
                 locate(s, t, gs1, multi_tag);
                 const bool tr_next = transparent(s);
 #if MFA_BULK_PF
@@ -891,7 +933,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 #endif
                 if (!tr_next) fetch(s);
 #if MFA_PREFETCH_NEXT
-                if constexpr (BEZ && !UNI) {
+                if constexpr (LAYOUT == kBezier && !UNI) {   // linear blocks only
                     // predict the span triple of the sample after this one from the
                     // current span bounds (one crossing per axis at most) and pull
                     // its block towards the SM a whole iteration before its load
@@ -938,6 +980,29 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 }
                 k += live ? 1 : 0;
                 live = live && !(A > args.o_max) && k < K;
+#if MFA_EARLY_LOAD
+                // the block of the NEXT iteration's sample, issued as soon as this
+                // iteration's contraction has read the cached one: its span triple
+                // follows from the span state and the advanced position by the
+                // same single-crossing rule nu_cross applies (exact unless a step
+                // crosses several spans, which the next fetch() then corrects), so
+                // the load latency overlaps the next locate and shading too.
+                if constexpr (kEarly) {
+                    int s2[3];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        if constexpr (UNI) {
+                            float t2;
+                            uni_span_fx(F[i], args.ax[i].nsp, s2[i], t2);
+                        } else {
+                            dn[i] = nu_offset(args.ax[i], F[i], nu[i]);   // reused by the next nu_cross_d
+                            s2[i] = (unsigned)dn[i] >= (unsigned)nu[i].wsh ? max(nu[i].s + ((dn[i] >> 31) | 1), 0)
+                                                                           : nu[i].s;
+                        }
+                    }
+                    if (live) fetch(s2);
+                }
+#endif
             }
         };
         if constexpr (kFlat) {
@@ -1083,7 +1148,7 @@ static cudaError_t launch_render_t(const RenderArgs& a, cudaStream_t st) {
 template <int P, int LAYOUT, bool EXT>
 static cudaError_t dispatch_render_l(const RenderArgs& a, bool uni, int shade, cudaStream_t st) {
     constexpr bool kSkip = !EXT && RenderShape<P, LAYOUT>::CACHE;   // SHADE = 2 is built for the hot path only
-    constexpr bool kSkipBlk = kSkip && LAYOUT == kBezier;             // SHADE = 3 needs the macro-block bounds
+    constexpr bool kSkipBlk = kSkip && is_bez(LAYOUT);               // SHADE = 3 needs the macro-block bounds
     if (shade == 2 && !kSkip) shade = 1;
     if (shade == 3 && !(kSkipBlk && a.tbits)) shade = 1;
     if (uni) {
@@ -1106,6 +1171,8 @@ template <int P, bool EXT>
 static cudaError_t dispatch_render(const RenderArgs& a, int layout, bool uni, int shade, cudaStream_t st) {
     if constexpr (P <= 3) {
         if (layout == kBezier) return dispatch_render_l<P, kBezier, EXT>(a, uni, shade, st);
+        if constexpr (P == 3)
+            if (layout == kBezierG) return dispatch_render_l<P, kBezierG, EXT>(a, uni, shade, st);
         if (layout == kBricks) return dispatch_render_l<P, kBricks, EXT>(a, uni, shade, st);
     }
     return dispatch_render_l<P, kQuads, EXT>(a, uni, shade, st);

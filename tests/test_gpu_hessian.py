@@ -72,7 +72,8 @@ def models(c, layout):
 
 
 @pytest.mark.parametrize("c,layout", [(1, "quads"), (2, "quads"), (2, "bezier"), (3, "quads"), (4, "quads"),
-                                      (5, "bezier"), (5, "quads"), (2, "bricks"), (5, "bricks")])
+                                      (5, "bezier"), (5, "quads"), (2, "bricks"), (5, "bricks"),
+                                      (5, "bezier_grouped"), (2, "bezier_grouped")])
 def test_hessian_parity_configs(c, layout):
     w, m, om = models(c, layout)
     u, v, ww = WL.query_points(c, 1 << 15)
@@ -118,7 +119,7 @@ def test_hessian_domain_errors_and_empty():
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("c,layout", [(3, "quads"), (5, "bezier")])
+@pytest.mark.parametrize("c,layout", [(3, "quads"), (5, "bezier"), (5, "bezier_grouped")])
 def test_hessian_binned_equals_direct(c, layout):
     w, m, _ = models(c, layout)
     u, v, ww = WL.query_points(c, 1 << 17)

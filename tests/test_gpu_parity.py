@@ -262,10 +262,11 @@ def test_invalid_models_raise():
 
 
 @pytest.mark.parametrize("c,layout", [(1, "bezier"), (2, "bezier"), (3, "bezier"), (5, "quads"),
-                                      (1, "bricks"), (2, "bricks"), (3, "bricks"), (5, "bricks")])
+                                      (1, "bricks"), (2, "bricks"), (3, "bricks"), (5, "bricks"),
+                                      (3, "bezier_grouped"), (5, "bezier")])
 def test_both_layouts_eval_and_render(c, layout):
     """Each model also through the other control-point layouts (bricked quads,
-    Bezier blocks, plain haloed bricks): eval parity on random + boundary
+    Bezier blocks linear or grouped, plain haloed bricks): eval parity on random + boundary
     points and a render parity check (a reduced image for C3/C5)."""
     w = workload(c) if c in (1, 2) else workload(c, width=256, height=192, n_views=1)
     m = gpu_model(c, layout)
@@ -287,8 +288,9 @@ def test_both_layouts_eval_and_render(c, layout):
 
 def test_default_layouts():
     assert gpu_model(3).info()["layout"] == "quads"
-    assert gpu_model(5).info()["layout"] == "bezier"
-    assert gpu_model(2).info()["layout"] == "bezier"   # uniform, but 58 MB of blocks: L2-resident
+    assert gpu_model(5).info()["layout"] == "bezier_grouped"   # p = 3 Bezier blocks: grouped
+    assert gpu_model(2).info()["layout"] == "bezier_grouped"   # uniform, but 58 MB of blocks: L2-resident
+    assert gpu_model(1).info()["layout"] == "bezier"           # p = 2: linear blocks
 
 
 @pytest.mark.parametrize("p", [2, 3])
@@ -308,7 +310,7 @@ def test_nonuniform_multiple_knots(p):
     w.v_lo, w.v_hi = float(ctrl.min()), float(ctrl.max())
     om = O.Model.from_workload(w)
     from paper_2204_11762_b200 import Model
-    for layout in ("quads", "bezier", "bricks"):
+    for layout in ("quads", "bezier", "bricks") + (("bezier_grouped",) if p == 3 else ()):
         m = Model.from_workload(w, layout=layout)
         u, v, ww = WL.query_points(1, 1 << 14)
         got = gpu_eval(m, u, v, ww)
@@ -593,7 +595,7 @@ def test_transparent_skip_in_tiled_scatter_path():
     assert torch.equal(img, full)
 
 
-@pytest.mark.parametrize("layout", ["auto", "quads", "bricks", "bezier"])
+@pytest.mark.parametrize("layout", ["auto", "quads", "bricks", "bezier", "bezier_grouped"])
 def test_model_info_footprint(layout):
     """mfa_model_info reports the grid bytes, the device bytes of the chosen
     layout (bricks <= 2x the grid) and the create time."""

@@ -1,0 +1,11 @@
+#!/bin/bash
+# round 2: A/B (alternating) of the early block load (MFA_EARLY_LOAD); image hashes must match
+for f in "" "-DMFA_EARLY_LOAD=1" "" "-DMFA_EARLY_LOAD=1"; do
+  echo "=== flags: $f"
+  MFA_EXTRA_NVCC_FLAGS="$f" python -m paper_2204_11762_b200.build > gpurun_out/bv.log 2>&1 || { tail -5 gpurun_out/bv.log; continue; }
+  python tools/img_hash.py 2 5
+  ./tools/quickbench.sh c5 c2
+done
+MFA_EXTRA_NVCC_FLAGS="-DMFA_EARLY_LOAD=1" python -m paper_2204_11762_b200.build > gpurun_out/bv.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "subset or nonuniform or narrower or degrees or skip or both_layouts or mfa_render" 2>&1 | tail -2
+python -m paper_2204_11762_b200.build > /dev/null 2>&1
