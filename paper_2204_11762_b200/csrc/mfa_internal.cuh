@@ -73,15 +73,36 @@ __host__ __device__ constexpr int bez_row(int p) { return p == 1 ? 2 : 4; }  // 
 // blocks -- so lanes of a warp that reload vertically neighbouring blocks in
 // the same instruction share L1 lines (wavefronts).  kBezier: one contiguous
 // block per span triple.
+// group shape (experiment MFA_BEZ_GSHAPE): log2 extents (u, v, w) of the 4-block group
+// 0 = (0,0,2) 4 w-spans, 1 = (0,1,1), 2 = (1,0,1), 3 = (2,0,0) 4 u-spans, 4 = (1,1,0)
+#ifndef MFA_BEZ_GSHAPE
+#define MFA_BEZ_GSHAPE 2
+#endif
+constexpr int kGLu = MFA_BEZ_GSHAPE == 2 || MFA_BEZ_GSHAPE == 4 ? 1 : (MFA_BEZ_GSHAPE == 3 ? 2 : 0);
+constexpr int kGLv = MFA_BEZ_GSHAPE == 1 || MFA_BEZ_GSHAPE == 4 ? 1 : 0;
+constexpr int kGLw = 2 - kGLu - kGLv;
+// grouped block (su, sv, sw): its offset in 32-byte units = (group << 5) | slot
+// (T = int in the render kernel: mfa_model_create keeps it below 2^31)
+template <typename T = long long>
+__host__ __device__ inline T bez_group_key(int S0, int S1, int su, int sv, int sw) {
+    const int S0g = (S0 + (1 << kGLu) - 1) >> kGLu, S1g = (S1 + (1 << kGLv) - 1) >> kGLv;
+    const T g = ((T)(sw >> kGLw) * S1g + (sv >> kGLv)) * S0g + (su >> kGLu);
+    const int slot = (((sw & ((1 << kGLw) - 1)) << kGLv | (sv & ((1 << kGLv) - 1))) << kGLu) | (su & ((1 << kGLu) - 1));
+    return (g << 5) | slot;
+}
 // float offset of block (su, sv, sw) (its sector 0) in the block array
 __host__ __device__ inline long long bez_block_offset(int p, bool grouped, int S0, int S1, int su, int sv, int sw) {
-    if (grouped) return ((((long long)(sw >> 2) * S1 + sv) * S0 + su) << 8) + ((sw & 3) << 3);
+    if (grouped) return bez_group_key(S0, S1, su, sv, sw) << 3;
     return (((long long)sw * S1 + sv) * S0 + su) * (long long)((p + 1) * (p + 1) * bez_row(p));
 }
 // floats between consecutive 32-byte sectors of one p = 3 block
 __host__ __device__ constexpr int bez_sec(bool grouped) { return grouped ? 32 : 8; }
-// blocks to allocate along w for S2 w-spans (grouped: whole groups)
-__host__ __device__ inline long long bez_alloc_s2(bool grouped, long long S2) { return grouped ? (S2 + 3) / 4 * 4 : S2; }
+// blocks to allocate (grouped: whole groups)
+__host__ __device__ inline long long bez_alloc_blocks(bool grouped, long long S0, long long S1, long long S2) {
+    if (!grouped) return S0 * S1 * S2;
+    auto up = [](long long n, int l) { return ((n + (1 << l) - 1) >> l) << l; };
+    return up(S0, kGLu) * up(S1, kGLv) * up(S2, kGLw);
+}
 
 // float4 per brick entry: p <= 3 stores row PAIRS (rows j and j+1 of a quad
 // column, 32 bytes: one 256-bit load fetches two rows), p >= 4 single quads

@@ -550,7 +550,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
     if (want_layout == MFA_LAYOUT_BRICKS && p > 3)
         return cleanup(fail(MFA_ERR_UNSUPPORTED, "plain-brick layout needs degree <= 3"));
     // 32-bit block index (render cache key; grouped layout: the offset in 32-byte units)
-    if (bez && (nctrl[0] - p) * (nctrl[1] - p) * bez_alloc_s2(grouped, nctrl[2] - p) * (grouped ? 8 : 1) >=
+    if (bez && bez_alloc_blocks(grouped, nctrl[0] - p, nctrl[1] - p, nctrl[2] - p) * (grouped ? 8 : 1) >=
                    ((int64_t)1 << 31)) {
         if (want_bez)
             return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs < 2^31 span triples"));
@@ -559,7 +559,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
     if (bez) {
         const int64_t S0 = nctrl[0] - p, S1 = nctrl[1] - p, S2 = nctrl[2] - p;
         const int64_t nblk = S0 * S1 * S2;
-        const int64_t nblk_alloc = S0 * S1 * bez_alloc_s2(grouped, S2);   // grouped layout: whole groups
+        const int64_t nblk_alloc = bez_alloc_blocks(grouped, S0, S1, S2);   // grouped layout: whole groups
         const int64_t bfl = (int64_t)(p + 1) * (p + 1) * bez_row(p);      // floats per block
         e = cudaMalloc(&m->Q, nblk_alloc * bfl * sizeof(float));
         if (e != cudaSuccess) {
