@@ -271,6 +271,8 @@ extern "C" mfa_status mfa_eval_hessian_ws(mfa_model h, int64_t n, const float* u
     a.bg.q_f4 = m->q_f4;
     a.bg.S0 = (int)(m->n[0] - m->p);
     a.bg.S1 = (int)(m->n[1] - m->p);
+    a.bg.S0g = bez_groups(a.bg.S0, kGLu);
+    a.bg.S1g = bez_groups(a.bg.S1, kGLv);
     for (int d = 0; d < 3; ++d) a.ax[d] = make_axis_args(m->ax[d]);
     a.u = u;
     a.v = v;

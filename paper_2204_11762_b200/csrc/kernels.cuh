@@ -372,13 +372,29 @@ struct NUAxis {
 #ifndef MFA_SPAN_REC
 #define MFA_SPAN_REC 1
 #endif
+
 #ifndef MFA_NU_SPLIT
 #define MFA_NU_SPLIT 1
 #endif
 
 __device__ __forceinline__ void nu_load(const AxisArgs& A, NUAxis& st) {
     MFA_DCHECK(st.s >= 0 && st.s < A.nsp);
-#if MFA_SPAN_REC
+#if MFA_SPAN_REC && MFA_SPAN_REC16
+    // one 16-byte record {lo, wsh | bits(1/h) << 32} (model.cu span_rec_kernel);
+    // tsc = (1/h) * 2^(dshift-62) is an exact power-of-two scaling of 1/h
+    long long r0, r1;
+    asm("ld.global.nc.v2.s64 {%0,%1}, [%2];" : "=l"(r0), "=l"(r1)
+        : "l"(reinterpret_cast<const longlong2*>(A.srec) + st.s));
+    st.lo = r0;
+    st.wsh = (int)(unsigned)r1;
+    const float ih = __int_as_float((int)(r1 >> 32));
+#if MFA_GSV
+    st.gsv = ih * A.gsc;
+#else
+    st.invh = ih;
+#endif
+    st.tsc = ih * A.dscale;
+#elif MFA_SPAN_REC
     // one 32-byte record: {lo, hi, bits(1/h), bits(tsc)} (model.cu span_rec_kernel)
     long long r0, r1, r2, r3;
     asm("ld.global.nc.v4.s64 {%0,%1,%2,%3}, [%4];"
@@ -967,6 +983,7 @@ __device__ __forceinline__ void bernstein_value(float t, float (&N)[P + 1]) {
 
 struct BezGrid {
     int S0, S1;            // spans along u, v
+    int S0g, S1g;          // grouped layout: groups along u, v (bez_groups)
     int64_t q_f4;          // size of the block array in float4 (debug bounds checks)
 };
 
@@ -983,7 +1000,8 @@ template <int P, int SEC = 8>
 __device__ __forceinline__ const float4* bez_block(const float4* Q, const BezGrid& g, int su, int sv, int sw) {
     static_assert(SEC == 8 || (SEC == 32 && P == 3), "grouped Bezier blocks are p = 3");
     MFA_DCHECK(su >= 0 && su < g.S0 && sv >= 0 && sv < g.S1 && sw >= 0);
-    const int64_t o = bez_block_offset(P, SEC == 32, g.S0, g.S1, su, sv, sw);
+    const int64_t o = SEC == 32 ? bez_group_key(g.S0g, g.S1g, su, sv, sw) << 3
+                                : bez_block_offset(P, false, g.S0, g.S1, su, sv, sw);
     MFA_DCHECK((o + (SEC == 32 ? 7 * SEC + 8 : BezBlock<P>::FLOATS)) / 4 <= g.q_f4);
     return reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Q) + o);
 }

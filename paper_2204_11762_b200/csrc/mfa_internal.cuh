@@ -48,6 +48,10 @@
 #ifndef MFA_NU_SHIFTCMP   // 1: span crossings tested on the shifted 32-bit offset d = (F - lo) >> dshift
 #define MFA_NU_SHIFTCMP 1    //    against the span width in the same units (wsh, from the record): C5 +2.1 %
 #endif
+#ifndef MFA_SPAN_REC16   // 16-byte render span records (one 128-bit load per crossing instead of 256-bit)
+#define MFA_SPAN_REC16 1
+#endif
+static_assert(!MFA_SPAN_REC16 || MFA_NU_SHIFTCMP, "16-byte span records carry wsh (MFA_NU_SHIFTCMP)");
 
 #ifndef MFA_SUPERTILE   // full-frame work order: supertiles of MFA_SUPERTILE x MFA_SUPERTILE 16x16 tiles
 #define MFA_SUPERTILE 2
@@ -83,16 +87,17 @@ constexpr int kGLv = MFA_BEZ_GSHAPE == 1 || MFA_BEZ_GSHAPE == 4 ? 1 : 0;
 constexpr int kGLw = 2 - kGLu - kGLv;
 // grouped block (su, sv, sw): its offset in 32-byte units = (group << 5) | slot
 // (T = int in the render kernel: mfa_model_create keeps it below 2^31)
+__host__ __device__ constexpr int bez_groups(int S, int l) { return (S + (1 << l) - 1) >> l; }
+// S0g = bez_groups(S0, kGLu), S1g = bez_groups(S1, kGLv) (BezGrid carries both)
 template <typename T = long long>
-__host__ __device__ inline T bez_group_key(int S0, int S1, int su, int sv, int sw) {
-    const int S0g = (S0 + (1 << kGLu) - 1) >> kGLu, S1g = (S1 + (1 << kGLv) - 1) >> kGLv;
+__host__ __device__ inline T bez_group_key(int S0g, int S1g, int su, int sv, int sw) {
     const T g = ((T)(sw >> kGLw) * S1g + (sv >> kGLv)) * S0g + (su >> kGLu);
     const int slot = (((sw & ((1 << kGLw) - 1)) << kGLv | (sv & ((1 << kGLv) - 1))) << kGLu) | (su & ((1 << kGLu) - 1));
     return (g << 5) | slot;
 }
 // float offset of block (su, sv, sw) (its sector 0) in the block array
 __host__ __device__ inline long long bez_block_offset(int p, bool grouped, int S0, int S1, int su, int sv, int sw) {
-    if (grouped) return bez_group_key(S0, S1, su, sv, sw) << 3;
+    if (grouped) return bez_group_key(bez_groups(S0, kGLu), bez_groups(S1, kGLv), su, sv, sw) << 3;
     return (((long long)sw * S1 + sv) * S0 + su) * (long long)((p + 1) * (p + 1) * bez_row(p));
 }
 // floats between consecutive 32-byte sectors of one p = 3 block

@@ -187,9 +187,15 @@ __global__ void span_rec_kernel(const long long* __restrict__ kfx, const float* 
 #else
     const long long second = s + 1 < nsp ? kfx[s + 1] : 0x7fffffffffffffffLL;
 #endif
+#if MFA_SPAN_REC16   // {lo, wsh | bits(1/h) << 32}: the kernels derive tsc = (1/h) * dscale
+    reinterpret_cast<longlong2*>(rec)[s] =
+        make_longlong2(kfx[s], (long long)(((unsigned long long)(unsigned)__float_as_int(ih) << 32) |
+                                           (unsigned long long)(unsigned)second));
+#else
     rec[s] = make_longlong4(kfx[s], second,
                             (long long)(unsigned)__float_as_int(ih),
                             (long long)(unsigned)__float_as_int(ih * dscale));
+#endif
 }
 
 // Bezier extraction operator of span s: N_{s+a}(t) = sum_j D[a][j] B_j(t) with

@@ -152,6 +152,8 @@ mfa_status launch_render(const Model* m, int32_t n_views, const mfa_camera* cams
     a->bg.q_f4 = m->q_f4;
     a->bg.S0 = (int)(m->n[0] - m->p);
     a->bg.S1 = (int)(m->n[1] - m->p);
+    a->bg.S0g = bez_groups(a->bg.S0, kGLu);
+    a->bg.S1g = bez_groups(a->bg.S1, kGLv);
     for (int d = 0; d < 3; ++d) a->ax[d] = make_axis_args(m->ax[d]);
     a->tf = reinterpret_cast<const float4*>(tf->rgba);
     a->tf_n = tf->n_entries;

@@ -511,7 +511,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         auto fetch = [&](const int (&s)[3]) {
             if constexpr (BEZ && CACHE && LAYOUT == kBezierG) {
                 // key = the block's offset in 32-byte units (< 2^31: mfa_model_create)
-                const int e = bez_group_key<int>(args.bg.S0, args.bg.S1, s[0], s[1], s[2]);
+                const int e = bez_group_key<int>(args.bg.S0g, args.bg.S1g, s[0], s[1], s[2]);
                 if (e != nb_key) {
                     load_bblock<P, SEC>(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(args.Q) + (int64_t)e * 8), nb);
                     nb_key = e;
