@@ -36,6 +36,8 @@ struct AxisArgs {
     float S;
     int dshift;      // non-uniform render: (F - U_s) >> dshift fits 23 bits on every span
     float dscale;    // 2^(dshift - 62)
+    unsigned dmagic; // bits of 2^(23 + dshift - 62): (d & 0x7fffff) | dmagic - dbias = d * 2^(dshift - 62) exactly
+    float dbias;     // 2^(23 + dshift - 62)
     int multi;       // non-uniform render: 1 if one ray step can cross more than one span (set per launch)
     float gsc;       // non-uniform render: parameter -> physical gradient scale 1/L (set per launch)
 };
@@ -61,6 +63,8 @@ __host__ inline AxisArgs make_axis_args(const AxisTables& A) {
     a.S = A.S;
     a.dshift = A.dshift;
     a.dscale = ldexpf(1.0f, A.dshift - kNonUniFracBits);
+    a.dmagic = (unsigned)(0x4b000000 + ((A.dshift - kNonUniFracBits) << 23));
+    a.dbias = ldexpf(1.0f, 23 + A.dshift - kNonUniFracBits);
     return a;
 }
 
@@ -353,6 +357,10 @@ __device__ __forceinline__ void nonuni_span_f32(const AxisArgs& A, float u, int&
 #define MFA_GSV 0
 #endif
 
+#ifndef MFA_NU_TMAGIC   // 1: the t scale folded into the magic-number exponent (no per-span tsc)
+#define MFA_NU_TMAGIC (MFA_SPAN_REC16 && !MFA_GSV)
+#endif
+static_assert(!MFA_NU_TMAGIC || (MFA_NU_SHIFTCMP && MFA_SPAN_REC16 && !MFA_GSV), "MFA_NU_TMAGIC: shifted offsets, 16-byte records");
 struct NUAxis {
     long long lo;       // left knot of span s (2^62 fixed point)
 #if MFA_NU_SHIFTCMP
@@ -360,7 +368,9 @@ struct NUAxis {
 #else
     long long hi;       // right knot of span s
 #endif
+#if !MFA_NU_TMAGIC
     float tsc;          // 2^(dshift-62) / h_s
+#endif
 #if MFA_GSV
     float gsv;          // (1 / h_s) * gsc: the span's t -> physical gradient scale (set at each crossing)
 #else
@@ -393,7 +403,9 @@ __device__ __forceinline__ void nu_load(const AxisArgs& A, NUAxis& st) {
 #else
     st.invh = ih;
 #endif
+#if !MFA_NU_TMAGIC
     st.tsc = ih * A.dscale;
+#endif
 #elif MFA_SPAN_REC
     // one 32-byte record: {lo, hi, bits(1/h), bits(tsc)} (model.cu span_rec_kernel)
     long long r0, r1, r2, r3;
@@ -559,13 +571,23 @@ __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxi
     // d < wsh <= 2^23 - 1 inside the span; negative only for exit-face rounding
     // on span 0; the mask keeps the exponent intact whatever happens
     unsigned bits;   // (max(d, 0) & 0x7fffff) | 0x4b000000 in one LOP3
+#if MFA_NU_TMAGIC
+    // the exponent of the magic number carries 2^(dshift - 62): fd = d * 2^(dshift - 62)
+    // exactly, so t = fd * (1/h) rounds the same exact product as d * tsc did
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(bits) : "r"(max(d, 0)), "r"(0x7fffff), "r"(A.dmagic));
+    const float fd = __uint_as_float(bits) - A.dbias;
+    return fd * st.invh;
+#else
     asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(bits) : "r"(max(d, 0)), "r"(0x7fffff), "r"(0x4b000000));
     const float fd = __uint_as_float(bits) - 8388608.0f;
+#endif
 #else
     d = min(max(d, 0), 8388607);
     const float fd = __int_as_float(0x4b000000 | d) - 8388608.0f;
 #endif
+#if !MFA_NU_TMAGIC
     return fd * st.tsc;
+#endif
 }
 
 // ---------------------------------------------------------------------------
