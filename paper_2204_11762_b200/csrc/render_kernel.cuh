@@ -39,6 +39,9 @@
 #ifndef MFA_VIEW_ORDER   // with MFA_VIEW_GROUP > 1: 1 = per supertile, 2 = per supertile row, 3 = per tile
 #define MFA_VIEW_ORDER 1
 #endif
+#ifndef MFA_TF_PAIR   // the TF lerp as paired FP32 instructions
+#define MFA_TF_PAIR 0   // measured neutral on C5 (56.7 either way): the lerp is off the critical path
+#endif
 #ifndef MFA_PRED_ADV   // experiment: the sample advance as a predicated add instead of a select
 #define MFA_PRED_ADV 0
 #endif
@@ -697,10 +700,20 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
             tf_pos(val, i0, wt);
             MFA_DCHECK(i0 >= 0 && i0 + 1 < args.tf_n);
             const float4 T0 = s_tf[i0], T1 = s_tf[i0 + 1];
+#if MFA_TF_PAIR   // the same lerps as paired FP32 (FADD2 / FFMA2): bit-identical, half the instructions
+            const float2 w2 = make_float2(wt, wt);
+            const float2 rg = __ffma2_rn(w2, __fadd2_rn(make_float2(T1.x, T1.y), make_float2(-T0.x, -T0.y)),
+                                         make_float2(T0.x, T0.y));
+            const float2 ba = __ffma2_rn(w2, __fadd2_rn(make_float2(T1.z, T1.w), make_float2(-T0.z, -T0.w)),
+                                         make_float2(T0.z, T0.w));
+            float cr = rg.x, cg = rg.y, cb = ba.x;
+            float a = ba.y;
+#else
             float cr = fmaf(wt, T1.x - T0.x, T0.x);
             float cg = fmaf(wt, T1.y - T0.y, T0.y);
             float cb = fmaf(wt, T1.z - T0.z, T0.z);
             float a = fmaf(wt, T1.w - T0.w, T0.w);
+#endif
             if constexpr (EXT) {   // curvature TF: bilinear in (kappa_1, kappa_2), modulates colour and opacity
                 if (args.curv.n > 0) {
                     const float x = fminf(fmaxf((k1 + args.curv.range) * args.curv.scale, 0.f), (float)(args.curv.n - 1));
