@@ -199,11 +199,19 @@ __global__ void __launch_bounds__(kCellThreads) eval_cells_kernel(const __grid_c
             int key = 0;
             if (b < args.nbins) {   // the point's cell in its bin (points outside [0,1]^3 sit in bin nbins)
                 const float q[3] = {r.x, r.y, r.z};
+                int c[3];
 #pragma unroll
-                for (int i = 0; i < 3; ++i) {   // u fastest (grouped Bezier layout: w fastest, the group axis)
-                    const int d = LAYOUT == kBezierG ? i : 2 - i;
-                    const int c = (int)((q[d] * (float)args.nb[d] - (float)bc[d]) * (float)kCellSub);
-                    key = key * kCellSub + min(max(c, 0), kCellSub - 1);
+                for (int d = 0; d < 3; ++d)
+                    c[d] = min(max((int)((q[d] * (float)args.nb[d] - (float)bc[d]) * (float)kCellSub), 0), kCellSub - 1);
+                if constexpr (LAYOUT == kBezierG) {
+                    // cells of one block group (the layout's 4-block group) consecutive, so
+                    // neighbouring lanes read the same 128-byte lines
+                    const int hi = (((c[2] >> kGLw) * (kCellSub >> kGLv) + (c[1] >> kGLv)) * (kCellSub >> kGLu)) + (c[0] >> kGLu);
+                    const int lo = ((c[2] & ((1 << kGLw) - 1)) << (kGLv + kGLu)) | ((c[1] & ((1 << kGLv) - 1)) << kGLu) |
+                                   (c[0] & ((1 << kGLu) - 1));
+                    key = (hi << 2) | lo;
+                } else {   // u fastest
+                    key = (c[2] * kCellSub + c[1]) * kCellSub + c[0];
                 }
             }
             s_key[j] = (unsigned short)key;
