@@ -76,3 +76,13 @@ def test_synchronous_validation_of_next_entry_points():
     assert st == 1
     assert L.mfa_ipc_open(None, None) == 1 and b"NULL" in L.mfa_last_error()
     assert L.mfa_ipc_close(None) == 1
+
+
+def test_layout_constants_match_binding():
+    """The binding's layout names map to the header's MFA_LAYOUT_* values
+    (including the grouped Bezier blocks, MFA_LAYOUT_BEZIER_GROUPED)."""
+    from paper_2204_11762_b200 import _lib
+    src = open(os.path.join(ROOT, "include", "mfa.h")).read()
+    hdr = {m.group(1).lower(): int(m.group(2)) for m in re.finditer(r"#define MFA_LAYOUT_(\w+) (\d+)", src)}
+    assert hdr == _lib.LAYOUTS
+    assert hdr["bezier_grouped"] == 4

@@ -595,6 +595,16 @@ def test_transparent_skip_in_tiled_scatter_path():
     assert torch.equal(img, full)
 
 
+def test_grouped_bezier_layout_needs_degree_3():
+    """MFA_LAYOUT_BEZIER_GROUPED is built for p = 3 only: other degrees are
+    refused (MFA_ERR_UNSUPPORTED); AUTO keeps linear blocks at p = 2."""
+    from paper_2204_11762_b200 import MfaError, Model
+    w = workload(1)
+    with pytest.raises(MfaError, match="UNSUPPORTED"):
+        Model.from_workload(w, layout="bezier_grouped")
+    assert Model.from_workload(w).info()["layout"] == "bezier"
+
+
 @pytest.mark.parametrize("layout", ["auto", "quads", "bricks", "bezier", "bezier_grouped"])
 def test_model_info_footprint(layout):
     """mfa_model_info reports the grid bytes, the device bytes of the chosen
