@@ -108,7 +108,7 @@ mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3],
  *   its 4 blocks), so neighbouring rays that reload vertically adjacent blocks
  *   in one instruction share cache lines (render +4 % on C5).  Random-point
  *   mfa_eval_batch / mfa_eval_hessian on models far larger than L2 are faster
- *   on MFA_LAYOUT_BEZIER (C5: 10.5 vs 7.3 G points/s); results are identical.
+ *   on MFA_LAYOUT_BEZIER (C5: 10.4 vs 8.0 G points/s); results are identical.
  *   Device memory as MFA_LAYOUT_BEZIER with S_w rounded up to a multiple of 4.
  */
 #define MFA_LAYOUT_AUTO 0
