@@ -106,7 +106,7 @@ mfa_status mfa_model_create(const int32_t degree[3], const int64_t nctrl[3],
  *   Bezier blocks at p = 3): the same blocks, 4 consecutive w-spans per
  *   1 KB group interleaved by 32-byte sector (line j of a group = sector j of
  *   its 4 blocks), so neighbouring rays that reload vertically adjacent blocks
- *   in one instruction share cache lines (render +8 % on C5).  Random-point
+ *   in one instruction share cache lines (render +6 % on C5).  Random-point
  *   mfa_eval_batch / mfa_eval_hessian on models far larger than L2 are faster
  *   on MFA_LAYOUT_BEZIER (C5: 10.4 vs 8.0 G points/s); results are identical.
  *   Device memory as MFA_LAYOUT_BEZIER with S_w rounded up to a multiple of 4.

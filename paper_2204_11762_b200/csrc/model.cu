@@ -551,7 +551,7 @@ extern "C" mfa_status mfa_model_create_ex(const int32_t degree[3], const int64_t
     if (bez && p > 3) return cleanup(fail(MFA_ERR_UNSUPPORTED, "Bezier-block layout needs degree <= 3"));
     if (want_layout == MFA_LAYOUT_BEZIER_GROUPED && p != 3)
         return cleanup(fail(MFA_ERR_UNSUPPORTED, "grouped Bezier layout needs degree 3"));
-    // AUTO takes the grouped blocks at p = 3 (C5 render +8 %, bit-identical)
+    // AUTO takes the grouped blocks at p = 3 (C5 render +6 %, bit-identical)
     const bool grouped = bez && p == 3 && want_layout != MFA_LAYOUT_BEZIER;
     if (want_layout == MFA_LAYOUT_BRICKS && p > 3)
         return cleanup(fail(MFA_ERR_UNSUPPORTED, "plain-brick layout needs degree <= 3"));
