@@ -536,6 +536,27 @@ __device__ __forceinline__ void nu_cross_d(const AxisArgs& A, int d, NUAxis& st)
 }
 #endif
 
+#if MFA_NU_SHIFTCMP && MFA_NU_UCMP && MFA_NU_TMAGIC
+// The multi-span step in two pieces for the render's deferred fixup
+// (MFA_MULTI_DEFER): nu_search moves st to the span that contains F by a
+// search over the knots (needed only when a step crossed more than one span,
+// i.e. (unsigned)nu_offset(F) >= wsh after nu_cross); nu_t converts the span
+// offset d = nu_offset(A, F, st) to the local coordinate, exactly as nu_finish.
+__device__ __forceinline__ void nu_search(const AxisArgs& A, long long F, NUAxis& st) {
+    int s = st.s;
+    while (s + 1 < A.nsp && F >= __ldg(A.kfx + s + 1)) ++s;
+    while (s > 0 && F < __ldg(A.kfx + s)) --s;
+    st.s = s;
+    nu_load(A, st);
+}
+
+__device__ __forceinline__ float nu_t(const AxisArgs& A, int d, const NUAxis& st) {
+    unsigned bits;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(bits) : "r"(max(d, 0)), "r"(0x7fffff), "r"(A.dmagic));
+    return (__uint_as_float(bits) - A.dbias) * st.invh;
+}
+#endif
+
 template <bool MULTI = true>
 __device__ __forceinline__ float nu_finish(const AxisArgs& A, long long F, NUAxis& st) {
     // rare: crossed more than one span this step; impossible when every span is

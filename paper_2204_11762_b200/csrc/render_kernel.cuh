@@ -39,6 +39,15 @@
 #ifndef MFA_VIEW_ORDER   // with MFA_VIEW_GROUP > 1: 1 = per supertile, 2 = per supertile row, 3 = per tile
 #define MFA_VIEW_ORDER 1
 #endif
+#ifndef MFA_MULTI_DEFER   // multi-span steps fixed behind one warp-uniform vote (see flat_loop)
+#define MFA_MULTI_DEFER 1
+#endif
+#ifndef MFA_DIAG_MULTICOUNT
+#define MFA_DIAG_MULTICOUNT 0
+#endif
+#ifndef MFA_DIAG_NOMULTI   // diagnostic only (wrong where a step crosses several spans): never run the multi-span loop
+#define MFA_DIAG_NOMULTI 0
+#endif
 #ifndef MFA_TF_PAIR   // the TF lerp as paired FP32 instructions
 #define MFA_TF_PAIR 0   // measured neutral on C5 (56.7 either way): the lerp is off the critical path
 #endif
@@ -324,6 +333,9 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
     constexpr int kST = MFA_SUPERTILE, kST2 = MFA_SUPERTILE * MFA_SUPERTILE;
     const int per_view = args.st_x * args.st_y * kST2;   // units are ordered by supertiles of tiles
     unsigned long long my_samples = 0;
+#if MFA_DIAG_MULTICOUNT   // diagnostic: lane-samples / warp-iterations with a multi-span step (samples[1..3])
+    unsigned long long dm_lane = 0, dm_warp = 0, dm_iters = 0;
+#endif
 #if MFA_LANE_STATS
     unsigned long long lane_slots = 0, lane_live = 0;
 #endif
@@ -884,6 +896,45 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
             while (__any_sync(0xffffffffu, live)) {
                 int s[3];
                 float t[3], gs1[3];
+#if MFA_DIAG_MULTICOUNT
+                int s_before[3];
+                if constexpr (!UNI) {
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) s_before[i] = nu[i].s;
+                }
+#endif
+#if MFA_MULTI_DEFER
+                if constexpr (!UNI && decltype(multi_tag)::value) {
+                    // the straight-line single-crossing tracker, and the rare step that
+                    // crossed more than one span (0.2 % of C5's lane-samples, 1.8 % of its
+                    // warp-iterations) fixed behind one warp-uniform vote instead of a
+                    // divergent search branch per axis in the common path
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) nu_cross(args.ax[i], F[i], nu[i]);
+                    int d[3];
+                    bool mh = false;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        d[i] = nu_offset(args.ax[i], F[i], nu[i]);
+                        mh |= (unsigned)d[i] >= (unsigned)nu[i].wsh;
+                    }
+                    if (__any_sync(0xffffffffu, mh)) {
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            if ((unsigned)d[i] >= (unsigned)nu[i].wsh) {
+                                nu_search(args.ax[i], F[i], nu[i]);
+                                d[i] = nu_offset(args.ax[i], F[i], nu[i]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        t[i] = nu_t(args.ax[i], d[i], nu[i]);
+                        s[i] = nu[i].s;
+                        gs1[i] = nu_gscale(args.ax[i], nu[i]);
+                    }
+                } else
+#endif
 #if MFA_EARLY_LOAD
                 if constexpr (kEarlyNU) {
                     constexpr bool MULTI = decltype(multi_tag)::value;
@@ -899,6 +950,17 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 #endif
                 locate(s, t, gs1, multi_tag);
                 const bool tr_next = transparent(s);
+#if MFA_DIAG_MULTICOUNT
+                if constexpr (!UNI) {
+                    bool mh = false;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) mh |= abs(s[i] - s_before[i]) > 1;
+                    mh = mh && live;
+                    dm_lane += mh ? 1 : 0;
+                    if (__any_sync(0xffffffffu, mh) && lane == 0) ++dm_warp;
+                    if (lane == 0) ++dm_iters;
+                }
+#endif
 #if MFA_BULK_PF
                 if constexpr (kPF) {
                     const int e = (s[2] * args.bg.S1 + s[1]) * args.bg.S0 + s[0];
@@ -1019,7 +1081,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
             }
         };
         if constexpr (kFlat) {
-            if (!UNI && (args.ax[0].multi | args.ax[1].multi | args.ax[2].multi))   // launch-uniform
+            if (!MFA_DIAG_NOMULTI && !UNI && (args.ax[0].multi | args.ax[1].multi | args.ax[2].multi))   // launch-uniform
                 flat_loop(std::true_type{});
             else
                 flat_loop(std::false_type{});
@@ -1096,6 +1158,14 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, o);
         if (lane == 0 && my_samples) atomicAdd(args.samples, my_samples);
+#if MFA_DIAG_MULTICOUNT
+        for (int o = 16; o > 0; o >>= 1) dm_lane += __shfl_xor_sync(0xffffffffu, dm_lane, o);
+        if (lane == 0) {
+            atomicAdd(args.samples + 1, dm_lane);
+            atomicAdd(args.samples + 2, dm_warp);
+            atomicAdd(args.samples + 3, dm_iters);
+        }
+#endif
 #if MFA_LANE_STATS
         if (lane == 0) {
             atomicAdd(args.samples + 1, lane_slots);
