@@ -40,7 +40,7 @@
 #define MFA_VIEW_ORDER 1
 #endif
 #ifndef MFA_MULTI_DEFER   // multi-span steps fixed behind one warp-uniform vote (see flat_loop)
-#define MFA_MULTI_DEFER 1
+#define MFA_MULTI_DEFER 2   // 2: and the block fetched before the span records arrive (C5 58.9 -> 61.4 G)
 #endif
 #ifndef MFA_DIAG_MULTICOUNT
 #define MFA_DIAG_MULTICOUNT 0
@@ -49,7 +49,7 @@
 #define MFA_DIAG_NOMULTI 0
 #endif
 #ifndef MFA_TF_PAIR   // the TF lerp as paired FP32 instructions
-#define MFA_TF_PAIR 0   // measured neutral on C5 (56.7 either way): the lerp is off the critical path
+#define MFA_TF_PAIR 1   // C5 +0.35 % with the deferred multi-span loop (neutral before it)
 #endif
 #ifndef MFA_PRED_ADV   // experiment: the sample advance as a predicated add instead of a select
 #define MFA_PRED_ADV 0
@@ -883,6 +883,9 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         // position is frozen (no reloads) and its compositing weight is 0.
         // Iteration k composites sample k and queries sample min(k+1, K-1).
         auto flat_loop = [&](auto multi_tag) {
+            // MFA_MULTI_DEFER == 2: the block load issued from the single-step span
+            // triple before the span records arrive (refetched in the rare fixup)
+            constexpr bool kFetchEarly = MFA_MULTI_DEFER == 2 && SHADE != 3 && !UNI;
 #if MFA_EARLY_LOAD
             constexpr bool kEarly = BEZ && SHADE != 3;
             constexpr bool kEarlyNU = kEarly && !UNI;
@@ -911,6 +914,11 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                     // divergent search branch per axis in the common path
 #pragma unroll
                     for (int i = 0; i < 3; ++i) nu_cross(args.ax[i], F[i], nu[i]);
+                    if constexpr (kFetchEarly) {   // the block of the single-step span triple, before the records arrive
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) s[i] = nu[i].s;
+                        fetch(s);
+                    }
                     int d[3];
                     bool mh = false;
 #pragma unroll
@@ -925,6 +933,12 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                                 nu_search(args.ax[i], F[i], nu[i]);
                                 d[i] = nu_offset(args.ax[i], F[i], nu[i]);
                             }
+                        }
+                        if constexpr (kFetchEarly) {   // lanes whose span triple moved refetch
+                            int s2[3];
+#pragma unroll
+                            for (int i = 0; i < 3; ++i) s2[i] = nu[i].s;
+                            fetch(s2);
                         }
                     }
 #pragma unroll
@@ -1006,7 +1020,9 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                     }
                 } else
 #endif
-                if (!tr_next) fetch(s);
+                if (!kFetchEarly || UNI || !decltype(multi_tag)::value) {
+                    if (!tr_next) fetch(s);
+                }
 #if MFA_PREFETCH_NEXT
                 if constexpr (LAYOUT == kBezier && !UNI) {   // linear blocks only
                     // predict the span triple of the sample after this one from the
@@ -1045,8 +1061,9 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                 tr_cur = tr_next;
                 const bool adv = live && k + 2 < K;
 #pragma unroll
+                for (int i = 0; i < 3; ++i) gs[i] = gs1[i];
+#pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    gs[i] = gs1[i];
 #if MFA_PRED_ADV
                     if (adv) F[i] += DF[i];   // predicated 64-bit add
 #else
