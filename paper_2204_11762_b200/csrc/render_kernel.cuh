@@ -885,7 +885,9 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         auto flat_loop = [&](auto multi_tag) {
             // MFA_MULTI_DEFER == 2: the block load issued from the single-step span
             // triple before the span records arrive (refetched in the rare fixup)
-            constexpr bool kFetchEarly = MFA_MULTI_DEFER == 2 && SHADE != 3 && !UNI;
+            constexpr bool kFetchEarly = MFA_MULTI_DEFER >= 2 && SHADE != 3 && !UNI;
+            // MFA_MULTI_DEFER == 3: and the previous sample shaded before the vote
+            constexpr bool kShadeEarly = MFA_MULTI_DEFER == 3 && SHADE != 3 && !UNI;
 #if MFA_EARLY_LOAD
             constexpr bool kEarly = BEZ && SHADE != 3;
             constexpr bool kEarlyNU = kEarly && !UNI;
@@ -918,6 +920,10 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
 #pragma unroll
                         for (int i = 0; i < 3; ++i) s[i] = nu[i].s;
                         fetch(s);
+                    }
+                    if constexpr (kShadeEarly) {   // the previous sample's shading overlaps the record loads
+                        comp_on = live && !tr_cur;
+                        shade_composite(val, gu, gv, gw, gs, 0.f, 0.f);
                     }
                     int d[3];
                     bool mh = false;
@@ -1052,8 +1058,10 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                     }
                 }
 #endif
-                comp_on = live && !tr_cur;   // a transparent sample composites with weight 0
-                shade_composite(val, gu, gv, gw, gs, 0.f, 0.f);
+                if (!kShadeEarly || UNI || !decltype(multi_tag)::value) {
+                    comp_on = live && !tr_cur;   // a transparent sample composites with weight 0
+                    shade_composite(val, gu, gv, gw, gs, 0.f, 0.f);
+                }
 #if MFA_ORDER
                 t[0] = fmaf(order_dep, 0.f, t[0]);   // exact: t[0] + 0 (A is finite)
 #endif
