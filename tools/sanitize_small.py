@@ -13,7 +13,7 @@ from paper_2204_11762_b200 import Model, unpack_tiles, workloads as WL
 
 for c, kw in ((1, {}), (2, dict(width=96, height=64)), (5, dict(width=64, height=48, n_views=2))):
     w = WL.make_config(c, **kw)
-    for layout in ("quads", "bezier", "bricks"):
+    for layout in ("quads", "bezier", "bricks") + (("bezier_grouped",) if w.degree == 3 else ()):
         m = Model.from_workload(w, layout=layout)
         u, v, ww = (torch.from_numpy(x).cuda() for x in WL.query_points(c, 4096))
         m.eval(u, v, ww)
@@ -35,7 +35,7 @@ for c, kw in ((1, {}), (2, dict(width=96, height=64)), (5, dict(width=64, height
 from paper_2204_11762_b200 import encode_grid, fit_grid, image_quality  # noqa: E402
 
 w = WL.make_config(2, width=96, height=64)
-for layout in ("quads", "bezier"):
+for layout in ("quads", "bezier", "bezier_grouped"):
     m = Model.from_workload(w, layout=layout)
     u, v, ww = (torch.from_numpy(x).cuda() for x in WL.query_points(2, 1 << 16))
     m.eval(u, v, ww, binned=True)
