@@ -885,7 +885,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         auto flat_loop = [&](auto multi_tag) {
             // MFA_MULTI_DEFER == 2: the block load issued from the single-step span
             // triple before the span records arrive (refetched in the rare fixup)
-            constexpr bool kFetchEarly = MFA_MULTI_DEFER >= 2 && SHADE != 3 && !UNI;
+            constexpr bool kFetchEarly = MFA_MULTI_DEFER >= 2 && !UNI;
             // MFA_MULTI_DEFER == 3: and the previous sample shaded before the vote
             constexpr bool kShadeEarly = MFA_MULTI_DEFER == 3 && SHADE != 3 && !UNI;
 #if MFA_EARLY_LOAD
@@ -919,7 +919,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                     if constexpr (kFetchEarly) {   // the block of the single-step span triple, before the records arrive
 #pragma unroll
                         for (int i = 0; i < 3; ++i) s[i] = nu[i].s;
-                        fetch(s);
+                        if (!transparent(s)) fetch(s);   // (SHADE == 3: transparent blocks are not fetched)
                     }
                     if constexpr (kShadeEarly) {   // the previous sample's shading overlaps the record loads
                         comp_on = live && !tr_cur;
@@ -944,7 +944,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
                             int s2[3];
 #pragma unroll
                             for (int i = 0; i < 3; ++i) s2[i] = nu[i].s;
-                            fetch(s2);
+                            if (!transparent(s2)) fetch(s2);
                         }
                     }
 #pragma unroll
