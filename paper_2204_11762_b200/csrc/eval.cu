@@ -166,17 +166,80 @@ __global__ void __launch_bounds__(256, MFA_EVAL_MINB) eval_kernel(const __grid_c
 #ifndef MFA_EVAL_CELLS      // 1: binned Bezier eval sorts each bin into cells in shared memory
 #define MFA_EVAL_CELLS 1
 #endif
+#ifndef MFA_EVAL_CELLS_QUADS   // experiment: the cell sort on the quad layouts too (C3 13.8 vs 14.2 G points/s: off)
+#define MFA_EVAL_CELLS_QUADS 0
+#endif
 constexpr int kCellSub = 8;                        // cells per bin edge
 constexpr int kCells = kCellSub * kCellSub * kCellSub;
+#ifndef MFA_CELL_THREADS
+#define MFA_CELL_THREADS 128
+#endif
 constexpr int kCellCap = 1024;                     // points per shared-memory piece
-constexpr int kCellThreads = 128;
+constexpr int kCellThreads = MFA_CELL_THREADS;
+
+// Quad layout (p = 3, 32-byte row-pair entries, 4 u-neighbours per 128-byte
+// line): an LDG.256 is served by the L1 data pipe in groups of 4 lanes, one
+// wavefront per distinct 128-byte line in a group (tools/ubench: 2 lanes per
+// line 16 wavefronts per warp, 4 lanes per line 8).  So the cell key is the
+// point's line group (span w, span v, span u / 4) and each key gets whole
+// 4-lane slots: the 4 lanes of a slot read the same line on all 8 row-pair
+// loads.  Idle lanes of a partly filled slot skip the evaluation.
+// Measured (C3, 2^24 points; tools/gpu_ab_lines.sh): global L1 wavefronts
+// 109 M -> 84 M against the plain cell sort, but 1.57x the instructions (idle
+// slot lanes, the span key, a second scan) and 2x the shared-memory
+// wavefronts: 12.6 vs 13.9 G points/s for the unsorted-bin kernel, so it is
+// off (kept as a measured experiment).
+#ifndef MFA_EVAL_LINES
+#define MFA_EVAL_LINES 0
+#endif
+constexpr int kLaneCap = 4 * kCellCap;             // worst case: one point per slot
+
+template <int P, int LAYOUT>
+constexpr bool eval_lines() { return MFA_EVAL_LINES && LAYOUT == kQuads && P == 3; }
+
+// exclusive scan of kCells counts in place (f applied to each count first);
+// returns the total.  All threads of the CTA call it.
+template <typename F>
+__device__ __forceinline__ unsigned cells_scan(unsigned* a, unsigned* wsum, F f) {
+    constexpr int E = kCells / kCellThreads;
+    unsigned c[E], tsum = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        c[e] = f(a[threadIdx.x * E + e]);
+        tsum += c[e];
+    }
+    unsigned x = tsum;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    unsigned run = x - tsum, total = 0;
+    for (int w = 0; w < kCellThreads / 32; ++w) {
+        if (w < wid) run += wsum[w];
+        total += wsum[w];
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        a[threadIdx.x * E + e] = run;
+        run += c[e];
+    }
+    __syncthreads();
+    return total;
+}
 
 template <int P, int LAYOUT, bool UNI, bool GRAD>
 __global__ void __launch_bounds__(kCellThreads) eval_cells_kernel(const __grid_constant__ EvalArgs args) {
+    constexpr bool LINES = eval_lines<P, LAYOUT>();
     __shared__ float4 s_rec[kCellCap];
     __shared__ unsigned short s_ord[kCellCap];
     __shared__ unsigned short s_key[kCellCap];
     __shared__ unsigned s_hist[kCells];
+    __shared__ unsigned s_kstart[LINES ? kCells : 1];
+    __shared__ unsigned s_slot[LINES ? kCells : 1];
+    __shared__ unsigned short s_lane[LINES ? kLaneCap : 1];
     __shared__ unsigned s_wsum[kCellThreads / 32];
     const int b = blockIdx.x;
     const unsigned cnt = __ldg(args.bin_cnt + b);
@@ -187,6 +250,16 @@ __global__ void __launch_bounds__(kCellThreads) eval_cells_kernel(const __grid_c
         bc[0] = b % args.nb[0];
         bc[1] = (b / args.nb[0]) % args.nb[1];
         bc[2] = b / (args.nb[0] * args.nb[1]);
+    }
+    int s0[3] = {0, 0, 0};   // LINES: spans of the bin's lower corner
+    if constexpr (LINES) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const float q0 = (float)bc[d] / (float)args.nb[d];
+            float t, h;
+            if (UNI) uni_span_f32(q0, args.ax[d].S, args.ax[d].nsp, s0[d], t);
+            else nonuni_span_f32(args.ax[d], q0, s0[d], t, h);
+        }
     }
     unsigned errs = 0;
     for (unsigned piece = 0; piece < cnt; piece += kCellCap) {
@@ -200,9 +273,21 @@ __global__ void __launch_bounds__(kCellThreads) eval_cells_kernel(const __grid_c
             if (b < args.nbins) {   // the point's cell in its bin (points outside [0,1]^3 sit in bin nbins)
                 const float q[3] = {r.x, r.y, r.z};
                 int c[3];
+                if constexpr (LINES) {   // line group: (span w, span v, span u / 4) relative to the bin corner
 #pragma unroll
-                for (int d = 0; d < 3; ++d)
-                    c[d] = min(max((int)((q[d] * (float)args.nb[d] - (float)bc[d]) * (float)kCellSub), 0), kCellSub - 1);
+                    for (int d = 0; d < 3; ++d) {
+                        int sd;
+                        float t, h;
+                        if (UNI) uni_span_f32(q[d], args.ax[d].S, args.ax[d].nsp, sd, t);
+                        else nonuni_span_f32(args.ax[d], q[d], sd, t, h);
+                        c[d] = d == 0 ? (sd >> 2) - (s0[0] >> 2) : sd - s0[d];
+                        c[d] = min(max(c[d], 0), kCellSub - 1);
+                    }
+                } else {
+#pragma unroll
+                    for (int d = 0; d < 3; ++d)
+                        c[d] = min(max((int)((q[d] * (float)args.nb[d] - (float)bc[d]) * (float)kCellSub), 0), kCellSub - 1);
+                }
                 if constexpr (LAYOUT == kBezierG) {
                     // cells of one block group (the layout's 4-block group) consecutive, so
                     // neighbouring lanes read the same 128-byte lines
@@ -218,35 +303,28 @@ __global__ void __launch_bounds__(kCellThreads) eval_cells_kernel(const __grid_c
             atomicAdd(s_hist + key, 1u);
         }
         __syncthreads();
-        {   // exclusive scan of the kCells counts (kCells / kCellThreads per thread)
-            constexpr int E = kCells / kCellThreads;
-            unsigned c[E], tsum = 0;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                c[e] = s_hist[threadIdx.x * E + e];
-                tsum += c[e];
-            }
-            unsigned x = tsum;
-            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (lane == 31) s_wsum[wid] = x;
+        int lanes = m;
+        if constexpr (LINES) {
+            for (int c = threadIdx.x; c < kCells; c += kCellThreads) s_slot[c] = s_hist[c];
             __syncthreads();
-            unsigned run = x - tsum;
-            for (int w = 0; w < wid; ++w) run += s_wsum[w];
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                s_hist[threadIdx.x * E + e] = run;
-                run += c[e];
-            }
+            lanes = 4 * (int)cells_scan(s_slot, s_wsum, [](unsigned x) { return (x + 3u) >> 2; });
+            for (int j = threadIdx.x; j < lanes; j += kCellThreads) s_lane[j] = 0xffff;
+        }
+        cells_scan(s_hist, s_wsum, [](unsigned x) { return x; });
+        if constexpr (LINES) {
+            for (int c = threadIdx.x; c < kCells; c += kCellThreads) s_kstart[c] = s_hist[c];
+            __syncthreads();
+        }
+        for (int j = threadIdx.x; j < m; j += kCellThreads) {
+            const int key = s_key[j];
+            const unsigned pos = atomicAdd(s_hist + key, 1u);
+            if constexpr (LINES) s_lane[4 * s_slot[key] + (pos - s_kstart[key])] = (unsigned short)j;
+            else s_ord[pos] = (unsigned short)j;
         }
         __syncthreads();
-        for (int j = threadIdx.x; j < m; j += kCellThreads) s_ord[atomicAdd(s_hist + s_key[j], 1u)] = (unsigned short)j;
-        __syncthreads();
-        for (int j = threadIdx.x; j < m; j += kCellThreads) {
-            const int li = s_ord[j];
+        for (int j = threadIdx.x; j < lanes; j += kCellThreads) {
+            const int li = LINES ? (int)s_lane[j] : (int)s_ord[j];
+            if (LINES && li == 0xffff) continue;
             const float4 r = s_rec[li];
             const float q[3] = {r.x, r.y, r.z};
             float val, gu, gv, gw;
@@ -274,7 +352,7 @@ static cudaError_t launch_eval_s(const EvalArgs& a, cudaStream_t st) {
 
 template <int P, int LAYOUT, bool UNI, bool GRAD>
 static cudaError_t launch_eval_t(const EvalArgs& a, cudaStream_t st) {
-    if (is_bez(LAYOUT) && a.rec && a.bin_cnt) {
+    if ((is_bez(LAYOUT) || eval_lines<P, LAYOUT>() || (MFA_EVAL_CELLS_QUADS && LAYOUT == kQuads)) && a.rec && a.bin_cnt) {
         eval_cells_kernel<P, LAYOUT, UNI, GRAD><<<(unsigned)(a.nbins + 1), kCellThreads, 0, st>>>(a);
         return cudaGetLastError();
     }

@@ -58,13 +58,18 @@ def test_eval_parity(c):
     print(f"C{c}: n={len(u)} worst value {wv:.2e} sigma, worst gradient {wg:.2e} sigma")
 
 
-@pytest.mark.parametrize("c,layout", [(3, "auto"), (5, "auto"), (5, "quads"), (2, "auto")])
-def test_eval_binned_equals_direct(c, layout):
+@pytest.mark.parametrize("c,layout,n,box", [(3, "auto", 1 << 18, 1.0), (5, "auto", 1 << 18, 1.0),
+                                             (5, "quads", 1 << 18, 1.0), (2, "auto", 1 << 18, 1.0),
+                                             (3, "auto", 1 << 22, 0.25)])
+def test_eval_binned_equals_direct(c, layout, n, box):
     """The three eval paths return identical outputs, NaN rows and domain-error
     counts: mfa_eval_batch (binned, stream-ordered scratch), mfa_eval_batch_ws
-    with a caller workspace (binned) and without one (the unbinned kernel)."""
+    with a caller workspace (binned) and without one (the unbinned kernel).
+    (3, 2^22 points in [0, 1/4]^3): ~8192 points per bin, so the binned p = 3
+    quad kernel (line-group slots, eval.cu) takes its bins in several
+    shared-memory pieces."""
     m = gpu_model(c, layout)
-    u, v, w = WL.query_points(c, 1 << 18)
+    u, v, w = (a * np.float32(box) for a in WL.query_points(c, n))
     u = u.copy()
     u[[5, 77, 1000]] = [1.5, np.nan, -0.25]
     cu, cv, cw = cuda(u), cuda(v), cuda(w)
