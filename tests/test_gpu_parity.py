@@ -65,9 +65,9 @@ def test_eval_binned_equals_direct(c, layout, n, box):
     """The three eval paths return identical outputs, NaN rows and domain-error
     counts: mfa_eval_batch (binned, stream-ordered scratch), mfa_eval_batch_ws
     with a caller workspace (binned) and without one (the unbinned kernel).
-    (3, 2^22 points in [0, 1/4]^3): ~8192 points per bin, so the binned p = 3
-    quad kernel (line-group slots, eval.cu) takes its bins in several
-    shared-memory pieces."""
+    (3, 2^22 points in [0, 1/4]^3): ~8192 points per bin (dense bins; with
+    MFA_EVAL_LINES=1 the line-slot kernel takes them in several shared-memory
+    pieces, which passed when that experiment was measured)."""
     m = gpu_model(c, layout)
     u, v, w = (a * np.float32(box) for a in WL.query_points(c, n))
     u = u.copy()
