@@ -33,6 +33,9 @@
 #ifndef MFA_UNIT_SHAPE   // lanes of a warp unit: 0 = 8x4 pixels, 1 = 4x8 (C5 +0.8 %, C4 +3 %), 2 = 16x2, 3 = 2x16
 #define MFA_UNIT_SHAPE 1
 #endif
+#ifndef MFA_QUAD_LANES   // 1: on the grouped Bezier layout, 8 x 4 units whose 4-lane groups are 2 x 2 pixel quads
+#define MFA_QUAD_LANES 1
+#endif
 #ifndef MFA_VIEW_GROUP   // full-frame work order: >1 interleaves groups of orbit-adjacent views
 #define MFA_VIEW_GROUP 4 // C5: DRAM per launch 506 -> 343 GB, L2 hit 44 -> 56 %, +1.4 %
 #endif
@@ -426,19 +429,36 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
         // compute_frame; uniform across the warp, no shared memory)
         const ViewFrame& fr = args.frames[view];
 #endif
-#if MFA_UNIT_SHAPE == 1   // 4 x 8 pixels per warp unit
-        const int lx = (sub & 3) * 4 + (lane & 3);
-        const int ly = (sub >> 2) * 8 + (lane >> 2);
-#elif MFA_UNIT_SHAPE == 2   // 16 x 2
-        const int lx = lane & 15;
-        const int ly = sub * 2 + (lane >> 4);
-#elif MFA_UNIT_SHAPE == 3   // 2 x 16
-        const int lx = sub * 2 + (lane & 1);
-        const int ly = lane >> 1;
-#else                       // 8 x 4
-        const int lx = (sub & 1) * 8 + (lane & 7);
-        const int ly = (sub >> 1) * 4 + (lane >> 3);
-#endif
+        // MFA_UNIT_SHAPE; on the grouped Bezier layout the unit is 8 x 4 pixels
+        // with its aligned 4-lane groups as 2 x 2 pixel quads (the L1 data pipe
+        // serves an LDG.256 in groups of 4 lanes, one wavefront per distinct
+        // 128-byte line in a group): C5 61.45 -> 62.2 G samples/s (4 x 8 with
+        // quads: 61.69), images bit-identical; the quad layout keeps 4 x 8 with
+        // 4 x 1 rows (quads there: C3 -2.5 %)
+        constexpr int kShape = (MFA_UNIT_SHAPE == 1 && MFA_QUAD_LANES && LAYOUT == kBezierG) ? 5 : MFA_UNIT_SHAPE;
+        int lx, ly;
+        if constexpr (kShape == 1) {          // 4 x 8 pixels per warp unit, 4-lane groups 4 x 1
+            lx = (sub & 3) * 4 + (lane & 3);
+            ly = (sub >> 2) * 8 + (lane >> 2);
+        } else if constexpr (kShape == 4) {   // 4 x 8, 4-lane groups 2 x 2 (experiment)
+            lx = (sub & 3) * 4 + ((lane >> 2) & 1) * 2 + (lane & 1);
+            ly = (sub >> 2) * 8 + (lane >> 3) * 2 + ((lane >> 1) & 1);
+        } else if constexpr (kShape == 5) {   // 8 x 4, 4-lane groups 2 x 2 (grouped Bezier default)
+            lx = (sub & 1) * 8 + ((lane >> 2) & 3) * 2 + (lane & 1);
+            ly = (sub >> 1) * 4 + (lane >> 4) * 2 + ((lane >> 1) & 1);
+        } else if constexpr (kShape == 6) {   // 16 x 2, 4-lane groups 2 x 2 (experiment)
+            lx = (lane >> 2) * 2 + (lane & 1);
+            ly = sub * 2 + ((lane >> 1) & 1);
+        } else if constexpr (kShape == 2) {   // 16 x 2
+            lx = lane & 15;
+            ly = sub * 2 + (lane >> 4);
+        } else if constexpr (kShape == 3) {   // 2 x 16
+            lx = sub * 2 + (lane & 1);
+            ly = lane >> 1;
+        } else {                              // 8 x 4
+            lx = (sub & 1) * 8 + (lane & 7);
+            ly = (sub >> 1) * 4 + (lane >> 3);
+        }
         const int px = tx * MFA_TILE + lx, py = ty * MFA_TILE + ly;
         const bool valid = px < args.W && py < args.H;
 
