@@ -792,7 +792,9 @@ def run_all_configs(args):
     from paper_2204_11762_b200 import Model, roofline as RL, workloads as WL
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream()
-    runs = [(c, None) for c in (1, 2, 3, 4, 5)] + [(1, 64), (2, 64)]   # + small frames batched 64 per launch
+    runs = [(c, None) for c in (1, 2, 3, 4, 5)] + [(1, 64), (2, 64), (3, 64), (4, 16)]   # + short frames batched per launch
+    if os.environ.get("MFA_BENCH_RUNS"):   # diagnostics: "3:2,3:4" = C3 at 2 and 4 views per launch
+        runs = [(int(a), int(b) or None) for a, b in (x.split(":") for x in os.environ["MFA_BENCH_RUNS"].split(","))]
     for c, nv in runs:
         w = WL.make_config(c, n_views=nv) if nv else WL.make_config(c)
         m = Model.from_workload(w, layout=args.layout)
@@ -834,8 +836,8 @@ def run_all_configs(args):
             "data": "synthetic (seeded generator of the BASELINE.json config recipe; no dataset)",
             "config": {"workload": w.name + (f" x{nv} views per launch" if nv else ""), "views": V, "width": W,
                        "height": H, "degree": w.degree,
-                       "batch": (None if not nv else ("64 copies of the same orthographic view" if c == 1 else
-                                                      "64 seeded orbit views of the config's camera model")),
+                       "batch": (None if not nv else (f"{nv} copies of the same orthographic view" if c == 1 else
+                                                      f"{nv} seeded orbit views of the config's camera model")),
                        "layout": info["layout"], "launches_per_step": reps * ((V + 63) // 64),
                        "model_bytes": info["model_bytes"], "device_bytes": info["device_bytes"],
                        "footprint_ratio": info["device_bytes"] / info["model_bytes"], "create_ms": info["create_ms"]},
