@@ -421,7 +421,7 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
             const unsigned st = t / kST2, lt = t % kST2;
 #endif
             unsigned sty = st / (unsigned)args.st_x;
-            const unsigned stx = st - sty * (unsigned)args.st_x;
+            unsigned stx = st - sty * (unsigned)args.st_x;
 #if MFA_CENTER_OUT
             // single-view launches (short: C2 0.18 ms, C3 0.87 ms): supertile rows
             // from the image centre outward (mid, mid-1, mid+1, ...), so the
@@ -430,6 +430,10 @@ __global__ void MFA_RENDER_BOUNDS render_kernel(const __grid_constant__ RenderAr
             if (args.n_views == 1) {
                 const unsigned mid = (unsigned)args.st_y >> 1, h = (sty + 1u) >> 1;
                 sty = (sty & 1u) ? mid - h : mid + h;
+#if MFA_CENTER_OUT == 2   // columns too: each row's corners last
+                const unsigned midx = (unsigned)args.st_x >> 1, hx = (stx + 1u) >> 1;
+                stx = (stx & 1u) ? midx - hx : midx + hx;
+#endif
             }
 #endif
             tx = (int)(stx * kST + lt % kST);
