@@ -37,11 +37,14 @@ MUTATIONS = [
     ("K6", "backward span crossings step forward (non-uniform tracker)", KC,
      "st.s = max(st.s + ((d >> 31) | 1), 0);", "st.s = max(st.s + 1, 0);", "render or subset or image"),
     ("K7", "eval gradient not scaled to parameter space", EV,
-     "store(val, gu * sc[0], gv * sc[1], gw * sc[2]);", "store(val, gu, gv * sc[1], gw * sc[2]);", "eval"),
+     "        gu *= sc[0];", "        gu *= 1.f;", "eval"),
     ("K8", "eval v-derivative basis at u's local coordinate (Bezier)", EV,
      "bernstein<P, true>(t[1], Bv);", "bernstein<P, true>(t[0], Bv);", "eval"),
     ("K9", "cubic Bernstein derivative of B_1 with the wrong sign", KC,
      "fmaf(ts3, -2.f, -d0)", "fmaf(ts3, 2.f, -d0)", "eval or render"),
+    ("K10", "quad-lane warp unit: the x bit of a 2 x 2 quad taken from lane bit 1 (rows and columns of a quad swapped)", RK,
+     "lx = (sub & 1) * 8 + ((lane >> 2) & 3) * 2 + (lane & 1);", "lx = (sub & 1) * 8 + ((lane >> 2) & 3) * 2 + ((lane >> 1) & 1);",
+     "render or subset or image"),
 ]
 
 
